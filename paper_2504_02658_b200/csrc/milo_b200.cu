@@ -1,0 +1,891 @@
+// C-ABI implementation (include/milo_b200.h): handle management, reference-
+// order validation, workspace planning and kernel launches.  Host C++.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/milo_b200.h"
+#include "gemv.cuh"
+#include "kernels.cuh"
+#include "moe.cuh"
+
+using namespace milo_dev;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local uint64_t g_launches = 0;
+
+milo_status fail(milo_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+#define CUDA_TRY(expr)                                                                   \
+  do {                                                                                   \
+    cudaError_t e__ = (expr);                                                            \
+    if (e__ != cudaSuccess)                                                              \
+      return fail(MILO_ERR_CUDA, "%s failed: %s", #expr, cudaGetErrorString(e__));      \
+  } while (0)
+
+struct DeviceProps {
+  int sms = 0;
+  int major = 0;
+  bool ok = false;
+};
+
+DeviceProps device_props() {
+  static std::mutex mu;
+  static DeviceProps cache[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return {};
+  std::lock_guard<std::mutex> lock(mu);
+  DeviceProps& p = cache[dev];
+  if (!p.ok) {
+    cudaDeviceGetAttribute(&p.sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&p.major, cudaDevAttrComputeCapabilityMajor, dev);
+    p.ok = p.sms > 0;
+    // Per-call workspaces come from the stream-ordered pool; keep freed
+    // blocks cached instead of returning them to the driver at every sync.
+    cudaMemPool_t pool;
+    if (p.ok && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t threshold = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
+    }
+  }
+  return p;
+}
+
+template <typename K>
+cudaError_t set_smem(K kernel, int bytes) {
+  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+// Launch with programmatic dependent launch allowed (the kernel itself calls
+// griddepcontrol.wait before touching the previous grid's outputs).
+template <typename... KArgs, typename... Args>
+cudaError_t launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                   cudaStream_t stream, bool pdl, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  ++g_launches;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
+// Bump allocator over one stream-ordered allocation.
+struct Arena {
+  size_t size = 0;
+  size_t take(size_t bytes) {
+    size_t off = (size + 255) & ~size_t(255);
+    size = off + bytes;
+    return off;
+  }
+};
+
+bool tile_allowed(int tk, int tn) {
+  return (tk == 64 && tn == 256) || (tk == 128 && tn == 128) || (tk == 256 && tn == 64);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// handles
+// ---------------------------------------------------------------------------
+struct milo_weight {
+  uint64_t rows = 0, cols = 0;
+  int32_t mode = 1;
+  uint64_t group_size = 64;
+  bool has_zeros = false;
+  uint8_t* tiles = nullptr;  // macro-tile layout (null when the layout is not representable)
+  uint64_t bytes = 0;
+};
+
+struct milo_comp {
+  uint64_t rows = 0, cols = 0, rank = 0;
+  int32_t storage = 1;
+  uint64_t group_size = 64;
+  void* mem = nullptr;
+  uint8_t* ucodes = nullptr;  // k x rank
+  float* uscales = nullptr;   // k x gpr
+  uint8_t* vcodes = nullptr;  // n x rank (qVt)
+  float* vscales = nullptr;   // n x gpr
+  float* ureal = nullptr;     // k x rank
+  float* vreal = nullptr;     // n x rank (V^T)
+  int32_t gpr = 0;
+};
+
+extern "C" {
+
+const char* milo_last_error(void) { return g_err.c_str(); }
+int milo_abi_version(void) { return MILO_B200_ABI_VERSION; }
+uint64_t milo_launch_count(void) { return g_launches; }
+
+const char* milo_status_name(milo_status s) {
+  switch (s) {
+    case MILO_OK: return "ok";
+    case MILO_ERR_FORMAT: return "format";
+    case MILO_ERR_DATA: return "data";
+    case MILO_ERR_IO: return "io";
+    case MILO_ERR_SHAPE: return "shape";
+    case MILO_ERR_RANK: return "rank";
+    case MILO_ERR_NUMERIC: return "numeric";
+    case MILO_ERR_STAT: return "stat";
+    case MILO_ERR_PLAN: return "plan";
+    case MILO_ERR_RANGE: return "range";
+    case MILO_ERR_CONFIG: return "config";
+    case MILO_ERR_CUDA: return "cuda";
+    case MILO_ERR_ARGUMENT: return "argument";
+  }
+  return "unknown";
+}
+
+milo_status milo_device_check(void) {
+  DeviceProps p = device_props();
+  if (!p.ok) return fail(MILO_ERR_CUDA, "no CUDA device");
+  if (p.major != 10) return fail(MILO_ERR_CUDA, "device is sm_%d0, this library is sm_100a only", p.major);
+  cudaFuncAttributes fa;
+  CUDA_TRY(cudaFuncGetAttributes(&fa, gemv_w3a16_kernel<2, 1>));
+  return MILO_OK;
+}
+
+milo_status milo_weight_create(const milo_packed_desc* d, milo_weight** out) {
+  if (!d || !out) return fail(MILO_ERR_ARGUMENT, "null argument");
+  *out = nullptr;
+  // PackedInt3Matrix invariants (pack.cpp:72-76, pack.hpp:47-58).
+  if (d->rows == 0 || d->cols == 0) return fail(MILO_ERR_SHAPE, "cannot pack an empty matrix");
+  if (d->cols % 32 != 0) return fail(MILO_ERR_SHAPE, "cols %llu not a multiple of 32", (unsigned long long)d->cols);
+  if (d->group_size == 0 || (d->rows * d->cols) % d->group_size != 0)
+    return fail(MILO_ERR_SHAPE, "group_size does not divide rows*cols");
+  if (d->layout != 0 && d->layout != 1) return fail(MILO_ERR_FORMAT, "unknown layout %d", d->layout);
+  if (d->mode != 0 && d->mode != 1) return fail(MILO_ERR_FORMAT, "unknown mode %d", d->mode);
+  if (d->layout == 1 && (d->rows % 16 != 0 || d->cols % 64 != 0))
+    return fail(MILO_ERR_SHAPE, "tiled layout needs rows %% 16 == 0 and cols %% 64 == 0");
+  const uint64_t groups = d->rows * d->cols / 32;
+  const uint64_t qg = d->rows * d->cols / d->group_size;
+  if (d->split) {
+    if (!d->plane_a || !d->plane_b || d->n_plane_a != groups * 2 || d->n_plane_b != groups)
+      return fail(MILO_ERR_FORMAT, "split planes must hold %llu + %llu words",
+                  (unsigned long long)(groups * 2), (unsigned long long)groups);
+  } else if (!d->words || d->n_words != groups * 3) {
+    return fail(MILO_ERR_FORMAT, "words must hold %llu words", (unsigned long long)(groups * 3));
+  }
+  if (!d->scales || d->n_scales != qg) return fail(MILO_ERR_FORMAT, "scales must hold %llu values", (unsigned long long)qg);
+  if (d->zeros && d->n_zeros != qg && d->n_zeros != 0)
+    return fail(MILO_ERR_FORMAT, "zeros must hold %llu values or be empty", (unsigned long long)qg);
+  DeviceProps props = device_props();
+  if (!props.ok) return fail(MILO_ERR_CUDA, "no CUDA device");
+
+  auto* w = new milo_weight();
+  w->rows = d->rows;
+  w->cols = d->cols;
+  w->mode = d->mode;
+  w->group_size = d->group_size;
+  w->has_zeros = d->zeros != nullptr && d->n_zeros == qg;
+  const bool representable = d->group_size == 64 && d->rows % 32 == 0 && d->cols % 64 == 0 &&
+                             (d->mode == 0 || w->has_zeros);
+  if (!representable) {  // gemm_w3a16 rejects these inputs (gemm.cpp:121-134)
+    *out = w;
+    return MILO_OK;
+  }
+  w->bytes = d->rows * d->cols / 2048 * kTileBytes;
+  const size_t word_bytes = groups * 3 * 4, meta_bytes = qg * 2;
+  void* staging = nullptr;
+  cudaError_t e = cudaMalloc(&w->tiles, w->bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&staging, word_bytes + 2 * meta_bytes + 64);
+  if (e != cudaSuccess) {
+    cudaFree(w->tiles);
+    delete w;
+    return fail(MILO_ERR_CUDA, "cudaMalloc failed: %s", cudaGetErrorString(e));
+  }
+  uint8_t* st = static_cast<uint8_t*>(staging);
+  uint32_t* dwords = reinterpret_cast<uint32_t*>(st);
+  uint16_t* dscales = reinterpret_cast<uint16_t*>(st + word_bytes);
+  uint16_t* dzeros = reinterpret_cast<uint16_t*>(st + word_bytes + meta_bytes);
+  RefStream rs{};
+  rs.rows = d->rows;
+  rs.cols = d->cols;
+  rs.layout = d->layout;
+  rs.split = d->split;
+  if (d->split) {
+    e = cudaMemcpy(dwords, d->plane_a, groups * 8, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(dwords + groups * 2, d->plane_b, groups * 4, cudaMemcpyHostToDevice);
+    rs.plane_a = dwords;
+    rs.plane_b = dwords + groups * 2;
+  } else {
+    e = cudaMemcpy(dwords, d->words, word_bytes, cudaMemcpyHostToDevice);
+    rs.words = dwords;
+  }
+  if (e == cudaSuccess) e = cudaMemcpy(dscales, d->scales, meta_bytes, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && w->has_zeros) e = cudaMemcpy(dzeros, d->zeros, meta_bytes, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    const uint64_t threads = (d->rows * d->cols / 2048) * 32;
+    ++g_launches;
+    repack_codes_kernel<<<(unsigned)((threads + 255) / 256), 256>>>(rs, w->tiles, d->rows, d->cols);
+    const uint64_t mthreads = d->rows * (d->cols / 64);
+    ++g_launches;
+    repack_meta_kernel<<<(unsigned)((mthreads + 255) / 256), 256>>>(dscales, dzeros, d->mode, w->tiles,
+                                                                   d->rows, d->cols);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  cudaFree(staging);
+  if (e != cudaSuccess) {
+    cudaFree(w->tiles);
+    delete w;
+    return fail(MILO_ERR_CUDA, "repack failed: %s", cudaGetErrorString(e));
+  }
+  *out = w;
+  return MILO_OK;
+}
+
+milo_status milo_weight_destroy(milo_weight* w) {
+  if (!w) return MILO_OK;
+  if (w->tiles) cudaFree(w->tiles);
+  delete w;
+  return MILO_OK;
+}
+
+milo_status milo_weight_info(const milo_weight* w, uint64_t* rows, uint64_t* cols, int32_t* mode,
+                             uint64_t* device_bytes) {
+  if (!w) return fail(MILO_ERR_ARGUMENT, "null weight");
+  if (rows) *rows = w->rows;
+  if (cols) *cols = w->cols;
+  if (mode) *mode = w->mode;
+  if (device_bytes) *device_bytes = w->bytes;
+  return MILO_OK;
+}
+
+static milo_status unpack_common(const milo_weight* w, int what, int mode, void* out, void* stream) {
+  if (!w || !out) return fail(MILO_ERR_ARGUMENT, "null argument");
+  if (what == 1 && mode == 1 && !w->has_zeros)
+    return fail(MILO_ERR_CONFIG, "asymmetric de-quantization needs zero-points");
+  if (!w->tiles)
+    return fail(MILO_ERR_CONFIG, "device layout needs group_size 64, rows %% 32 == 0, cols %% 64 == 0");
+  if (what == 1 && mode != w->mode)
+    return fail(MILO_ERR_CONFIG, "device de-quantization uses the weight's own mode");
+  const uint64_t threads = (w->rows * w->cols / 2048) * 32;
+  ++g_launches;
+  unpack_tiles_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      w->tiles, w->rows, w->cols, w->mode, what, out);
+  CUDA_TRY(cudaGetLastError());
+  return MILO_OK;
+}
+
+milo_status milo_unpack_codes(const milo_weight* w, uint8_t* out, void* stream) {
+  return unpack_common(w, 0, w ? w->mode : 0, out, stream);
+}
+
+milo_status milo_dequant_half(const milo_weight* w, int32_t mode, uint16_t* out, void* stream) {
+  return unpack_common(w, 1, mode, out, stream);
+}
+
+milo_status milo_comp_create(const milo_comp_desc* d, milo_comp** out) {
+  if (!d || !out) return fail(MILO_ERR_ARGUMENT, "null argument");
+  *out = nullptr;
+  auto* c = new milo_comp();
+  c->rows = d->rows;
+  c->cols = d->cols;
+  c->rank = d->rank;
+  c->storage = d->storage;
+  c->group_size = d->group_size;
+  if (d->rank == 0) {
+    *out = c;
+    return MILO_OK;
+  }
+  if (d->storage == 1 && d->group_size != 64) {
+    delete c;
+    return fail(MILO_ERR_CONFIG, "device compensator needs symm-int3 group_size 64");
+  }
+  const uint64_t k = d->rows, n = d->cols, r = d->rank;
+  c->gpr = (int32_t)((r + 63) / 64);
+  Arena ar;
+  size_t o_uc = 0, o_us = 0, o_vc = 0, o_vs = 0, o_ur = 0, o_vr = 0;
+  if (d->storage == 1) {
+    if (!d->qu_codes || !d->qu_scales || !d->qvt_codes || !d->qvt_scales) {
+      delete c;
+      return fail(MILO_ERR_ARGUMENT, "symm-int3 compensator arrays missing");
+    }
+    o_uc = ar.take(k * r);
+    o_us = ar.take(k * c->gpr * 4);
+    o_vc = ar.take(n * r);
+    o_vs = ar.take(n * c->gpr * 4);
+  } else {
+    if (!d->U || !d->V) {
+      delete c;
+      return fail(MILO_ERR_ARGUMENT, "real compensator factors missing");
+    }
+    o_ur = ar.take(k * r * 4);
+    o_vr = ar.take(n * r * 4);
+  }
+  cudaError_t e = cudaMalloc(&c->mem, ar.size);
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(MILO_ERR_CUDA, "cudaMalloc failed: %s", cudaGetErrorString(e));
+  }
+  uint8_t* base = static_cast<uint8_t*>(c->mem);
+  if (d->storage == 1) {
+    c->ucodes = base + o_uc;
+    c->uscales = reinterpret_cast<float*>(base + o_us);
+    c->vcodes = base + o_vc;
+    c->vscales = reinterpret_cast<float*>(base + o_vs);
+    e = cudaMemcpy(c->ucodes, d->qu_codes, k * r, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(c->uscales, d->qu_scales, k * c->gpr * 4, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(c->vcodes, d->qvt_codes, n * r, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(c->vscales, d->qvt_scales, n * c->gpr * 4, cudaMemcpyHostToDevice);
+  } else {
+    c->ureal = reinterpret_cast<float*>(base + o_ur);
+    c->vreal = reinterpret_cast<float*>(base + o_vr);
+    std::vector<float> vt(n * r);
+    for (uint64_t j = 0; j < n; ++j)
+      for (uint64_t q = 0; q < r; ++q) vt[j * r + q] = d->V[q * n + j];
+    e = cudaMemcpy(c->ureal, d->U, k * r * 4, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(c->vreal, vt.data(), n * r * 4, cudaMemcpyHostToDevice);
+  }
+  if (e != cudaSuccess) {
+    cudaFree(c->mem);
+    delete c;
+    return fail(MILO_ERR_CUDA, "upload failed: %s", cudaGetErrorString(e));
+  }
+  *out = c;
+  return MILO_OK;
+}
+
+milo_status milo_comp_destroy(milo_comp* c) {
+  if (!c) return MILO_OK;
+  if (c->mem) cudaFree(c->mem);
+  delete c;
+  return MILO_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// GEMM
+// ---------------------------------------------------------------------------
+namespace {
+
+void fill_comp(GemvProblem& p, int mat, const milo_comp* c) {
+  if (!c || c->rank == 0) return;
+  p.rank[mat] = (int32_t)c->rank;
+  p.vgpr[mat] = c->gpr;
+  p.vcodes[mat] = c->vcodes;
+  p.vscales[mat] = c->vscales;
+  p.vreal[mat] = c->vreal;
+  p.ucodes[mat] = c->ucodes;
+  p.uscales[mat] = c->uscales;
+  p.ureal[mat] = c->ureal;
+}
+
+template <int NT, int NMAT>
+milo_status launch_gemv(const GemvArgs& args, cudaStream_t stream, int sms, bool pdl) {
+  using SM = GemvSmem<NT, NMAT>;
+  static thread_local int configured_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured_dev != dev) {
+    CUDA_TRY(set_smem(gemv_w3a16_kernel<NT, NMAT>, SM::kBytes));
+    configured_dev = dev;
+  }
+  CUDA_TRY(launch(gemv_w3a16_kernel<NT, NMAT>, dim3(sms), dim3(32 * (1 + kConsumerWarps)),
+                  SM::kBytes, stream, pdl, args));
+  return MILO_OK;
+}
+
+milo_status validate_gemm(const milo_weight* w, const milo_comp* comp, const milo_gemm_config* cfg,
+                          int64_t a_cols) {
+  // GemmConfig::validate (gemm.cpp:23-30) then gemm.cpp:120-139, in order.
+  if (!tile_allowed(cfg->tile_k, cfg->tile_n))
+    return fail(MILO_ERR_CONFIG, "tile shape (%d, %d) not in {(64,256),(128,128),(256,64)}",
+                cfg->tile_k, cfg->tile_n);
+  if (cfg->group_size != 64) return fail(MILO_ERR_CONFIG, "group size must be 64");
+  if (cfg->pipeline_depth < 1) return fail(MILO_ERR_CONFIG, "pipeline depth must be >= 1");
+  if (w->group_size != 64) return fail(MILO_ERR_CONFIG, "packed weight group size must be 64");
+  if (cfg->mode != w->mode) return fail(MILO_ERR_CONFIG, "config mode does not match the packed weight's mode");
+  if (cfg->mode == 1 && !w->has_zeros) return fail(MILO_ERR_CONFIG, "asymmetric mode needs zero-points");
+  if (w->rows % (uint64_t)cfg->tile_k != 0 || w->cols % (uint64_t)cfg->tile_n != 0)
+    return fail(MILO_ERR_SHAPE, "(k, n) = (%llu, %llu) not a multiple of tile shape (%d, %d)",
+                (unsigned long long)w->rows, (unsigned long long)w->cols, cfg->tile_k, cfg->tile_n);
+  if ((uint64_t)a_cols != w->rows)
+    return fail(MILO_ERR_SHAPE, "A has %lld cols, expected k = %llu", (long long)a_cols,
+                (unsigned long long)w->rows);
+  if (comp && (comp->rows != w->rows || comp->cols != w->cols))
+    return fail(MILO_ERR_SHAPE, "compensator shape does not match the weight");
+  if (!w->tiles) return fail(MILO_ERR_CONFIG, "weight has no device layout");
+  return MILO_OK;
+}
+
+}  // namespace
+
+extern "C" milo_status milo_gemm_w3a16(const milo_weight* w, const milo_comp* comp,
+                                       const milo_gemm_config* cfg, const void* A, int64_t m,
+                                       int64_t a_cols, int32_t a_dtype, void* C, int32_t c_dtype,
+                                       void* stream_) {
+  if (!w || !cfg) return fail(MILO_ERR_ARGUMENT, "null argument");
+  milo_status st = validate_gemm(w, comp, cfg, a_cols);
+  if (st != MILO_OK) return st;
+  if (m < 0) return fail(MILO_ERR_SHAPE, "negative row count");
+  if (m == 0) return MILO_OK;
+  if (!A || !C) return fail(MILO_ERR_ARGUMENT, "null A or C");
+  if ((a_dtype != 0 && a_dtype != 1) || (c_dtype != 0 && c_dtype != 1))
+    return fail(MILO_ERR_ARGUMENT, "unsupported dtype");
+  DeviceProps props = device_props();
+  if (!props.ok || props.major != 10) return fail(MILO_ERR_CUDA, "no sm_100 device");
+  cudaStream_t stream = (cudaStream_t)stream_;
+
+  const int nt = m <= 8 ? 1 : 2;
+  const int m_pad = 8 * nt;
+  const int64_t k = (int64_t)w->rows, n = (int64_t)w->cols;
+  const int rank = (comp && comp->rank > 0) ? (int)comp->rank : 0;
+  int64_t done = 0;
+  while (done < m) {
+    const int64_t mm = std::min<int64_t>(m - done, (int64_t)(kMaxProblems - 1) * m_pad);
+    const int blocks = (int)((mm + m_pad - 1) / m_pad);
+    const int chunks = (int)std::max<int64_t>(1, std::min<int64_t>(16, k / 512));
+    Arena ar;
+    const int64_t act_block_words = (k / 32) * m_pad * 16;
+    const size_t o_act = ar.take((size_t)blocks * act_block_words * 4);
+    const size_t o_prob = ar.take((size_t)blocks * sizeof(GemvProblem));
+    const size_t o_np = ar.take(4);
+    const size_t o_t = ar.take((size_t)blocks * m_pad * std::max(rank, 1) * 4);
+    const size_t o_part = ar.take((size_t)blocks * 2 * chunks * m_pad * std::max(rank, 1) * 4);
+    const size_t o_tc = ar.take((size_t)blocks * 2 * 4);
+    const size_t o_ws = ar.take((size_t)props.sms * 2 * m_pad * 64 * 4);
+    const int n_counters = (int)(blocks * (n / 64));
+    const size_t o_cnt = ar.take((size_t)n_counters * 4);
+    void* mem = nullptr;
+    CUDA_TRY(cudaMallocAsync(&mem, ar.size, stream));
+    uint8_t* base = static_cast<uint8_t*>(mem);
+
+    GemvProblem tmpl{};
+    tmpl.w[0] = w->tiles;
+    tmpl.k = (int32_t)k;
+    tmpl.n = (int32_t)n;
+    tmpl.mode = w->mode;
+    tmpl.kind = kStoreRows;
+    tmpl.out_dtype = c_dtype;
+    tmpl.ldo = n;
+    tmpl.out = c_dtype == 0 ? (void*)(static_cast<float*>(C) + done * n)
+                            : (void*)(static_cast<__half*>(C) + done * n);
+    if (rank > 0) {
+      fill_comp(tmpl, 0, comp);
+      tmpl.t[0] = reinterpret_cast<float*>(base + o_t);
+    }
+    LinearPrep lp{};
+    lp.A = a_dtype == 0 ? (const void*)(static_cast<const float*>(A) + done * a_cols)
+                        : (const void*)(static_cast<const __half*>(A) + done * a_cols);
+    lp.m = mm;
+    lp.k = k;
+    lp.lda = a_cols;
+    lp.a_dtype = a_dtype;
+    lp.m_pad = m_pad;
+    lp.n_blocks = blocks;
+    lp.act = reinterpret_cast<uint32_t*>(base + o_act);
+    lp.tmpl = tmpl;
+    lp.act_block_words = act_block_words;
+    lp.t_block_floats = (int64_t)m_pad * rank;
+    lp.out_block_elems = (int64_t)m_pad * n;
+    lp.problems = reinterpret_cast<GemvProblem*>(base + o_prob);
+    lp.n_problems = reinterpret_cast<int32_t*>(base + o_np);
+    lp.counters = reinterpret_cast<int32_t*>(base + o_cnt);
+    lp.n_counters = n_counters;
+    lp.t_counters = reinterpret_cast<int32_t*>(base + o_tc);
+    lp.n_t_counters = blocks * 2;
+    const int64_t prep_threads = (int64_t)blocks * m_pad * (k / 2);
+    const int prep_grid = (int)std::min<int64_t>((prep_threads + 255) / 256, props.sms * 8);
+    cudaError_t e = launch(prep_linear_kernel, dim3(prep_grid), dim3(256), 0, stream, false, lp);
+    if (e == cudaSuccess && rank > 0) {
+      LorcArgs la{};
+      la.problems = lp.problems;
+      la.n_problems = lp.n_problems;
+      la.partial = reinterpret_cast<float*>(base + o_part);
+      la.counters = lp.t_counters;
+      la.m_pad = m_pad;
+      la.chunks = chunks;
+      la.rank_max = rank;
+      e = launch(lorc_t_kernel, dim3(blocks * 2, chunks), dim3(32 * kLorcWarps), 0, stream, true, la);
+    }
+    if (e != cudaSuccess) {
+      cudaFreeAsync(mem, stream);
+      return fail(MILO_ERR_CUDA, "launch failed: %s", cudaGetErrorString(e));
+    }
+    GemvArgs ga{};
+    ga.problems = lp.problems;
+    ga.n_problems = lp.n_problems;
+    ga.ws = reinterpret_cast<float*>(base + o_ws);
+    ga.counters = lp.counters;
+    st = nt == 1 ? launch_gemv<1, 1>(ga, stream, props.sms, true)
+                 : launch_gemv<2, 1>(ga, stream, props.sms, true);
+    cudaFreeAsync(mem, stream);
+    if (st != MILO_OK) return st;
+    done += mm;
+  }
+  return MILO_OK;
+}
+
+extern "C" milo_status milo_gemm_w3a16_host(const milo_weight* w, const milo_comp* comp,
+                                            const milo_gemm_config* cfg, const float* A,
+                                            int64_t m, int64_t a_cols, float* C) {
+  if (!w || !cfg) return fail(MILO_ERR_ARGUMENT, "null argument");
+  milo_status st = validate_gemm(w, comp, cfg, a_cols);
+  if (st != MILO_OK) return st;
+  if (m <= 0) return m == 0 ? MILO_OK : fail(MILO_ERR_SHAPE, "negative row count");
+  cudaStream_t stream = nullptr;
+  void *dA = nullptr, *dC = nullptr;
+  const size_t abytes = (size_t)m * a_cols * 4, cbytes = (size_t)m * w->cols * 4;
+  CUDA_TRY(cudaMallocAsync(&dA, abytes, stream));
+  CUDA_TRY(cudaMallocAsync(&dC, cbytes, stream));
+  CUDA_TRY(cudaMemcpyAsync(dA, A, abytes, cudaMemcpyHostToDevice, stream));
+  st = milo_gemm_w3a16(w, comp, cfg, dA, m, a_cols, MILO_F32, dC, MILO_F32, stream);
+  if (st == MILO_OK) {
+    cudaError_t e = cudaMemcpyAsync(C, dC, cbytes, cudaMemcpyDeviceToHost, stream);
+    if (e != cudaSuccess) st = fail(MILO_ERR_CUDA, "copy back failed: %s", cudaGetErrorString(e));
+  }
+  cudaFreeAsync(dA, stream);
+  cudaFreeAsync(dC, stream);
+  cudaError_t e = cudaStreamSynchronize(stream);
+  if (st == MILO_OK && e != cudaSuccess) st = fail(MILO_ERR_CUDA, "%s", cudaGetErrorString(e));
+  return st;
+}
+
+// ---------------------------------------------------------------------------
+// MoE layer
+// ---------------------------------------------------------------------------
+struct milo_moe {
+  int32_t E = 0, n_shared = 0, K = 0, score_mode = 0;
+  int32_t d = 0, f_max = 0, rank1_max = 0, rank2_max = 0;
+  ExpertDev* dev_experts = nullptr;  // E + n_shared entries
+};
+
+extern "C" milo_status milo_moe_create(const milo_expert_desc* experts, int32_t n_experts,
+                                       const milo_expert_desc* shared, int32_t n_shared,
+                                       int32_t top_k, int32_t score_mode, milo_moe** out) {
+  if (!out) return fail(MILO_ERR_ARGUMENT, "null out");
+  *out = nullptr;
+  if (n_experts < 0 || n_shared < 0 || n_experts + n_shared <= 0 ||
+      n_experts + n_shared > kRouteMaxE)
+    return fail(MILO_ERR_CONFIG, "need 1..%d experts", kRouteMaxE);
+  if (n_experts > 0 && (top_k < 1 || top_k > 16 || top_k > n_experts))
+    return fail(MILO_ERR_CONFIG, "top_k must be in [1, min(16, n_experts)]");
+  if (score_mode != 0 && score_mode != 1) return fail(MILO_ERR_CONFIG, "unknown score mode");
+  std::vector<ExpertDev> host(n_experts + n_shared);
+  auto* moe = new milo_moe();
+  moe->E = n_experts;
+  moe->n_shared = n_shared;
+  moe->K = n_experts > 0 ? top_k : 0;
+  moe->score_mode = score_mode;
+  for (int i = 0; i < n_experts + n_shared; ++i) {
+    const milo_expert_desc& ex = i < n_experts ? experts[i] : shared[i - n_experts];
+    const milo_weight* w[3] = {ex.w1, ex.w3, ex.w2};
+    const milo_comp* c[3] = {ex.c1, ex.c3, ex.c2};
+    for (int j = 0; j < 3; ++j)
+      if (!w[j] || !w[j]->tiles) {
+        delete moe;
+        return fail(MILO_ERR_CONFIG, "expert %d matrix %d has no device layout", i, j);
+      }
+    const uint64_t d = w[0]->rows, f = w[0]->cols;
+    if (w[1]->rows != d || w[1]->cols != f || w[2]->rows != f || w[2]->cols != d) {
+      delete moe;
+      return fail(MILO_ERR_SHAPE, "expert %d: need w1,w3 d x f and w2 f x d", i);
+    }
+    if (moe->d == 0) moe->d = (int32_t)d;
+    if ((int32_t)d != moe->d) {
+      delete moe;
+      return fail(MILO_ERR_SHAPE, "expert %d: hidden size differs", i);
+    }
+    if (w[0]->mode != w[1]->mode) {
+      delete moe;
+      return fail(MILO_ERR_CONFIG, "expert %d: w1 and w3 modes differ", i);
+    }
+    ExpertDev& e = host[i];
+    e.f = (int32_t)f;
+    e.mode = w[0]->mode;
+    moe->f_max = std::max(moe->f_max, (int32_t)f);
+    for (int j = 0; j < 3; ++j) {
+      e.w[j] = w[j]->tiles;
+      if (j == 2 && w[2]->mode != w[0]->mode) {
+        delete moe;
+        return fail(MILO_ERR_CONFIG, "expert %d: w2 mode differs", i);
+      }
+      if (c[j] && c[j]->rank > 0) {
+        if (c[j]->rows != w[j]->rows || c[j]->cols != w[j]->cols) {
+          delete moe;
+          return fail(MILO_ERR_SHAPE, "expert %d: compensator %d shape mismatch", i, j);
+        }
+        e.rank[j] = (int32_t)c[j]->rank;
+        e.gpr[j] = c[j]->gpr;
+        e.ucodes[j] = c[j]->ucodes;
+        e.uscales[j] = c[j]->uscales;
+        e.ureal[j] = c[j]->ureal;
+        e.vcodes[j] = c[j]->vcodes;
+        e.vscales[j] = c[j]->vscales;
+        e.vreal[j] = c[j]->vreal;
+        if (j < 2) moe->rank1_max = std::max(moe->rank1_max, e.rank[j]);
+        else moe->rank2_max = std::max(moe->rank2_max, e.rank[j]);
+      }
+    }
+  }
+  cudaError_t err = cudaMalloc(&moe->dev_experts, host.size() * sizeof(ExpertDev));
+  if (err == cudaSuccess)
+    err = cudaMemcpy(moe->dev_experts, host.data(), host.size() * sizeof(ExpertDev),
+                     cudaMemcpyHostToDevice);
+  if (err != cudaSuccess) {
+    cudaFree(moe->dev_experts);
+    delete moe;
+    return fail(MILO_ERR_CUDA, "expert table upload failed: %s", cudaGetErrorString(err));
+  }
+  *out = moe;
+  return MILO_OK;
+}
+
+extern "C" milo_status milo_moe_destroy(milo_moe* moe) {
+  if (!moe) return MILO_OK;
+  cudaFree(moe->dev_experts);
+  delete moe;
+  return MILO_OK;
+}
+
+extern "C" milo_status milo_router_topk(const float* logits, int64_t m, int32_t E, int32_t K,
+                                        int32_t score_mode, int32_t* ids, float* w,
+                                        void* stream) {
+  if (m < 0 || E < 1 || K < 1 || K > 16 || K > E) return fail(MILO_ERR_CONFIG, "bad router shape");
+  if (m == 0) return MILO_OK;
+  if (!logits || !ids || !w) return fail(MILO_ERR_ARGUMENT, "null argument");
+  const int warps = 8;
+  CUDA_TRY(launch(router_topk_kernel, dim3((unsigned)((m + warps - 1) / warps)), dim3(32 * warps),
+                  0, (cudaStream_t)stream, true, logits, m, E, K, score_mode, ids, w));
+  return MILO_OK;
+}
+
+namespace {
+
+template <int NT>
+milo_status moe_run(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype, const int32_t* ids,
+                    const float* wts, void* out, int32_t out_dtype, cudaStream_t stream,
+                    int sms) {
+  constexpr int m_pad = 8 * NT;
+  const int K = moe->K, E = moe->E, S = moe->n_shared;
+  const int64_t d = moe->d, f_max = moe->f_max;
+  const int64_t blocks_max = std::min<int64_t>(
+      kMaxProblems - 1, (m * K + m_pad - 1) / m_pad + std::min<int64_t>(E, m * K) +
+                            (int64_t)S * ((m + m_pad - 1) / m_pad));
+  const int chunks1 = (int)std::max<int64_t>(1, std::min<int64_t>(16, d / 512));
+  const int chunks2 = (int)std::max<int64_t>(1, std::min<int64_t>(16, f_max / 512));
+  const int r1 = std::max(moe->rank1_max, 1), r2 = std::max(moe->rank2_max, 1);
+  Arena ar;
+  const size_t o_elist = ar.take((size_t)(m * K + S * m + 1) * 4);
+  const size_t o_bexp = ar.take((size_t)blocks_max * 4);
+  const size_t o_bst = ar.take((size_t)blocks_max * 4);
+  const size_t o_p1 = ar.take((size_t)blocks_max * sizeof(GemvProblem));
+  const size_t o_p2 = ar.take((size_t)blocks_max * sizeof(GemvProblem));
+  const size_t o_np = ar.take(16);
+  const int64_t act_block = (d / 32) * m_pad * 64;
+  const int64_t h_block = (f_max / 32) * m_pad * 64;
+  const size_t o_act = ar.take((size_t)blocks_max * act_block);
+  const size_t o_h = ar.take((size_t)blocks_max * h_block);
+  const size_t o_t1 = ar.take((size_t)blocks_max * 2 * m_pad * r1 * 4);
+  const size_t o_t2 = ar.take((size_t)blocks_max * m_pad * r2 * 4);
+  const size_t o_pa1 = ar.take((size_t)blocks_max * 2 * chunks1 * m_pad * r1 * 4);
+  const size_t o_pa2 = ar.take((size_t)blocks_max * 2 * chunks2 * m_pad * r2 * 4);
+  const size_t o_ws = ar.take((size_t)sms * 2 * 2 * m_pad * 64 * 4);
+  const int64_t n_cnt1 = blocks_max * (f_max / 64), n_cnt2 = blocks_max * (d / 64);
+  const int64_t n_zero = n_cnt1 + n_cnt2 + 4 * blocks_max;
+  const size_t o_zero = ar.take((size_t)n_zero * 4);
+  const size_t o_Y = ar.take((size_t)(m * K + S * m) * d * 4);
+  void* mem = nullptr;
+  CUDA_TRY(cudaMallocAsync(&mem, ar.size, stream));
+  uint8_t* base = static_cast<uint8_t*>(mem);
+  int32_t* np = reinterpret_cast<int32_t*>(base + o_np);
+  int32_t* zero = reinterpret_cast<int32_t*>(base + o_zero);
+  int32_t* cnt1 = zero;
+  int32_t* cnt2 = zero + n_cnt1;
+  int32_t* tc1 = cnt2 + n_cnt2;
+  int32_t* tc2 = tc1 + 2 * blocks_max;
+
+  MoeRouteArgs ra{};
+  ra.ids = ids;
+  ra.m = m;
+  ra.K = K;
+  ra.E = E;
+  ra.n_shared = S;
+  ra.d = (int32_t)d;
+  ra.m_pad = m_pad;
+  ra.experts = moe->dev_experts;
+  ra.max_blocks = (int32_t)blocks_max;
+  ra.elist = reinterpret_cast<int32_t*>(base + o_elist);
+  ra.block_expert = reinterpret_cast<int32_t*>(base + o_bexp);
+  ra.block_start = reinterpret_cast<int32_t*>(base + o_bst);
+  ra.p1 = reinterpret_cast<GemvProblem*>(base + o_p1);
+  ra.p2 = reinterpret_cast<GemvProblem*>(base + o_p2);
+  ra.n_p1 = np;
+  ra.n_p2 = np + 1;
+  ra.n_blocks_out = np + 2;
+  ra.act_pool = base + o_act;
+  ra.h_pool = base + o_h;
+  ra.h_block_bytes = h_block;
+  ra.t1_pool = reinterpret_cast<float*>(base + o_t1);
+  ra.t2_pool = reinterpret_cast<float*>(base + o_t2);
+  ra.rank1_max = r1;
+  ra.rank2_max = r2;
+  ra.Y = reinterpret_cast<float*>(base + o_Y);
+  ra.zero_ptr = zero;
+  ra.zero_count = n_zero;
+  cudaError_t e = launch(moe_route_kernel, dim3(1), dim3(kRouteThreads), 0, stream, true, ra);
+  if (e == cudaSuccess)
+    e = launch(moe_gather_kernel, dim3((unsigned)blocks_max), dim3(256), 0, stream, true, x,
+               x_dtype, d, K, m, (const int32_t*)ra.elist, (const int32_t*)ra.block_start,
+               (const int32_t*)ra.block_expert, (const int32_t*)ra.n_p1, E, m_pad, ra.act_pool,
+               (const GemvProblem*)ra.p1);
+  if (e == cudaSuccess && moe->rank1_max > 0) {
+    LorcArgs la{};
+    la.problems = ra.p1;
+    la.n_problems = ra.n_p1;
+    la.partial = reinterpret_cast<float*>(base + o_pa1);
+    la.counters = tc1;
+    la.m_pad = m_pad;
+    la.chunks = chunks1;
+    la.rank_max = r1;
+    e = launch(lorc_t_kernel, dim3((unsigned)(blocks_max * 2), chunks1), dim3(32 * kLorcWarps), 0,
+               stream, true, la);
+  }
+  milo_status st = MILO_OK;
+  if (e != cudaSuccess) st = fail(MILO_ERR_CUDA, "launch failed: %s", cudaGetErrorString(e));
+  if (st == MILO_OK) {
+    GemvArgs ga{};
+    ga.problems = ra.p1;
+    ga.n_problems = ra.n_p1;
+    ga.ws = reinterpret_cast<float*>(base + o_ws);
+    ga.counters = cnt1;
+    st = launch_gemv<NT, 2>(ga, stream, sms, true);
+  }
+  if (st == MILO_OK && moe->rank2_max > 0) {
+    LorcArgs la{};
+    la.problems = ra.p2;
+    la.n_problems = ra.n_p2;
+    la.partial = reinterpret_cast<float*>(base + o_pa2);
+    la.counters = tc2;
+    la.m_pad = m_pad;
+    la.chunks = chunks2;
+    la.rank_max = r2;
+    e = launch(lorc_t_kernel, dim3((unsigned)(blocks_max * 2), chunks2), dim3(32 * kLorcWarps), 0,
+               stream, true, la);
+    if (e != cudaSuccess) st = fail(MILO_ERR_CUDA, "launch failed: %s", cudaGetErrorString(e));
+  }
+  if (st == MILO_OK) {
+    GemvArgs ga{};
+    ga.problems = ra.p2;
+    ga.n_problems = ra.n_p2;
+    ga.ws = reinterpret_cast<float*>(base + o_ws);
+    ga.counters = cnt2;
+    st = launch_gemv<NT, 1>(ga, stream, sms, true);
+  }
+  if (st == MILO_OK) {
+    const int64_t total = m * (d / 4);
+    const int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)sms * 8);
+    e = launch(moe_combine_kernel, dim3(grid), dim3(256), 0, stream, true,
+               (const float*)ra.Y, ids, wts, m, K, S, d, out, out_dtype);
+    if (e != cudaSuccess) st = fail(MILO_ERR_CUDA, "launch failed: %s", cudaGetErrorString(e));
+  }
+  cudaFreeAsync(mem, stream);
+  return st;
+}
+
+}  // namespace
+
+extern "C" milo_status milo_moe_forward_routed(milo_moe* moe, const void* x, int64_t m,
+                                               int32_t x_dtype, const int32_t* ids,
+                                               const float* wts, void* out, int32_t out_dtype,
+                                               void* stream_) {
+  if (!moe) return fail(MILO_ERR_ARGUMENT, "null moe");
+  if (m < 0) return fail(MILO_ERR_SHAPE, "negative token count");
+  if (m == 0) return MILO_OK;
+  if (!x || !out || (moe->K > 0 && (!ids || !wts))) return fail(MILO_ERR_ARGUMENT, "null argument");
+  if ((x_dtype != 0 && x_dtype != 1) || (out_dtype != 0 && out_dtype != 1))
+    return fail(MILO_ERR_ARGUMENT, "unsupported dtype");
+  DeviceProps props = device_props();
+  if (!props.ok || props.major != 10) return fail(MILO_ERR_CUDA, "no sm_100 device");
+  cudaStream_t stream = (cudaStream_t)stream_;
+  // Token chunks keep every launch under the problem-table bound.
+  const int nt = m <= 8 ? 1 : 2;
+  const int m_pad = 8 * nt;
+  const int64_t per_tok = std::max(1, moe->K) + moe->n_shared;
+  const int64_t chunk = std::max<int64_t>(
+      m_pad, ((int64_t)(kMaxProblems - 1 - moe->E - moe->n_shared) * m_pad) / per_tok / m_pad * m_pad);
+  for (int64_t t0 = 0; t0 < m; t0 += chunk) {
+    const int64_t mm = std::min(chunk, m - t0);
+    const size_t xs = x_dtype == 0 ? 4 : 2, os = out_dtype == 0 ? 4 : 2;
+    const void* xc = static_cast<const uint8_t*>(x) + t0 * moe->d * xs;
+    void* oc = static_cast<uint8_t*>(out) + t0 * moe->d * os;
+    const int32_t* ic = ids ? ids + t0 * moe->K : nullptr;
+    const float* wc = wts ? wts + t0 * moe->K : nullptr;
+    milo_status st = nt == 1 ? moe_run<1>(moe, xc, mm, x_dtype, ic, wc, oc, out_dtype, stream, props.sms)
+                             : moe_run<2>(moe, xc, mm, x_dtype, ic, wc, oc, out_dtype, stream, props.sms);
+    if (st != MILO_OK) return st;
+  }
+  return MILO_OK;
+}
+
+extern "C" milo_status milo_moe_forward(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype,
+                                        const float* logits, void* out, int32_t out_dtype,
+                                        int32_t* topk_ids, float* topk_w, void* stream_) {
+  if (!moe) return fail(MILO_ERR_ARGUMENT, "null moe");
+  if (m <= 0) return m == 0 ? MILO_OK : fail(MILO_ERR_SHAPE, "negative token count");
+  cudaStream_t stream = (cudaStream_t)stream_;
+  int32_t* ids = topk_ids;
+  float* w = topk_w;
+  void* mem = nullptr;
+  if (moe->K > 0 && (!ids || !w)) {
+    CUDA_TRY(cudaMallocAsync(&mem, (size_t)m * moe->K * 8, stream));
+    ids = static_cast<int32_t*>(mem);
+    w = reinterpret_cast<float*>(ids + m * moe->K);
+  }
+  milo_status st = MILO_OK;
+  if (moe->K > 0) st = milo_router_topk(logits, m, moe->E, moe->K, moe->score_mode, ids, w, stream);
+  if (st == MILO_OK) st = milo_moe_forward_routed(moe, x, m, x_dtype, ids, w, out, out_dtype, stream);
+  if (mem) cudaFreeAsync(mem, stream);
+  return st;
+}
+
+extern "C" milo_status milo_moe_forward_host(milo_moe* moe, const float* x, int64_t m,
+                                             const float* logits, float* out) {
+  if (!moe) return fail(MILO_ERR_ARGUMENT, "null moe");
+  if (m <= 0) return m == 0 ? MILO_OK : fail(MILO_ERR_SHAPE, "negative token count");
+  cudaStream_t stream = nullptr;
+  const size_t xb = (size_t)m * moe->d * 4, lb = (size_t)m * std::max(moe->E, 1) * 4;
+  void* mem = nullptr;
+  CUDA_TRY(cudaMallocAsync(&mem, 2 * xb + lb, stream));
+  uint8_t* b = static_cast<uint8_t*>(mem);
+  cudaError_t e = cudaMemcpyAsync(b, x, xb, cudaMemcpyHostToDevice, stream);
+  if (e == cudaSuccess && moe->E > 0)
+    e = cudaMemcpyAsync(b + xb, logits, (size_t)m * moe->E * 4, cudaMemcpyHostToDevice, stream);
+  milo_status st = e == cudaSuccess ? MILO_OK : fail(MILO_ERR_CUDA, "%s", cudaGetErrorString(e));
+  if (st == MILO_OK)
+    st = milo_moe_forward(moe, b, m, MILO_F32, reinterpret_cast<float*>(b + xb), b + xb + lb,
+                          MILO_F32, nullptr, nullptr, stream);
+  if (st == MILO_OK) {
+    e = cudaMemcpyAsync(out, b + xb + lb, xb, cudaMemcpyDeviceToHost, stream);
+    if (e != cudaSuccess) st = fail(MILO_ERR_CUDA, "%s", cudaGetErrorString(e));
+  }
+  cudaFreeAsync(mem, stream);
+  e = cudaStreamSynchronize(stream);
+  if (st == MILO_OK && e != cudaSuccess) st = fail(MILO_ERR_CUDA, "%s", cudaGetErrorString(e));
+  return st;
+}

@@ -1,0 +1,347 @@
+// MoE layer kernels (new: the reference has no MoE layer).
+//
+//   router_topk_kernel : top-k by descending fp32 logit (ties -> lower id),
+//                        softmax weights (Mixtral top-k renorm / DeepSeek all).
+//   moe_route_kernel   : one CTA; deterministic counting sort of the (token, k)
+//                        entries by expert (ascending token order inside an
+//                        expert, warp ballots + fixed-order warp scans), then
+//                        the two grouped-GEMM problem tables:
+//                          phase 1: per (expert, 16-token block) SwiGLU problem
+//                                   over w1|w3 -> h act tiles
+//                          phase 2: per block, w2 -> rows of the slot buffer Y
+//                        plus zeroed fix-up counters.
+//   moe_gather_kernel  : x rows of every block -> binary16 act tiles.
+//   moe_combine_kernel : out[t] = sum_k w[t,k] Y[t*K+k] (k order) + shared rows.
+#pragma once
+#include <cstdint>
+#include <cuda_fp16.h>
+
+#include "gemv.cuh"
+#include "layout.cuh"
+#include "ptx.cuh"
+
+namespace milo_dev {
+
+// ---------------------------------------------------------------------------
+// router
+// ---------------------------------------------------------------------------
+__global__ void router_topk_kernel(const float* __restrict__ logits, int64_t m, int E, int K,
+                                   int score_mode, int32_t* __restrict__ ids,
+                                   float* __restrict__ wts) {
+  const int warps = blockDim.x >> 5;
+  const int64_t t = (int64_t)blockIdx.x * warps + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (t >= m) return;
+  const float* l = logits + t * E;
+  int sel[16];
+  for (int k = 0; k < K; ++k) {
+    float best = -INFINITY;
+    int bid = 0x7fffffff;
+    for (int e = lane; e < E; e += 32) {
+      bool used = false;
+      for (int q = 0; q < k; ++q) used |= (sel[q] == e);
+      const float v = l[e];
+      if (!used && (v > best || (v == best && e < bid) || bid == 0x7fffffff)) {
+        best = v;
+        bid = e;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oid = __shfl_xor_sync(0xffffffffu, bid, o);
+      if (oid != 0x7fffffff && (bid == 0x7fffffff || ov > best || (ov == best && oid < bid))) {
+        best = ov;
+        bid = oid;
+      }
+    }
+    sel[k] = bid;
+  }
+  if (lane == 0) {
+    float w[16];
+    if (score_mode == 0) {
+      const float mx = l[sel[0]];
+      float sum = 0.0f;
+      for (int k = 0; k < K; ++k) {
+        w[k] = expf(l[sel[k]] - mx);
+        sum += w[k];
+      }
+      for (int k = 0; k < K; ++k) w[k] = w[k] / sum;
+    } else {
+      float mx = l[0];
+      for (int e = 1; e < E; ++e) mx = l[e] > mx ? l[e] : mx;
+      float sum = 0.0f;
+      for (int e = 0; e < E; ++e) sum += expf(l[e] - mx);
+      for (int k = 0; k < K; ++k) w[k] = expf(l[sel[k]] - mx) / sum;
+    }
+    for (int k = 0; k < K; ++k) {
+      ids[t * K + k] = sel[k];
+      wts[t * K + k] = w[k];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// routing -> problem tables
+// ---------------------------------------------------------------------------
+struct ExpertDev {
+  const uint8_t* w[3];       // w1, w3, w2 tiles
+  const uint8_t* ucodes[3];
+  const float* uscales[3];
+  const float* ureal[3];
+  const uint8_t* vcodes[3];
+  const float* vscales[3];
+  const float* vreal[3];
+  int32_t rank[3];
+  int32_t gpr[3];
+  int32_t f;                 // intermediate width of this expert
+  int32_t mode;
+};
+
+struct MoeRouteArgs {
+  const int32_t* ids;        // m x K (-1 = unused)
+  int64_t m;
+  int32_t K, E, n_shared;
+  int32_t d;
+  int32_t m_pad;
+  const ExpertDev* experts;  // E routed then n_shared shared
+  int32_t max_blocks;
+  // outputs / workspace
+  int32_t* elist;            // entries grouped by expert: entry index (t*K+k) or shared slot
+  int32_t* block_expert;     // per block: expert
+  int32_t* block_start;      // per block: first position in elist
+  GemvProblem* p1;
+  GemvProblem* p2;
+  int32_t* n_p1;
+  int32_t* n_p2;
+  uint8_t* act_pool;         // per block: (d/32) * m_pad * 64 bytes
+  uint8_t* h_pool;           // per block: (f_max/32) * m_pad * 64 bytes
+  int64_t h_block_bytes;
+  float* t1_pool;            // per block: 2 x m_pad x rank1_max
+  float* t2_pool;            // per block: m_pad x rank2_max
+  int32_t rank1_max, rank2_max;
+  float* Y;                  // (m*K + n_shared*m) x d fp32
+  int32_t* zero_ptr;         // counters to clear
+  int64_t zero_count;
+  int32_t* n_blocks_out;
+};
+
+constexpr int kRouteThreads = 1024;
+constexpr int kRouteMaxE = 256;
+
+__global__ void __launch_bounds__(kRouteThreads) moe_route_kernel(MoeRouteArgs a) {
+  pdl_wait();
+  __shared__ int32_t wtot[32][kRouteMaxE];  // per-warp per-expert counts of the round
+  __shared__ int32_t cnt[kRouteMaxE + 8];
+  __shared__ int32_t base[kRouteMaxE + 8];
+  __shared__ int32_t off[kRouteMaxE + 8];
+  __shared__ int32_t boff[kRouteMaxE + 8];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int E = a.E, K = a.K;
+  const int ET = E + a.n_shared;
+  for (int64_t i = tid; i < a.zero_count; i += blockDim.x) a.zero_ptr[i] = 0;
+  for (int e = tid; e < ET; e += blockDim.x) {
+    cnt[e] = e < E ? 0 : (int32_t)a.m;
+    base[e] = 0;
+  }
+  __syncthreads();
+  const uint32_t ltmask = (1u << lane) - 1u;
+  // pass 0: counts; pass 1: positions (ascending token order within an expert)
+  for (int pass = 0; pass < 2; ++pass) {
+    if (pass == 1) {
+      if (tid == 0) {
+        int32_t acc = 0, bacc = 0;
+        for (int e = 0; e < ET; ++e) {
+          off[e] = acc;
+          boff[e] = bacc;
+          acc += cnt[e];
+          bacc += (cnt[e] + a.m_pad - 1) / a.m_pad;
+        }
+        off[ET] = acc;
+        boff[ET] = bacc;
+        *a.n_blocks_out = bacc;
+      }
+      __syncthreads();
+    }
+    for (int64_t r0 = 0; r0 < a.m; r0 += kRouteThreads) {
+      const int64_t t = r0 + tid;
+      int32_t my[16];
+      for (int k = 0; k < K; ++k) my[k] = (t < a.m) ? a.ids[t * K + k] : -1;
+      for (int e = 0; e < E; ++e) {
+        int kk = -1;
+        for (int k = 0; k < K; ++k)
+          if (my[k] == e) kk = k;
+        const uint32_t vote = __ballot_sync(0xffffffffu, kk >= 0);
+        if (lane == 0) wtot[warp][e] = __popc(vote);
+        if (pass == 1 && kk >= 0) my[kk] = -2 - __popc(vote & ltmask);  // stash lane rank
+      }
+      __syncthreads();
+      if (pass == 0) {
+        for (int e = tid; e < E; e += blockDim.x) {
+          int32_t s = 0;
+          for (int w = 0; w < 32; ++w) s += wtot[w][e];
+          cnt[e] += s;
+        }
+      } else {
+        // positions: off[e] + base[e] + (warps before) + lane rank
+        for (int k = 0; k < K; ++k) {
+          if (t < a.m && my[k] <= -2) {
+            const int32_t e = a.ids[t * K + k];
+            int32_t before = 0;
+            for (int w = 0; w < warp; ++w) before += wtot[w][e];
+            const int32_t pos = off[e] + base[e] + before + (-2 - my[k]);
+            a.elist[pos] = (int32_t)(t * K + k);
+          }
+        }
+        __syncthreads();
+        for (int e = tid; e < E; e += blockDim.x) {
+          int32_t s = 0;
+          for (int w = 0; w < 32; ++w) s += wtot[w][e];
+          base[e] += s;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // shared experts: every token, slot m*K + s*m + t
+  for (int s = 0; s < a.n_shared; ++s)
+    for (int64_t t = tid; t < a.m; t += blockDim.x)
+      a.elist[off[E + s] + t] = (int32_t)(a.m * K + s * a.m + t);
+  __syncthreads();
+  // problem tables: one thread per expert, blocks in order
+  for (int e = tid; e < ET; e += blockDim.x) {
+    const ExpertDev& ex = a.experts[e];
+    const int nb = (cnt[e] + a.m_pad - 1) / a.m_pad;
+    for (int b = 0; b < nb; ++b) {
+      const int blk = boff[e] + b;
+      if (blk >= a.max_blocks) break;
+      a.block_expert[blk] = e;
+      a.block_start[blk] = off[e] + b * a.m_pad;
+      const int rows = min(a.m_pad, cnt[e] - b * a.m_pad);
+      GemvProblem p{};
+      p.w[0] = ex.w[0];
+      p.w[1] = ex.w[1];
+      p.act = a.act_pool + (int64_t)blk * (a.d / 32) * a.m_pad * 64;
+      for (int mat = 0; mat < 2; ++mat) {
+        p.rank[mat] = ex.rank[mat];
+        p.vgpr[mat] = ex.gpr[mat];
+        p.vcodes[mat] = ex.vcodes[mat];
+        p.vscales[mat] = ex.vscales[mat];
+        p.vreal[mat] = ex.vreal[mat];
+        p.ucodes[mat] = ex.ucodes[mat];
+        p.uscales[mat] = ex.uscales[mat];
+        p.ureal[mat] = ex.ureal[mat];
+        p.t[mat] = ex.rank[mat] > 0
+                       ? a.t1_pool + ((int64_t)blk * 2 + mat) * a.m_pad * a.rank1_max
+                       : nullptr;
+      }
+      p.k = a.d;
+      p.n = ex.f;
+      p.m = rows;
+      p.mode = ex.mode;
+      p.kind = kSwigluAct;
+      p.out = a.h_pool + (int64_t)blk * a.h_block_bytes;
+      a.p1[blk] = p;
+      GemvProblem q{};
+      q.w[0] = ex.w[2];
+      q.act = a.h_pool + (int64_t)blk * a.h_block_bytes;
+      q.rank[0] = ex.rank[2];
+      q.vgpr[0] = ex.gpr[2];
+      q.vcodes[0] = ex.vcodes[2];
+      q.vscales[0] = ex.vscales[2];
+      q.vreal[0] = ex.vreal[2];
+      q.ucodes[0] = ex.ucodes[2];
+      q.uscales[0] = ex.uscales[2];
+      q.ureal[0] = ex.ureal[2];
+      q.t[0] = ex.rank[2] > 0 ? a.t2_pool + (int64_t)blk * a.m_pad * a.rank2_max : nullptr;
+      q.k = ex.f;
+      q.n = a.d;
+      q.m = rows;
+      q.mode = ex.mode;
+      q.kind = kStoreRows;
+      q.out_dtype = 0;
+      q.ldo = a.d;
+      q.out = a.Y;
+      q.row_map = a.elist + off[e] + b * a.m_pad;
+      a.p2[blk] = q;
+    }
+  }
+  if (tid == 0) {
+    const int nb = min(boff[ET], a.max_blocks);
+    *a.n_p1 = nb;
+    *a.n_p2 = nb;
+  }
+  pdl_launch_dependents();
+}
+
+// x rows of each block -> binary16 act tiles (m_pad rows, zero padded).
+__global__ void moe_gather_kernel(const void* __restrict__ x, int32_t x_dtype, int64_t d, int K,
+                                  int64_t m, const int32_t* __restrict__ elist,
+                                  const int32_t* __restrict__ block_start,
+                                  const int32_t* __restrict__ block_expert,
+                                  const int32_t* __restrict__ n_blocks, int32_t n_routed,
+                                  int32_t m_pad, uint8_t* act_pool, const GemvProblem* __restrict__ p1) {
+  pdl_wait();
+  const int blk = blockIdx.x;
+  if (blk >= *n_blocks) return;
+  const GemvProblem& pr = p1[blk];
+  const int rows = pr.m;
+  const int32_t* list = elist + block_start[blk];
+  const bool shared = block_expert[blk] >= n_routed;
+  uint32_t* act = reinterpret_cast<uint32_t*>(act_pool + (int64_t)blk * (d / 32) * m_pad * 64);
+  const int64_t kw = d / 2;
+  for (int64_t i = threadIdx.x; i < (int64_t)m_pad * kw; i += blockDim.x) {
+    const int r = (int)(i / kw);
+    const int64_t w = i % kw;
+    __half2 v = __floats2half2_rn(0.0f, 0.0f);
+    if (r < rows) {
+      const int32_t entry = list[r];
+      const int64_t tok = shared ? (entry - m * K) % m : entry / K;
+      if (x_dtype == 0) {
+        const float2 f = reinterpret_cast<const float2*>(x)[(tok * d) / 2 + w];
+        v = __floats2half2_rn(f.x, f.y);
+      } else {
+        v = reinterpret_cast<const __half2*>(x)[(tok * d) / 2 + w];
+      }
+    }
+    act[act_word(m_pad, r, (int)(2 * w))] = h2_as_u32(v);
+  }
+  pdl_launch_dependents();
+}
+
+__global__ void moe_combine_kernel(const float* __restrict__ Y, const int32_t* __restrict__ ids,
+                                   const float* __restrict__ wts, int64_t m, int K, int n_shared,
+                                   int64_t d, void* out, int32_t out_dtype) {
+  pdl_wait();
+  const int64_t total = m * (d / 4);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = i / (d / 4), c4 = i % (d / 4);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int k = 0; k < K; ++k) {
+      if (ids[t * K + k] < 0) continue;
+      const float w = wts[t * K + k];
+      const float4 y = reinterpret_cast<const float4*>(Y + (t * K + k) * d)[c4];
+      acc.x += w * y.x;
+      acc.y += w * y.y;
+      acc.z += w * y.z;
+      acc.w += w * y.w;
+    }
+    for (int s = 0; s < n_shared; ++s) {
+      const float4 y = reinterpret_cast<const float4*>(Y + (m * K + s * m + t) * d)[c4];
+      acc.x += 1.0f * y.x;
+      acc.y += 1.0f * y.y;
+      acc.z += 1.0f * y.z;
+      acc.w += 1.0f * y.w;
+    }
+    if (out_dtype == 0) {
+      reinterpret_cast<float4*>(out)[i] = acc;
+    } else {
+      __half2* o = reinterpret_cast<__half2*>(out) + i * 2;
+      o[0] = __floats2half2_rn(acc.x, acc.y);
+      o[1] = __floats2half2_rn(acc.z, acc.w);
+    }
+  }
+}
+
+}  // namespace milo_dev
