@@ -1,0 +1,375 @@
+#!/usr/bin/env python3
+"""Benchmark: INT3+LoRC MoE-layer latency (us) & achieved HBM GB/s on B200.
+
+Default workload (BASELINE.json configs[1]): one Mixtral-8x7B MoE layer —
+8 experts (d=4096, f=14336), top-2 router, INT3 g64 asymmetric weights with
+ragged symm-int3 compensator ranks — at batch 1 (decode), random-init
+synthetic weights/activations of that shape.  A "step" is one full layer
+call: router top-k -> permute -> grouped W3A16+LoRC (w1|w3 + SwiGLU) ->
+grouped W3A16+LoRC (w2) -> weighted combine.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl milo|reference]
+                    [--config mixtral|deepseek|arctic] [--batch M] [--no-sweep]
+
+Timing: W untimed warm-up steps, then K steps, each bracketed by CUDA events on
+the launching stream; the 256 MiB L2-flush write between steps is outside the
+events.  Barrier + synchronize around the timed region, max over ranks.
+`value` = mean layer latency (us, lower is better).  `e2e` = the same through
+the host-buffer C-ABI entry point (milo_moe_forward_host: pinned host x and
+logits copied in, output copied back inside the timed call), wall clock.
+`roofline` = the dominant kernel (grouped GEMM phase 1, w1|w3 + SwiGLU),
+algorithmic bytes (matrix_memory_bytes of every touched expert + fp16
+activations) / its CUDA-event duration, against the
+measured HBM copy bandwidth in MEASURED_PEAKS.json.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "INT3+LoRC MoE-layer latency (us) & achieved HBM GB/s, batch 1-256, 1/8 GPU"
+FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured (MEASURED_PEAKS.json)"
+    return FALLBACK_PEAKS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """Samples SM clocks and throttle reasons through NVML during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, index: int):
+        self.samples = []
+        self.max_mhz = None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001 - sampling is best effort
+            self._nv = None
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                sm = self._nv.nvmlDeviceGetClockInfo(self._h, self._nv.NVML_CLOCK_SM)
+                rs = self._nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                self.samples.append((sm, rs))
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self._nv is not None:
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._nv is not None:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        busy = [s for s in self.samples if not (s[1] & 0x1)] or self.samples
+        reasons = set()
+        for _, r in busy:
+            for bit, name in self.REASONS.items():
+                if r & bit and bit != 0x1:
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median([s[0] for s in busy])), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_reference_time(spec, routed, shared, m, steps, seed, which="ref"):
+    """Times the reference CPU implementation (oracle/_ref: the reference's
+    own gemm_w3a16 composed per expert through its parallel_for), or our C
+    restatement if the reference library was not built.  Returns dict."""
+    from oracle.oracle import Comp, Oracle, Packed
+    kind = "reference" if which == "ref" and Oracle.available("ref") else "port"
+    o = Oracle("ref" if kind == "reference" else "oracle")
+    cores = os.cpu_count() or 1
+
+    def cv(P):
+        return Packed(P.rows, P.cols, 0, False, P.mode, 64, P.words, None, None, P.scales, P.zeros)
+
+    def cc(c):
+        if c is None:
+            return None
+        return Comp(c.rows, c.cols, c.rank, 1, None, None, c.qu_codes, c.qu_scales, c.qvt_codes,
+                    c.qvt_scales, 64)
+
+    ex = [{"w": [cv(P) for P in h.w], "c": [cc(c) for c in h.c]} for h in routed]
+    sh = [{"w": [cv(P) for P in h.w], "c": [cc(c) for c in h.c]} for h in shared]
+    rng = np.random.default_rng(seed + 99)
+    orc = Oracle("oracle")
+    times = []
+    for _ in range(steps):
+        x = rng.normal(0, 1, (m, spec.d)).astype(np.float32)
+        logits = rng.normal(0, 1, (m, spec.experts)).astype(np.float32)
+        t0 = time.perf_counter()
+        ids, w = orc.router_topk(logits, spec.top_k, spec.score_mode)
+        o.moe_forward(ex, sh, x, ids, w, n_threads=cores)
+        times.append(time.perf_counter() - t0)
+    return {"us": float(np.mean(times)) * 1e6, "kind": kind, "cores": cores,
+            "sample": f"{steps} x {spec.name} layer calls at batch {m} (all experts' weights "
+                      f"resident in host RAM; {cores} threads via parallel_for over active experts)"}
+
+
+def run_reference_arm(args, spec):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2504_02658_b200.synth import build_host_layer
+    routed, shared = build_host_layer(spec, seed=args.seed)
+    steps = max(1, args.steps)
+    for _ in range(max(0, min(args.warmup, 1))):
+        cpu_reference_time(spec, routed, shared, args.batch, 1, args.seed)
+    res = cpu_reference_time(spec, routed, shared, args.batch, steps, args.seed)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(res["us"], 1), "unit": "us",
+        "n_gpus": ws, "steps": steps, "warmup": args.warmup, "ms_per_step": round(res["us"] / 1e3, 3),
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f16/f32",
+        "data": "synthetic", "config": {"workload": spec.name, "batch": args.batch,
+                                        "experts": spec.experts, "top_k": spec.top_k,
+                                        "d": spec.d, "f": spec.f},
+        "cpu_baseline": {"value": round(res["us"], 1), "unit": "us", "cores": res["cores"],
+                         "kind": res["kind"], "sample": res["sample"]},
+        "e2e": {"value": round(res["us"], 1), "unit": "us", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="milo", choices=["milo", "reference"])
+    ap.add_argument("--config", default="mixtral", choices=["mixtral", "deepseek", "arctic"])
+    ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    from paper_2504_02658_b200.synth import CONFIGS
+    spec = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference_arm(args, spec)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2504_02658_b200 as mb
+    from paper_2504_02658_b200.synth import build_host_layer, layer_traffic
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    mb.device_check()
+    peaks, peaks_src = load_peaks()
+
+    routed_h, shared_h = build_host_layer(spec, seed=args.seed)
+    experts = [mb.Expert(*(mb.Weight(P) for P in h.w),
+                         *((mb.Comp(c) if c is not None else None) for c in h.c)) for h in routed_h]
+    shared = [mb.Expert(*(mb.Weight(P) for P in h.w),
+                        *((mb.Comp(c) if c is not None else None) for c in h.c)) for h in shared_h]
+    layer = mb.MoELayer(experts, shared, top_k=spec.top_k, score_mode=spec.score_mode)
+    # Replicas: with N > 1 every rank runs its own layer instance on its own
+    # token batch (weak scaling).  Expert-parallel sharding is DESIGN.md section 7.
+
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def make_inputs(m, n_steps, seed):
+        g = torch.Generator(device="cuda").manual_seed(seed * 1000 + rank)
+        xs = [torch.randn(m, spec.d, device="cuda", generator=g).half() for _ in range(n_steps)]
+        ls = [torch.randn(m, spec.experts, device="cuda", generator=g) for _ in range(n_steps)]
+        return xs, ls
+
+    def time_steps(m, n_steps, warmup, profile=False):
+        xs, ls = make_inputs(m, warmup + n_steps, args.seed + m)
+        out = torch.empty(m, spec.d, device="cuda", dtype=torch.float16)
+        for i in range(warmup):
+            layer.forward(xs[i], ls[i], out_dtype=torch.float16)
+        ids_all = []
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(n_steps)]
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        l0 = mb.launch_count()
+        if profile:
+            mb.profile_enable(True)
+        for i in range(n_steps):
+            flush.zero_()
+            s, e = evs[i]
+            s.record(stream)
+            o, ids, _ = layer.forward(xs[warmup + i], ls[warmup + i], out_dtype=torch.float16,
+                                      return_routing=True)
+            e.record(stream)
+            ids_all.append(ids)
+        torch.cuda.synchronize()
+        if profile:
+            mb.profile_enable(False)
+        launches = mb.launch_count() - l0
+        if ws > 1:
+            dist.barrier()
+        ms = np.array([s.elapsed_time(e) for s, e in evs])
+        ids_np = [i.cpu().numpy() for i in ids_all]
+        return ms, ids_np, launches
+
+    # ---------------- headline timed region ----------------
+    m = args.batch
+    with ClockSampler(local) as clk:
+        ms, ids_np, launches = time_steps(m, args.steps, args.warmup)
+    mean_ms = float(ms.mean())
+    if ws > 1:
+        t = torch.tensor([mean_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        mean_ms = float(t.item())
+    traffic = [layer_traffic(spec, routed_h, shared_h, i) for i in ids_np]
+    tot_bytes = float(np.mean([t["total_bytes"] for t in traffic]))
+    tot_flops = float(np.mean([t["total_flops"] for t in traffic]))
+
+    # ---------------- roofline of the dominant kernel (live CUDA events) ----------------
+    ms_p, ids_p, _ = time_steps(m, args.steps, 2, profile=True)
+    n1, t1 = mb.profile_read(0)
+    n2, t2 = mb.profile_read(1)
+    nl, tl = mb.profile_read(2)
+    tr_p = [layer_traffic(spec, routed_h, shared_h, i) for i in ids_p]
+    p1_bytes = float(np.mean([t["phase1_bytes"] for t in tr_p]))
+    p2_bytes = float(np.mean([t["phase2_bytes"] for t in tr_p]))
+    p1_ms = t1 / max(n1, 1)
+    p2_ms = t2 / max(n2, 1)
+    hbm = float(peaks["hbm_gbs"])
+    achieved = p1_bytes / (p1_ms * 1e-3) / 1e9
+    traffic_ncu = None
+    ncu_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(ncu_path):
+        try:
+            traffic_ncu = json.load(open(ncu_path)).get(args.config, {}).get(str(m))
+        except Exception:  # noqa: BLE001
+            traffic_ncu = None
+
+    # ---------------- end to end through the host-buffer C ABI ----------------
+    e2e_steps = max(3, min(args.steps, 50))
+    xh = torch.randn(m, spec.d).pin_memory()
+    lh = torch.randn(m, spec.experts).pin_memory()
+    xn, ln = xh.numpy(), lh.numpy()
+    for _ in range(2):
+        layer.forward_host(xn, ln)
+    if ws > 1:
+        dist.barrier()
+    wall = []
+    for _ in range(e2e_steps):
+        t0 = time.perf_counter()
+        layer.forward_host(xn, ln)
+        wall.append(time.perf_counter() - t0)
+    e2e_us = float(np.mean(wall)) * 1e6
+    if ws > 1:
+        t = torch.tensor([e2e_us], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_us = float(t.item())
+
+    # ---------------- batch sweep (N=1) ----------------
+    sweep = []
+    if not args.no_sweep and ws == 1:
+        for mm in (1, 16, 64, 256):
+            sms, sids, _ = time_steps(mm, 10, 3)
+            tr = [layer_traffic(spec, routed_h, shared_h, i) for i in sids]
+            b = float(np.mean([t["total_bytes"] for t in tr]))
+            fl = float(np.mean([t["total_flops"] for t in tr]))
+            us = float(sms.mean()) * 1e3
+            t_roof = max(b / (hbm * 1e9), fl / (float(peaks["bf16_tflops"]) * 1e12)) * 1e6
+            sweep.append({"batch": mm, "us": round(us, 2), "GBps": round(b / us / 1e3, 1),
+                          "TFLOPs": round(fl / us / 1e6, 2), "roofline_us": round(t_roof, 2),
+                          "roofline_frac": round(t_roof / us, 3)})
+
+    # ---------------- CPU baseline (rank 0, N=1) ----------------
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        try:
+            res = cpu_reference_time(spec, routed_h, shared_h, m, 2, args.seed)
+            cpu = {"value": round(res["us"], 1), "unit": "us", "cores": res["cores"],
+                   "kind": res["kind"], "sample": res["sample"]}
+        except Exception as exc:  # noqa: BLE001
+            cpu = {"value": None, "unit": "us", "cores": os.cpu_count(), "kind": "port",
+                   "sample": f"unavailable: {exc}"}
+
+    if rank != 0:
+        if ws > 1:
+            dist.destroy_process_group()
+        return
+    value_us = mean_ms * 1e3
+    line = {
+        "metric": METRIC, "value": round(value_us, 2), "unit": "us", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(mean_ms, 4),
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f16 (activations, de-quantized weights) / f32 accumulate",
+        "data": "synthetic (random-init INT3 g64 weights, symm-int3 LoRC, N(0,1) activations "
+                "and router logits)",
+        "config": {"workload": spec.name, "batch": m, "experts": spec.experts,
+                   "top_k": spec.top_k, "d": spec.d, "f": spec.f, "shared_experts": spec.shared,
+                   "ranks": list(spec.routed_ranks), "parallelism": f"replicas x{ws}",
+                   "l2": "flushed between steps (256 MiB write, outside the timed events)"},
+        "achieved_GBps_layer": round(tot_bytes / (value_us * 1e-6) / 1e9, 1),
+        "layer_bytes": int(tot_bytes), "layer_flops": int(tot_flops),
+        "roofline": {"bound": "hbm", "kernel": "gemv_w3a16_kernel<NT,2> (phase 1: w1|w3 + "
+                     "SwiGLU + LoRC)", "achieved": round(achieved, 1), "peak": hbm,
+                     "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": traffic_ncu,
+                     "algorithmic_bytes_per_launch": int(p1_bytes),
+                     "launch_us": round(p1_ms * 1e3, 2), "peak_source": peaks_src,
+                     "phase2": {"algorithmic_bytes_per_launch": int(p2_bytes),
+                                "launch_us": round(p2_ms * 1e3, 2),
+                                "achieved": round(p2_bytes / (p2_ms * 1e-3) / 1e9, 1)},
+                     "lorc_us_per_step": round(tl / max(1, len(ms_p)) * 1e3, 2),
+                     "layer_frac": round(tot_bytes / (value_us * 1e-6) / 1e9 / hbm, 4)},
+        "e2e": {"value": round(e2e_us, 2), "unit": "us",
+                "h2d_bytes_per_step": int(m * spec.d * 4 + m * spec.experts * 4),
+                "d2h_bytes_per_step": int(m * spec.d * 4)},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+        "sweep": sweep,
+    }
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -203,6 +203,14 @@ milo_status milo_moe_forward_host(milo_moe* moe, const float* x, int64_t m,
  * bench's gpu_launches claim). */
 uint64_t milo_launch_count(void);
 
+/* Optional CUDA-event timing of the library's own kernels on the launching
+ * stream (calling thread only).  kind: 0 grouped GEMM phase 1 (w1|w3 +
+ * SwiGLU, or the single-linear GEMM), 1 grouped GEMM phase 2 (w2),
+ * 2 compensator t = A U, 3 other.  milo_profile_read returns the number of
+ * recorded launches of that kind and their summed duration, then clears. */
+void milo_profile_enable(int32_t on);
+int64_t milo_profile_read(int32_t kind, double* total_ms);
+
 #ifdef __cplusplus
 }
 #endif

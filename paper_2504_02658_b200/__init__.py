@@ -113,6 +113,10 @@ def lib() -> C.CDLL:
     L.milo_last_error.restype = C.c_char_p
     L.milo_status_name.restype = C.c_char_p
     L.milo_launch_count.restype = u64
+    L.milo_profile_enable.argtypes = [i32]
+    L.milo_profile_enable.restype = None
+    L.milo_profile_read.argtypes = [i32, C.POINTER(C.c_double)]
+    L.milo_profile_read.restype = i64
     sig = {
         "milo_device_check": [],
         "milo_weight_create": [C.POINTER(_PackedDesc), C.POINTER(vp)],
@@ -149,6 +153,17 @@ def _check(status: int):
 
 def launch_count() -> int:
     return int(lib().milo_launch_count())
+
+
+def profile_enable(on: bool = True):
+    lib().milo_profile_enable(int(on))
+
+
+def profile_read(kind: int):
+    """(launches, total_ms) of kernel kind 0 gemm phase 1, 1 phase 2, 2 lorc, 3 other."""
+    t = C.c_double()
+    n = lib().milo_profile_read(kind, C.byref(t))
+    return int(n), float(t.value)
 
 
 def device_check():

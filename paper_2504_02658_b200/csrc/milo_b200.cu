@@ -91,6 +91,32 @@ cudaError_t launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
+// Optional per-kernel CUDA-event timing (milo_profile_*), recorded on the
+// launching stream around selected launches.  Off by default.
+enum ProfKind { kProfGemv1 = 0, kProfGemv2 = 1, kProfLorc = 2, kProfOther = 3, kProfKinds = 4 };
+struct ProfState {
+  bool on = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[kProfKinds];
+};
+thread_local ProfState g_prof;
+
+struct ProfScope {
+  cudaEvent_t b = nullptr, e = nullptr;
+  cudaStream_t s;
+  int kind;
+  ProfScope(int k, cudaStream_t st) : s(st), kind(k) {
+    if (!g_prof.on) return;
+    cudaEventCreate(&b);
+    cudaEventCreate(&e);
+    cudaEventRecord(b, s);
+  }
+  ~ProfScope() {
+    if (!b) return;
+    cudaEventRecord(e, s);
+    g_prof.ev[kind].push_back({b, e});
+  }
+};
+
 // Bump allocator over one stream-ordered allocation.
 struct Arena {
   size_t size = 0;
@@ -156,6 +182,28 @@ const char* milo_status_name(milo_status s) {
     case MILO_ERR_ARGUMENT: return "argument";
   }
   return "unknown";
+}
+
+void milo_profile_enable(int32_t on) { g_prof.on = on != 0; }
+
+// Sums the recorded durations of one kernel kind (synchronizing on the last
+// event), returns the count, and releases the events.
+int64_t milo_profile_read(int32_t kind, double* total_ms) {
+  if (kind < 0 || kind >= kProfKinds) return -1;
+  double tot = 0.0;
+  auto& v = g_prof.ev[kind];
+  for (auto& pe : v) {
+    float ms = 0.0f;
+    cudaEventSynchronize(pe.second);
+    cudaEventElapsedTime(&ms, pe.first, pe.second);
+    tot += ms;
+    cudaEventDestroy(pe.first);
+    cudaEventDestroy(pe.second);
+  }
+  const int64_t n = (int64_t)v.size();
+  v.clear();
+  if (total_ms) *total_ms = tot;
+  return n;
 }
 
 milo_status milo_device_check(void) {
@@ -521,6 +569,7 @@ extern "C" milo_status milo_gemm_w3a16(const milo_weight* w, const milo_comp* co
       la.m_pad = m_pad;
       la.chunks = chunks;
       la.rank_max = rank;
+      ProfScope ps(kProfLorc, stream);
       e = launch(lorc_t_kernel, dim3(blocks * 2, chunks), dim3(32 * kLorcWarps), 0, stream, true, la);
     }
     if (e != cudaSuccess) {
@@ -532,8 +581,11 @@ extern "C" milo_status milo_gemm_w3a16(const milo_weight* w, const milo_comp* co
     ga.n_problems = lp.n_problems;
     ga.ws = reinterpret_cast<float*>(base + o_ws);
     ga.counters = lp.counters;
-    st = nt == 1 ? launch_gemv<1, 1>(ga, stream, props.sms, true)
-                 : launch_gemv<2, 1>(ga, stream, props.sms, true);
+    {
+      ProfScope ps(kProfGemv1, stream);
+      st = nt == 1 ? launch_gemv<1, 1>(ga, stream, props.sms, true)
+                   : launch_gemv<2, 1>(ga, stream, props.sms, true);
+    }
     cudaFreeAsync(mem, stream);
     if (st != MILO_OK) return st;
     done += mm;
@@ -763,6 +815,7 @@ milo_status moe_run(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype, co
     la.m_pad = m_pad;
     la.chunks = chunks1;
     la.rank_max = r1;
+    ProfScope ps(kProfLorc, stream);
     e = launch(lorc_t_kernel, dim3((unsigned)(blocks_max * 2), chunks1), dim3(32 * kLorcWarps), 0,
                stream, true, la);
   }
@@ -774,6 +827,7 @@ milo_status moe_run(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype, co
     ga.n_problems = ra.n_p1;
     ga.ws = reinterpret_cast<float*>(base + o_ws);
     ga.counters = cnt1;
+    ProfScope ps(kProfGemv1, stream);
     st = launch_gemv<NT, 2>(ga, stream, sms, true);
   }
   if (st == MILO_OK && moe->rank2_max > 0) {
@@ -785,6 +839,7 @@ milo_status moe_run(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype, co
     la.m_pad = m_pad;
     la.chunks = chunks2;
     la.rank_max = r2;
+    ProfScope ps(kProfLorc, stream);
     e = launch(lorc_t_kernel, dim3((unsigned)(blocks_max * 2), chunks2), dim3(32 * kLorcWarps), 0,
                stream, true, la);
     if (e != cudaSuccess) st = fail(MILO_ERR_CUDA, "launch failed: %s", cudaGetErrorString(e));
@@ -795,6 +850,7 @@ milo_status moe_run(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype, co
     ga.n_problems = ra.n_p2;
     ga.ws = reinterpret_cast<float*>(base + o_ws);
     ga.counters = cnt2;
+    ProfScope ps(kProfGemv2, stream);
     st = launch_gemv<NT, 1>(ga, stream, sms, true);
   }
   if (st == MILO_OK) {
