@@ -97,25 +97,27 @@ __device__ __forceinline__ DqConsts make_dq_consts(int mode) {
   return c;
 }
 
-__device__ __forceinline__ __half2 lanes(uint32_t w, uint32_t mask) {
-  return u32_as_h2((w & mask) | 0x64006400u);
-}
-
 // Exact integer codes (c - bias) of the 16 pairs of one unit, as half2.
+// Per pair: one LOP3 ((w & mask) | 0x64006400 -> 1024 + 2^(3t) c in each
+// lane) and one HADD2/HFMA2 back to c - bias; slots 3,4 share one shift.
 __device__ __forceinline__ void unit_codes(uint32_t W0, uint32_t W1, uint32_t W2,
                                            const DqConsts& k, __half2 (&e)[16]) {
+  uint32_t magic = 0x64006400u;
+  asm volatile("" : "+r"(magic));  // keep the OR operand in a register (one LOP3 per pair)
   const uint32_t W[3] = {W0, W1, W2};
 #pragma unroll
   for (int w = 0; w < 3; ++w) {
     const uint32_t y = W[w] >> 9;
-    e[5 * w + 0] = __hadd2(lanes(W[w], 0x00070007u), k.c0);
-    e[5 * w + 1] = __hfma2(lanes(W[w], 0x00380038u), k.r8, k.c1);
-    e[5 * w + 2] = __hfma2(lanes(W[w], 0x01C001C0u), k.r64, k.c2);
-    e[5 * w + 3] = __hadd2(lanes(y, 0x00070007u), k.c0);
-    e[5 * w + 4] = __hfma2(lanes(y, 0x00380038u), k.r8, k.c1);
+    e[5 * w + 0] = __hadd2(u32_as_h2(and_or<0x00070007u>(W[w], magic)), k.c0);
+    e[5 * w + 1] = __hfma2(u32_as_h2(and_or<0x00380038u>(W[w], magic)), k.r8, k.c1);
+    e[5 * w + 2] = __hfma2(u32_as_h2(and_or<0x01C001C0u>(W[w], magic)), k.r64, k.c2);
+    e[5 * w + 3] = __hadd2(u32_as_h2(and_or<0x00070007u>(y, magic)), k.c0);
+    e[5 * w + 4] = __hfma2(u32_as_h2(and_or<0x00380038u>(y, magic)), k.r8, k.c1);
   }
-  const uint32_t v = ((W0 >> 15) & 0x00010001u) | ((W1 >> 14) & 0x00020002u) |
-                     ((W2 >> 13) & 0x00040004u) | 0x64006400u;
+  // virtual pair: bit b of each code is bit 15 (lo) / 31 (hi) of word b
+  const uint32_t v = and_or<0x00040004u>(W2 >> 13,
+                                         and_or<0x00020002u>(W1 >> 14,
+                                                             and_or<0x00010001u>(W0 >> 15, magic)));
   e[15] = __hadd2(u32_as_h2(v), k.c0);
 }
 

@@ -212,6 +212,7 @@ milo_status milo_device_check(void) {
   if (p.major != 10) return fail(MILO_ERR_CUDA, "device is sm_%d0, this library is sm_100a only", p.major);
   cudaFuncAttributes fa;
   CUDA_TRY(cudaFuncGetAttributes(&fa, gemv_w3a16_kernel<2, 1>));
+  CUDA_TRY(cudaFuncGetAttributes(&fa, lorc_t_kernel));
   return MILO_OK;
 }
 
@@ -443,18 +444,62 @@ void fill_comp(GemvProblem& p, int mat, const milo_comp* c) {
   p.ureal[mat] = c->ureal;
 }
 
+// Workspace of one grouped GEMM launch (sizes in bytes).
 template <int NT, int NMAT>
-milo_status launch_gemv(const GemvArgs& args, cudaStream_t stream, int sms, bool pdl) {
-  using SM = GemvSmem<NT, NMAT>;
+struct GroupedWs {
+  using CF = GemvCfg<NT, NMAT>;
+  static size_t ws_bytes(int sms) { return (size_t)sms * CF::kWarps * 2 * CF::kPartFloats * 4; }
+  static size_t full_bytes(int64_t slabs) { return (size_t)slabs * CF::kPartFloats * 4; }
+  static int lorc_chunks(int64_t k) { return (int)((k + kLorcChunk - 1) / kLorcChunk); }
+  static size_t lorc_bytes(int64_t problems, int64_t k, int rank) {
+    return (size_t)problems * 2 * lorc_chunks(k) * CF::kMPad * std::max(rank, 1) * 4;
+  }
+};
+
+// GEMM (weights stream, partials) -> t = A U (co-runs, PDL) -> fix-up/epilogue.
+template <int NT, int NMAT>
+milo_status run_grouped(const GemvProblem* problems, const int32_t* n_problems,
+                        int64_t problems_max, int64_t slabs_max, int64_t k_max, int rank_max,
+                        float* ws, float* full, float* lorc_partial, int32_t* lorc_counters,
+                        cudaStream_t stream, int sms, int prof_kind) {
+  using CF = GemvCfg<NT, NMAT>;
   static thread_local int configured_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
   if (configured_dev != dev) {
-    CUDA_TRY(set_smem(gemv_w3a16_kernel<NT, NMAT>, SM::kBytes));
+    CUDA_TRY(set_smem(gemv_w3a16_kernel<NT, NMAT>, CF::kBytes));
     configured_dev = dev;
   }
-  CUDA_TRY(launch(gemv_w3a16_kernel<NT, NMAT>, dim3(sms), dim3(32 * (1 + kConsumerWarps)),
-                  SM::kBytes, stream, pdl, args));
+  GemvArgs ga{};
+  ga.problems = problems;
+  ga.n_problems = n_problems;
+  ga.ws = ws;
+  ga.full = full;
+  ga.gw = sms * CF::kWarps;
+  ga.pdl_trigger_early = rank_max > 0 ? 1 : 0;
+  {
+    ProfScope ps(prof_kind, stream);
+    CUDA_TRY(launch(gemv_w3a16_kernel<NT, NMAT>, dim3(sms), dim3(32 * CF::kWarps), CF::kBytes,
+                    stream, true, ga));
+  }
+  if (rank_max > 0) {
+    LorcArgs la{};
+    la.problems = problems;
+    la.n_problems = n_problems;
+    la.partial = lorc_partial;
+    la.counters = lorc_counters;
+    la.m_pad = CF::kMPad;
+    la.chunks = GroupedWs<NT, NMAT>::lorc_chunks(k_max);
+    la.rank_max = rank_max;
+    ProfScope ps(kProfLorc, stream);
+    CUDA_TRY(launch(lorc_t_kernel, dim3((unsigned)(problems_max * 2), la.chunks),
+                    dim3(kLorcThreads), 0, stream, true, la));
+  }
+  {
+    ProfScope ps(kProfOther, stream);
+    CUDA_TRY(launch(gemv_epilogue_kernel<NT, NMAT>, dim3((unsigned)slabs_max), dim3(256), 0,
+                    stream, true, ga));
+  }
   return MILO_OK;
 }
 
@@ -507,18 +552,21 @@ extern "C" milo_status milo_gemm_w3a16(const milo_weight* w, const milo_comp* co
   while (done < m) {
     const int64_t mm = std::min<int64_t>(m - done, (int64_t)(kMaxProblems - 1) * m_pad);
     const int blocks = (int)((mm + m_pad - 1) / m_pad);
-    const int chunks = (int)std::max<int64_t>(1, std::min<int64_t>(16, k / 512));
+    const int64_t slabs = (int64_t)blocks * (n / 64);
     Arena ar;
     const int64_t act_block_words = (k / 32) * m_pad * 16;
     const size_t o_act = ar.take((size_t)blocks * act_block_words * 4);
     const size_t o_prob = ar.take((size_t)blocks * sizeof(GemvProblem));
     const size_t o_np = ar.take(4);
     const size_t o_t = ar.take((size_t)blocks * m_pad * std::max(rank, 1) * 4);
-    const size_t o_part = ar.take((size_t)blocks * 2 * chunks * m_pad * std::max(rank, 1) * 4);
+    const size_t ws_b = nt == 1 ? GroupedWs<1, 1>::ws_bytes(props.sms) : GroupedWs<2, 1>::ws_bytes(props.sms);
+    const size_t full_b = nt == 1 ? GroupedWs<1, 1>::full_bytes(slabs) : GroupedWs<2, 1>::full_bytes(slabs);
+    const size_t part_b = nt == 1 ? GroupedWs<1, 1>::lorc_bytes(blocks, k, rank)
+                                  : GroupedWs<2, 1>::lorc_bytes(blocks, k, rank);
+    const size_t o_ws = ar.take(ws_b);
+    const size_t o_full = ar.take(full_b);
+    const size_t o_part = ar.take(part_b);
     const size_t o_tc = ar.take((size_t)blocks * 2 * 4);
-    const size_t o_ws = ar.take((size_t)props.sms * 2 * m_pad * 64 * 4);
-    const int n_counters = (int)(blocks * (n / 64));
-    const size_t o_cnt = ar.take((size_t)n_counters * 4);
     void* mem = nullptr;
     CUDA_TRY(cudaMallocAsync(&mem, ar.size, stream));
     uint8_t* base = static_cast<uint8_t*>(mem);
@@ -553,39 +601,25 @@ extern "C" milo_status milo_gemm_w3a16(const milo_weight* w, const milo_comp* co
     lp.out_block_elems = (int64_t)m_pad * n;
     lp.problems = reinterpret_cast<GemvProblem*>(base + o_prob);
     lp.n_problems = reinterpret_cast<int32_t*>(base + o_np);
-    lp.counters = reinterpret_cast<int32_t*>(base + o_cnt);
-    lp.n_counters = n_counters;
+    lp.counters = nullptr;
+    lp.n_counters = 0;
     lp.t_counters = reinterpret_cast<int32_t*>(base + o_tc);
     lp.n_t_counters = blocks * 2;
     const int64_t prep_threads = (int64_t)blocks * m_pad * (k / 2);
     const int prep_grid = (int)std::min<int64_t>((prep_threads + 255) / 256, props.sms * 8);
     cudaError_t e = launch(prep_linear_kernel, dim3(prep_grid), dim3(256), 0, stream, false, lp);
-    if (e == cudaSuccess && rank > 0) {
-      LorcArgs la{};
-      la.problems = lp.problems;
-      la.n_problems = lp.n_problems;
-      la.partial = reinterpret_cast<float*>(base + o_part);
-      la.counters = lp.t_counters;
-      la.m_pad = m_pad;
-      la.chunks = chunks;
-      la.rank_max = rank;
-      ProfScope ps(kProfLorc, stream);
-      e = launch(lorc_t_kernel, dim3(blocks * 2, chunks), dim3(32 * kLorcWarps), 0, stream, true, la);
-    }
     if (e != cudaSuccess) {
       cudaFreeAsync(mem, stream);
       return fail(MILO_ERR_CUDA, "launch failed: %s", cudaGetErrorString(e));
     }
-    GemvArgs ga{};
-    ga.problems = lp.problems;
-    ga.n_problems = lp.n_problems;
-    ga.ws = reinterpret_cast<float*>(base + o_ws);
-    ga.counters = lp.counters;
-    {
-      ProfScope ps(kProfGemv1, stream);
-      st = nt == 1 ? launch_gemv<1, 1>(ga, stream, props.sms, true)
-                   : launch_gemv<2, 1>(ga, stream, props.sms, true);
-    }
+    float* ws = reinterpret_cast<float*>(base + o_ws);
+    float* full = reinterpret_cast<float*>(base + o_full);
+    float* part = reinterpret_cast<float*>(base + o_part);
+    int32_t* tc = lp.t_counters;
+    st = nt == 1 ? run_grouped<1, 1>(lp.problems, lp.n_problems, blocks, slabs, k, rank, ws, full,
+                                     part, tc, stream, props.sms, kProfGemv1)
+                 : run_grouped<2, 1>(lp.problems, lp.n_problems, blocks, slabs, k, rank, ws, full,
+                                     part, tc, stream, props.sms, kProfGemv1);
     cudaFreeAsync(mem, stream);
     if (st != MILO_OK) return st;
     done += mm;
@@ -739,9 +773,8 @@ milo_status moe_run(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype, co
   const int64_t blocks_max = std::min<int64_t>(
       kMaxProblems - 1, (m * K + m_pad - 1) / m_pad + std::min<int64_t>(E, m * K) +
                             (int64_t)S * ((m + m_pad - 1) / m_pad));
-  const int chunks1 = (int)std::max<int64_t>(1, std::min<int64_t>(16, d / 512));
-  const int chunks2 = (int)std::max<int64_t>(1, std::min<int64_t>(16, f_max / 512));
-  const int r1 = std::max(moe->rank1_max, 1), r2 = std::max(moe->rank2_max, 1);
+  const int r1 = moe->rank1_max, r2 = moe->rank2_max;
+  const int64_t slabs1 = blocks_max * (f_max / 64), slabs2 = blocks_max * (d / 64);
   Arena ar;
   const size_t o_elist = ar.take((size_t)(m * K + S * m + 1) * 4);
   const size_t o_bexp = ar.take((size_t)blocks_max * 4);
@@ -753,13 +786,14 @@ milo_status moe_run(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype, co
   const int64_t h_block = (f_max / 32) * m_pad * 64;
   const size_t o_act = ar.take((size_t)blocks_max * act_block);
   const size_t o_h = ar.take((size_t)blocks_max * h_block);
-  const size_t o_t1 = ar.take((size_t)blocks_max * 2 * m_pad * r1 * 4);
-  const size_t o_t2 = ar.take((size_t)blocks_max * m_pad * r2 * 4);
-  const size_t o_pa1 = ar.take((size_t)blocks_max * 2 * chunks1 * m_pad * r1 * 4);
-  const size_t o_pa2 = ar.take((size_t)blocks_max * 2 * chunks2 * m_pad * r2 * 4);
-  const size_t o_ws = ar.take((size_t)sms * 2 * 2 * m_pad * 64 * 4);
-  const int64_t n_cnt1 = blocks_max * (f_max / 64), n_cnt2 = blocks_max * (d / 64);
-  const int64_t n_zero = n_cnt1 + n_cnt2 + 4 * blocks_max;
+  const size_t o_t1 = ar.take((size_t)blocks_max * 2 * m_pad * std::max(r1, 1) * 4);
+  const size_t o_t2 = ar.take((size_t)blocks_max * m_pad * std::max(r2, 1) * 4);
+  const size_t o_pa1 = ar.take(GroupedWs<NT, 2>::lorc_bytes(blocks_max, d, r1));
+  const size_t o_pa2 = ar.take(GroupedWs<NT, 1>::lorc_bytes(blocks_max, f_max, r2));
+  const size_t o_ws = ar.take(std::max(GroupedWs<NT, 2>::ws_bytes(sms), GroupedWs<NT, 1>::ws_bytes(sms)));
+  const size_t o_full1 = ar.take(GroupedWs<NT, 2>::full_bytes(slabs1));
+  const size_t o_full2 = ar.take(GroupedWs<NT, 1>::full_bytes(slabs2));
+  const int64_t n_zero = 4 * blocks_max;
   const size_t o_zero = ar.take((size_t)n_zero * 4);
   const size_t o_Y = ar.take((size_t)(m * K + S * m) * d * 4);
   void* mem = nullptr;
@@ -767,9 +801,7 @@ milo_status moe_run(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype, co
   uint8_t* base = static_cast<uint8_t*>(mem);
   int32_t* np = reinterpret_cast<int32_t*>(base + o_np);
   int32_t* zero = reinterpret_cast<int32_t*>(base + o_zero);
-  int32_t* cnt1 = zero;
-  int32_t* cnt2 = zero + n_cnt1;
-  int32_t* tc1 = cnt2 + n_cnt2;
+  int32_t* tc1 = zero;
   int32_t* tc2 = tc1 + 2 * blocks_max;
 
   MoeRouteArgs ra{};
@@ -795,64 +827,28 @@ milo_status moe_run(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype, co
   ra.h_block_bytes = h_block;
   ra.t1_pool = reinterpret_cast<float*>(base + o_t1);
   ra.t2_pool = reinterpret_cast<float*>(base + o_t2);
-  ra.rank1_max = r1;
-  ra.rank2_max = r2;
+  ra.rank1_max = std::max(r1, 1);
+  ra.rank2_max = std::max(r2, 1);
   ra.Y = reinterpret_cast<float*>(base + o_Y);
   ra.zero_ptr = zero;
   ra.zero_count = n_zero;
+  milo_status st = MILO_OK;
   cudaError_t e = launch(moe_route_kernel, dim3(1), dim3(kRouteThreads), 0, stream, true, ra);
   if (e == cudaSuccess)
     e = launch(moe_gather_kernel, dim3((unsigned)blocks_max), dim3(256), 0, stream, true, x,
                x_dtype, d, K, m, (const int32_t*)ra.elist, (const int32_t*)ra.block_start,
                (const int32_t*)ra.block_expert, (const int32_t*)ra.n_p1, E, m_pad, ra.act_pool,
                (const GemvProblem*)ra.p1);
-  if (e == cudaSuccess && moe->rank1_max > 0) {
-    LorcArgs la{};
-    la.problems = ra.p1;
-    la.n_problems = ra.n_p1;
-    la.partial = reinterpret_cast<float*>(base + o_pa1);
-    la.counters = tc1;
-    la.m_pad = m_pad;
-    la.chunks = chunks1;
-    la.rank_max = r1;
-    ProfScope ps(kProfLorc, stream);
-    e = launch(lorc_t_kernel, dim3((unsigned)(blocks_max * 2), chunks1), dim3(32 * kLorcWarps), 0,
-               stream, true, la);
-  }
-  milo_status st = MILO_OK;
   if (e != cudaSuccess) st = fail(MILO_ERR_CUDA, "launch failed: %s", cudaGetErrorString(e));
-  if (st == MILO_OK) {
-    GemvArgs ga{};
-    ga.problems = ra.p1;
-    ga.n_problems = ra.n_p1;
-    ga.ws = reinterpret_cast<float*>(base + o_ws);
-    ga.counters = cnt1;
-    ProfScope ps(kProfGemv1, stream);
-    st = launch_gemv<NT, 2>(ga, stream, sms, true);
-  }
-  if (st == MILO_OK && moe->rank2_max > 0) {
-    LorcArgs la{};
-    la.problems = ra.p2;
-    la.n_problems = ra.n_p2;
-    la.partial = reinterpret_cast<float*>(base + o_pa2);
-    la.counters = tc2;
-    la.m_pad = m_pad;
-    la.chunks = chunks2;
-    la.rank_max = r2;
-    ProfScope ps(kProfLorc, stream);
-    e = launch(lorc_t_kernel, dim3((unsigned)(blocks_max * 2), chunks2), dim3(32 * kLorcWarps), 0,
-               stream, true, la);
-    if (e != cudaSuccess) st = fail(MILO_ERR_CUDA, "launch failed: %s", cudaGetErrorString(e));
-  }
-  if (st == MILO_OK) {
-    GemvArgs ga{};
-    ga.problems = ra.p2;
-    ga.n_problems = ra.n_p2;
-    ga.ws = reinterpret_cast<float*>(base + o_ws);
-    ga.counters = cnt2;
-    ProfScope ps(kProfGemv2, stream);
-    st = launch_gemv<NT, 1>(ga, stream, sms, true);
-  }
+  float* ws = reinterpret_cast<float*>(base + o_ws);
+  if (st == MILO_OK)
+    st = run_grouped<NT, 2>(ra.p1, ra.n_p1, blocks_max, slabs1, d, r1, ws,
+                            reinterpret_cast<float*>(base + o_full1),
+                            reinterpret_cast<float*>(base + o_pa1), tc1, stream, sms, kProfGemv1);
+  if (st == MILO_OK)
+    st = run_grouped<NT, 1>(ra.p2, ra.n_p2, blocks_max, slabs2, f_max, r2, ws,
+                            reinterpret_cast<float*>(base + o_full2),
+                            reinterpret_cast<float*>(base + o_pa2), tc2, stream, sms, kProfGemv2);
   if (st == MILO_OK) {
     const int64_t total = m * (d / 4);
     const int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)sms * 8);
