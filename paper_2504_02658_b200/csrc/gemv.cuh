@@ -19,11 +19,14 @@
 // The warp de-quantizes a macro tile in registers (bit-exact binary16 FMA, see
 // layout.cuh) and issues mma.m16n8k16 with W^T as the A operand.
 //
-// A warp range is cut into segments at slab boundaries.  Each segment's fp32
-// partial (64 x m_pad per matrix) goes to ws[warp][0] (first segment),
-// ws[warp][1] (last segment) or full[slab] (a middle segment, which is always a
-// whole slab).  gemv_epilogue_kernel then sums each slab's contributors in
-// warp order (deterministic: depends only on T and GW), adds t V, and stores.
+// A warp range is cut into segments at slab boundaries.  A segment covering a
+// whole slab is finished in registers.  Otherwise its fp32 partial (64 x m_pad
+// per matrix) goes to ws[warp][0] (first segment of the warp) or ws[warp][1]
+// (last segment) and the warp bumps the slab's counter; the last contributor
+// re-reads all partials, sums them in warp order (deterministic: depends only
+// on T and GW, never on timing), resets the counter and runs the epilogue:
+// + t V (LoRC, t = A U from lorc_t_kernel, which completes before this grid
+// starts), then SwiGLU -> binary16 act tiles of the next GEMM, or row stores.
 #pragma once
 #include <cstdint>
 #include <cuda_fp16.h>
@@ -63,8 +66,8 @@ struct GemvArgs {
   const int32_t* n_problems;  // device scalar (problem tables may be built on device)
   float* ws;                  // [GW][2][NMAT][64][m_pad] segment partials
   float* full;                // [slabs][NMAT][64][m_pad] whole-slab partials
+  int32_t* counters;          // one per slab, zero on entry, restored to zero
   int32_t gw;                 // total warps of the GEMM grid (grid * GemvCfg::kWarps)
-  int32_t pdl_trigger_early;  // let the next grid (e.g. the t = A U kernel) co-run
 };
 
 template <int NT, int NMAT>
@@ -78,7 +81,9 @@ struct GemvCfg {
   static constexpr int kSlotBytes = kSlotW + kMPad * 64;
   static constexpr int kWarpBytes = kSlots * kSlotBytes;
   static constexpr int kPartFloats = NMAT * 64 * kMPad;
-  static constexpr int kBytes = kWarps * kWarpBytes + kWarps * kSlots * 8 +
+  static constexpr int kScratchFloats = 64 * (kMPad + 1);  // per-warp epilogue scratch
+  static constexpr int kBytes = kWarps * kWarpBytes + kWarps * kScratchFloats * 4 +
+                                kWarps * kSlots * 8 +
                                 2 * (kMaxProblems + 1) * 4 + 64;
 };
 
@@ -132,6 +137,134 @@ __device__ __forceinline__ float* partial_ptr(float* ws, float* full, int64_t gw
   return full + (int64_t)slab_id * part_floats;          // middle: a whole slab
 }
 
+// Epilogue of one slab on the summed accumulator fragments of a warp.  Lane
+// (g, q) holds, per matrix, i in 0..3, nt, e in 0..3:
+//   column n = 16 i + g + 8 (e >> 1), row = 8 nt + 2 q + (e & 1).
+// 1) compensator: acc += t[row, :] . V^T[n0 + n, :]  (v_real, lowrank.cpp:24-32:
+//    step = s * (2/7), v = step * (c - 4), or real f32 V)
+// 2) kSwigluAct: h = silu(c1) * c3 -> binary16 act tiles (k' = n) of the next
+//    GEMM (pairs along k' formed with a shuffle); kStoreRows: f32/f16 rows.
+template <int NT, int NMAT>
+__device__ __forceinline__ void slab_epilogue(float (&acc)[NMAT][4][NT][4], const GemvProblem& pr,
+                                              int n0, int g, int q, int lane, float* scratch) {
+  constexpr int kMPad = 8 * NT;
+  const int rows = min(pr.m, kMPad);
+#pragma unroll
+  for (int mat = 0; mat < NMAT; ++mat) {
+    const int rank = pr.rank[mat];
+    const float* tt = pr.t[mat];
+    if (rank <= 0 || tt == nullptr) continue;
+    // Lane -> columns (2 lane, 2 lane + 1), every valid row: m x 2 x rank MACs
+    // per lane (no work on padding rows), through a per-warp smem scratch
+    // [64][m_pad] back into the MMA fragment layout.
+    const uint8_t* vc = pr.vcodes[mat];
+    const float* vs = pr.vscales[mat];
+    const float* vr = pr.vreal[mat];
+    const int gpr = pr.vgpr[mat];
+    const int64_t nA = n0 + 2 * lane, nB = nA + 1;
+    float cA[kMPad], cB[kMPad];
+#pragma unroll
+    for (int r = 0; r < kMPad; ++r) cA[r] = cB[r] = 0.0f;
+    int j = 0;
+    if (vc && (rank & 7) == 0) {
+      for (; j < rank; j += 8) {  // 8 rank columns per step, one 8-byte code load per column
+        const uint2 wa = __ldg(reinterpret_cast<const uint2*>(vc + nA * rank + j));
+        const uint2 wb = __ldg(reinterpret_cast<const uint2*>(vc + nB * rank + j));
+        const float sa = __ldg(vs + nA * gpr + (j >> 6)) * (2.0f / 7.0f);
+        const float sb = __ldg(vs + nB * gpr + (j >> 6)) * (2.0f / 7.0f);
+        float va[8], vb[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {  // (float)c - 4 exactly via the 2^23 magic
+          const uint32_t ca = ((u < 4 ? wa.x : wa.y) >> (8 * (u & 3))) & 0xFFu;
+          const uint32_t cb = ((u < 4 ? wb.x : wb.y) >> (8 * (u & 3))) & 0xFFu;
+          va[u] = sa * (__int_as_float(0x4B000000 | ca) - 8388612.0f);
+          vb[u] = sb * (__int_as_float(0x4B000000 | cb) - 8388612.0f);
+        }
+#pragma unroll
+        for (int r = 0; r < kMPad; ++r) {
+          if (r < rows) {
+            const float4 t0 = *reinterpret_cast<const float4*>(tt + r * rank + j);
+            const float4 t1 = *reinterpret_cast<const float4*>(tt + r * rank + j + 4);
+            const float tv[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              cA[r] += tv[u] * va[u];
+              cB[r] += tv[u] * vb[u];
+            }
+          }
+        }
+      }
+    }
+    for (; j < rank; ++j) {
+      float va, vb;
+      if (vc) {
+        va = vs[nA * gpr + (j >> 6)] * (2.0f / 7.0f) * ((float)vc[nA * rank + j] - 4.0f);
+        vb = vs[nB * gpr + (j >> 6)] * (2.0f / 7.0f) * ((float)vc[nB * rank + j] - 4.0f);
+      } else {
+        va = vr[nA * rank + j];
+        vb = vr[nB * rank + j];
+      }
+#pragma unroll
+      for (int r = 0; r < kMPad; ++r)
+        if (r < rows) {
+          cA[r] += tt[r * rank + j] * va;
+          cB[r] += tt[r * rank + j] * vb;
+        }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < kMPad; ++r) {
+      scratch[(2 * lane) * (kMPad + 1) + r] = cA[r];
+      scratch[(2 * lane + 1) * (kMPad + 1) + r] = cB[r];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int n = 16 * i + g + 8 * (e >> 1), row = 8 * nt + 2 * q + (e & 1);
+          acc[mat][i][nt][e] += scratch[n * (kMPad + 1) + row];
+        }
+  }
+  if (pr.kind == kStoreRows) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int row = 8 * nt + 2 * q + (e & 1);
+          if (row >= pr.m) continue;
+          const int orow = pr.row_map ? pr.row_map[row] : row;
+          const int64_t off = (int64_t)orow * pr.ldo + n0 + 16 * i + g + 8 * (e >> 1);
+          if (pr.out_dtype == 0)
+            reinterpret_cast<float*>(pr.out)[off] = acc[0][i][nt][e];
+          else
+            reinterpret_cast<__half*>(pr.out)[off] = __float2half_rn(acc[0][i][nt][e]);
+        }
+  } else {
+    uint32_t* outw = reinterpret_cast<uint32_t*>(pr.out);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int row = 8 * nt + 2 * q + (e & 1);
+          const float a = acc[0][i][nt][e];
+          float h = silu_f(a) * acc[NMAT - 1][i][nt][e];
+          if (row >= pr.m) h = 0.0f;
+          const float h_next = __shfl_down_sync(0xffffffffu, h, 4);  // column n + 1 (g + 1)
+          if ((g & 1) == 0) {
+            const int n = n0 + 16 * i + g + 8 * (e >> 1);
+            outw[act_word(kMPad, row, n)] = h2_as_u32(__floats2half2_rn(h, h_next));
+          }
+        }
+  }
+}
+
 template <int NT, int NMAT>
 __global__ void __launch_bounds__(32 * GemvCfg<NT, NMAT>::kWarps, 1)
     gemv_w3a16_kernel(GemvArgs args) {
@@ -146,6 +279,7 @@ __global__ void __launch_bounds__(32 * GemvCfg<NT, NMAT>::kWarps, 1)
   int32_t* pre_u = reinterpret_cast<int32_t*>(smem + kWarpsPerCta * CF::kWarpBytes +
                                               kWarpsPerCta * kSlots * 8);
   int32_t* pre_s = pre_u + kMaxProblems + 1;
+  float* scratch = reinterpret_cast<float*>(pre_s + kMaxProblems + 1) + warp * CF::kScratchFloats;
 
   if (lane == 0)
     for (int s = 0; s < kSlots; ++s) mbar_init(&bars[s], 1);
@@ -154,42 +288,63 @@ __global__ void __launch_bounds__(32 * GemvCfg<NT, NMAT>::kWarps, 1)
   const int P = min(*args.n_problems, kMaxProblems);
   if (warp == 0) problem_prefix(args.problems, P, pre_u, pre_s, lane);
   __syncthreads();
-  if (args.pdl_trigger_early) pdl_launch_dependents();
 
   const int64_t T = pre_u[P];
   const int64_t G = min((int64_t)args.gw, T);
   const int64_t gw = (int64_t)blockIdx.x * kWarpsPerCta + warp;
   if (gw >= G) return;
   const int64_t start = range_start(gw, T, G), end = range_start(gw + 1, T, G);
+  int p0 = 0;
+  while (pre_u[p0 + 1] <= start) ++p0;
 
-  // ---- per-warp TMA pipeline (lane 0 is the producer of its own warp) ----
-  int pp = 0;
-  while (pre_u[pp + 1] <= start) ++pp;
-  int64_t ppos = start;
+  // ---- per-warp TMA pipeline: lane 0 is the producer of its own warp ----
+  // Producer cursor advanced incrementally (no divisions, one problem-struct
+  // load per problem change): tile pointers are slab-contiguous along k.
+  int pp = p0, p_kt = 0, p_kts = 1;
+  const uint8_t* p_w[NMAT];
+  const uint8_t* p_act = nullptr;
+  const uint8_t* p_act0 = nullptr;
+  int32_t p_left = (int32_t)(end - start);
+  auto load_problem = [&](int prob, int64_t rel) {
+    const GemvProblem& pr = args.problems[prob];
+    p_kts = pr.k / kTileK;
+    const int64_t s = rel / p_kts;
+    p_kt = (int)(rel - s * p_kts);
+#pragma unroll
+    for (int mat = 0; mat < NMAT; ++mat) p_w[mat] = pr.w[mat] + rel * kTileBytes;
+    p_act0 = pr.act;
+    p_act = pr.act + p_kt * (kMPad * 64);
+  };
   auto issue = [&](int slot) {
-    while (pre_u[pp + 1] <= ppos) ++pp;
-    const GemvProblem& pr = args.problems[pp];
-    const int kts = pr.k / kTileK;
-    const int64_t rel = ppos - pre_u[pp];
-    const int64_t s = rel / kts, kt = rel - s * kts;
     uint8_t* dst = ring + slot * CF::kSlotBytes;
     mbar_arrive_expect_tx(&bars[slot], CF::kSlotBytes);
 #pragma unroll
-    for (int mat = 0; mat < NMAT; ++mat)
-      bulk_g2s(dst + mat * kTileBytes, pr.w[mat] + (s * kts + kt) * kTileBytes, kTileBytes,
-               &bars[slot]);
-    bulk_g2s(dst + CF::kSlotW, pr.act + kt * (kMPad * 64), kMPad * 64, &bars[slot]);
-    ++ppos;
+    for (int mat = 0; mat < NMAT; ++mat) {
+      bulk_g2s(dst + mat * kTileBytes, p_w[mat], kTileBytes, &bars[slot]);
+      p_w[mat] += kTileBytes;
+    }
+    bulk_g2s(dst + CF::kSlotW, p_act, kMPad * 64, &bars[slot]);
+    p_act += kMPad * 64;
+    if (--p_left > 0 && ++p_kt == p_kts) {
+      p_kt = 0;
+      p_act = p_act0;
+      if (p_w[0] == args.problems[pp].w[0] + (int64_t)(pre_u[pp + 1] - pre_u[pp]) * kTileBytes) {
+        ++pp;  // next problem (skip empty ones)
+        while (pre_u[pp + 1] == pre_u[pp]) ++pp;
+        load_problem(pp, 0);
+      }
+    }
   };
-  if (lane == 0)
-    for (int s = 0; s < kSlots && ppos < end; ++s) issue(s);
+  if (lane == 0) {
+    load_problem(p0, start - pre_u[p0]);
+    for (int s = 0; s < kSlots && p_left > 0; ++s) issue(s);
+  }
 
   const int g = lane >> 2, q = lane & 3;
-  int p = 0;
-  while (pre_u[p + 1] <= start) ++p;
   int slot = 0;
   uint32_t phase = 0;
   int64_t pos = start;
+  int p = p0;
   while (pos < end) {
     while (pre_u[p + 1] <= pos) ++p;
     const GemvProblem& pr = args.problems[p];
@@ -209,7 +364,7 @@ __global__ void __launch_bounds__(32 * GemvCfg<NT, NMAT>::kWarps, 1)
 #pragma unroll
           for (int e = 0; e < 4; ++e) acc[a][i][nt][e] = 0.0f;
 
-    for (; pos < seg_end; ++pos) {
+    for (int32_t left = (int32_t)(seg_end - pos); left > 0; --left) {
       mbar_wait(&bars[slot], phase);
       const uint8_t* st = ring + slot * CF::kSlotBytes;
       const uint32_t* act = reinterpret_cast<const uint32_t*>(st + CF::kSlotW);
@@ -244,158 +399,73 @@ __global__ void __launch_bounds__(32 * GemvCfg<NT, NMAT>::kWarps, 1)
               mma_16816(acc[mat][i][nt], &wv[4 * i], bf[j][nt][0], bf[j][nt][1]);
         }
       }
+      // Every LDS of this slot has been consumed by the MMAs above, so the slot
+      // can be refilled once all lanes are past this point.
       __syncwarp();
-      if (lane == 0 && ppos < end) {
-        fence_proxy_async();  // generic reads of this slot before the async overwrite
-        issue(slot);
-      }
+      if (lane == 0 && p_left > 0) issue(slot);
       if (++slot == kSlots) { slot = 0; phase ^= 1; }
     }
+    const int64_t seg_begin = pos;
+    pos = seg_end;
 
-    // ---- segment partial -> ws / full ([mat][n 64][m_pad]) ----
-    float* dst = partial_ptr(args.ws, args.full, gw, T, G, sb, se, pre_s[p] + (int)s,
-                             CF::kPartFloats);
+    // ---- fix-up ----
+    // Whole slab in this warp: finish in registers.  Otherwise the slab's first
+    // contributor w0 (for which the slab is its LAST segment, reached at the
+    // end of its range) is the finisher: every other contributor stores its
+    // partial and releases a counter increment without waiting; w0 waits for
+    // the count, adds the others' partials to its own registers in warp order
+    // (deterministic) and runs the epilogue.  A warp only ever waits at the end
+    // of its range, for warps that never wait: no deadlock.
+    const int slab_id = pre_s[p] + (int)s;
+    if (!(seg_begin == sb && seg_end == se)) {
+      const int64_t w0 = owner_of(sb, T, G), w1 = owner_of(se - 1, T, G);
+      if (gw != w0) {
+        // segment partial -> ws ([mat][n 64][m_pad]), fragment order
+        float* dst = partial_ptr(args.ws, args.full, gw, T, G, sb, se, slab_id, CF::kPartFloats);
 #pragma unroll
-    for (int mat = 0; mat < NMAT; ++mat)
+        for (int mat = 0; mat < NMAT; ++mat)
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+          for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          float* d0 = dst + (mat * 64 + 16 * i + g) * kMPad + 8 * nt + 2 * q;
-          *reinterpret_cast<float2*>(d0) = make_float2(acc[mat][i][nt][0], acc[mat][i][nt][1]);
-          *reinterpret_cast<float2*>(d0 + 8 * kMPad) =
-              make_float2(acc[mat][i][nt][2], acc[mat][i][nt][3]);
-        }
-  }
-  if (!args.pdl_trigger_early) pdl_launch_dependents();
-}
-
-// ---------------------------------------------------------------------------
-// Fix-up / epilogue: one CTA (256 threads) per slab.  Sums contributors in
-// warp order, adds the compensator term t V (v_real, lowrank.cpp:24-32), then
-// stores rows (f32/f16) or SwiGLU -> binary16 act tiles of the next GEMM.
-// ---------------------------------------------------------------------------
-template <int NT, int NMAT>
-__global__ void __launch_bounds__(256) gemv_epilogue_kernel(GemvArgs args) {
-  using CF = GemvCfg<NT, NMAT>;
-  constexpr int kMPad = CF::kMPad;
-  __shared__ int32_t pre_u[kMaxProblems + 1];
-  __shared__ int32_t pre_s[kMaxProblems + 1];
-  __shared__ float vals[NMAT][64][kMPad + 1];
-  pdl_wait();
-  const int P = min(*args.n_problems, kMaxProblems);
-  if (threadIdx.x < 32) problem_prefix(args.problems, P, pre_u, pre_s, threadIdx.x);
-  __syncthreads();
-  const int slab_id = blockIdx.x;
-  if (slab_id >= pre_s[P]) return;
-  int lo = 0, hi = P - 1;  // problem of this slab (binary search over pre_s)
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (pre_s[mid] <= slab_id) lo = mid; else hi = mid - 1;
-  }
-  const int p = lo;
-  const GemvProblem& pr = args.problems[p];
-  const int kts = pr.k / kTileK;
-  const int s = slab_id - pre_s[p];
-  const int64_t T = pre_u[P];
-  const int64_t G = min((int64_t)args.gw, T);
-  const int64_t sb = (int64_t)pre_u[p] + (int64_t)s * kts, se = sb + kts;
-  const int64_t w0 = owner_of(sb, T, G), w1 = owner_of(se - 1, T, G);
-  constexpr int kMaxContrib = 512;
-  __shared__ const float* contrib[kMaxContrib];
-  const int nc = (int)(w1 - w0 + 1 < kMaxContrib ? w1 - w0 + 1 : kMaxContrib);  // <= kts
-  for (int c = threadIdx.x; c < nc; c += blockDim.x)
-    contrib[c] = partial_ptr(args.ws, args.full, w0 + c, T, G, sb, se, slab_id, CF::kPartFloats);
-  __syncthreads();
-  for (int v = threadIdx.x; v < CF::kPartFloats; v += blockDim.x) {
-    float sum = 0.0f;
-    for (int c = 0; c < nc; ++c) sum += contrib[c][v];  // warp order: deterministic
-    const int mat = v / (64 * kMPad), rem = v % (64 * kMPad);
-    vals[mat][rem / kMPad][rem % kMPad] = sum;
-  }
-  __syncthreads();
-  const int n0 = s * kTileN;
-  // compensator: vals[:, col] += t (rows x rank) . V^T[col, :], rank in chunks
-  // of kRC staged in smem (t rows and the de-quantized V^T slab).
-  constexpr int kRC = 64;
-  __shared__ float s_t[kMPad][kRC];
-  __shared__ float s_v[64][kRC + 1];
-#pragma unroll
-  for (int mat = 0; mat < NMAT; ++mat) {
-    const int rank = pr.rank[mat];
-    if (rank > 0 && pr.t[mat] != nullptr) {
-      const int col = threadIdx.x & 63, rh = threadIdx.x >> 6;  // 4 row groups
-      constexpr int kRowsPer = (kMPad + 3) / 4;
-      const uint8_t* vc = pr.vcodes[mat];
-      const float* vs = pr.vscales[mat];
-      const float* vr = pr.vreal[mat];
-      const int gpr = pr.vgpr[mat];
-      const float* tt = pr.t[mat];
-      const int rows = min(pr.m, kMPad);
-      float add[kRowsPer];
-#pragma unroll
-      for (int r = 0; r < kRowsPer; ++r) add[r] = 0.0f;
-      for (int jb = 0; jb < rank; jb += kRC) {
-        const int jn = min(kRC, rank - jb);
-        for (int v = threadIdx.x; v < kMPad * kRC; v += blockDim.x) {
-          const int r = v / kRC, j = v % kRC;
-          s_t[r][j] = (r < rows && j < jn) ? tt[r * rank + jb + j] : 0.0f;
-        }
-        for (int v = threadIdx.x; v < 64 * kRC; v += blockDim.x) {
-          const int nn = v / kRC, j = v % kRC;
-          float vv = 0.0f;
-          if (j < jn) {
-            const int64_t n = n0 + nn;
-            if (vc) {  // v_real (lowrank.cpp:24-32): step = s * (2/7), v = step * (c - 4)
-              const float step = vs[n * gpr + ((jb + j) >> 6)] * (2.0f / 7.0f);
-              vv = step * ((float)vc[n * rank + jb + j] - 4.0f);
-            } else {
-              vv = vr[n * rank + jb + j];
+            for (int nt = 0; nt < NT; ++nt) {
+              float* d0 = dst + (mat * 64 + 16 * i + g) * kMPad + 8 * nt + 2 * q;
+              __stcg(reinterpret_cast<float2*>(d0), make_float2(acc[mat][i][nt][0], acc[mat][i][nt][1]));
+              __stcg(reinterpret_cast<float2*>(d0 + 8 * kMPad),
+                     make_float2(acc[mat][i][nt][2], acc[mat][i][nt][3]));
             }
-          }
-          s_v[nn][j] = vv;
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence();  // release this warp's partial
+          atomicAdd(&args.counters[slab_id], 1);
         }
-        __syncthreads();
-#pragma unroll 8
-        for (int j = 0; j < jn; ++j) {
-          const float vv = s_v[col][j];
+        continue;
+      }
+      if (lane == 0) {
+        const int need = (int)(w1 - w0);
+        while (ld_acquire_gpu(&args.counters[slab_id]) < need) __nanosleep(64);
+        args.counters[slab_id] = 0;  // every increment has landed: ready for the next launch
+      }
+      __syncwarp();
+      for (int64_t w = w0 + 1; w <= w1; ++w) {
+        const float* src = partial_ptr(args.ws, args.full, w, T, G, sb, se, slab_id,
+                                       CF::kPartFloats);
 #pragma unroll
-          for (int r = 0; r < kRowsPer; ++r) add[r] += s_t[min(rh * kRowsPer + r, kMPad - 1)][j] * vv;
-        }
-        __syncthreads();
-      }
+        for (int mat = 0; mat < NMAT; ++mat)
 #pragma unroll
-      for (int r = 0; r < kRowsPer; ++r) {
-        const int row = rh * kRowsPer + r;
-        if (row < rows) vals[mat][col][row] += add[r];
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+              const float* s0 = src + (mat * 64 + 16 * i + g) * kMPad + 8 * nt + 2 * q;
+              const float2 a = __ldcg(reinterpret_cast<const float2*>(s0));
+              const float2 b = __ldcg(reinterpret_cast<const float2*>(s0 + 8 * kMPad));
+              acc[mat][i][nt][0] += a.x;
+              acc[mat][i][nt][1] += a.y;
+              acc[mat][i][nt][2] += b.x;
+              acc[mat][i][nt][3] += b.y;
+            }
       }
     }
-  }
-  __syncthreads();
-  if (pr.kind == kStoreRows) {
-    for (int v = threadIdx.x; v < kMPad * 64; v += blockDim.x) {
-      const int row = v >> 6, col = v & 63;
-      if (row >= pr.m) continue;
-      const int orow = pr.row_map ? pr.row_map[row] : row;
-      const float val = vals[0][col][row];
-      const int64_t off = (int64_t)orow * pr.ldo + n0 + col;
-      if (pr.out_dtype == 0)
-        reinterpret_cast<float*>(pr.out)[off] = val;
-      else
-        reinterpret_cast<__half*>(pr.out)[off] = __float2half_rn(val);
-    }
-  } else {
-    uint32_t* outw = reinterpret_cast<uint32_t*>(pr.out);
-    for (int v = threadIdx.x; v < kMPad * 32; v += blockDim.x) {
-      const int row = v >> 5, cp = (v & 31) * 2;
-      uint32_t packed = 0;
-      if (row < pr.m) {
-        const float h0 = silu_f(vals[0][cp][row]) * vals[NMAT - 1][cp][row];
-        const float h1 = silu_f(vals[0][cp + 1][row]) * vals[NMAT - 1][cp + 1][row];
-        packed = h2_as_u32(__floats2half2_rn(h0, h1));
-      }
-      outw[act_word(kMPad, row, n0 + cp)] = packed;
-    }
+    slab_epilogue<NT, NMAT>(acc, pr, (int)s * kTileN, g, q, lane, scratch);
   }
   pdl_launch_dependents();
 }

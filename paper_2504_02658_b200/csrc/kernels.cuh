@@ -208,137 +208,4 @@ __global__ void prep_linear_kernel(LinearPrep a) {
   pdl_launch_dependents();
 }
 
-// ---------------------------------------------------------------------------
-// Compensator product t = A_f16 U for every (problem, matrix) with rank > 0.
-// U is the reference's u_real (lowrank.cpp:19-22): symm-int3 codes with f32
-// scales per 64-group along the rank (step = s*(2/7), u = step*(c-4)), or real
-// f32.  Grid (problem*2 + mat, k-chunk of kLorcChunk rows); the chunk's
-// activations and U rows are staged in smem, partial sums over the chunk are
-// reduced in a fixed order, and the last CTA of an item (atomic counter) sums
-// the chunks in order: deterministic.
-//
-// Launch order: GEMM -> this kernel (PDL) -> GEMM epilogue.  The GEMM triggers
-// its dependents right after its prologue, so this kernel co-runs with the
-// weight stream; every CTA ends with griddepcontrol.wait, so completion of this
-// grid implies completion of the GEMM for the epilogue that waits on it.
-// ---------------------------------------------------------------------------
-struct LorcArgs {
-  const GemvProblem* problems;
-  const int32_t* n_problems;
-  float* partial;                // [items][chunks][m_pad][rank_max]
-  int32_t* counters;             // one per item
-  int32_t m_pad;
-  int32_t chunks;
-  int32_t rank_max;
-};
-
-constexpr int kLorcThreads = 256;
-constexpr int kLorcChunk = 128;   // k rows per CTA
-constexpr int kLorcRanks = 32;    // rank columns per pass (x 8 k slices = 256 threads)
-
-__global__ void __launch_bounds__(kLorcThreads) lorc_t_kernel(LorcArgs a) {
-  __shared__ __align__(16) uint32_t s_act[16][kLorcChunk / 2 + 1];  // [row][k pair] f16x2
-  __shared__ float s_u[kLorcChunk][kLorcRanks + 1];
-  __shared__ float s_red[8][16][kLorcRanks + 1];
-  __shared__ int s_last;
-  const int item = blockIdx.x, chunk = blockIdx.y;
-  const int p = item >> 1, mat = item & 1;
-  const int tid = threadIdx.x;
-  if (p < *a.n_problems) {
-    const GemvProblem& pr = a.problems[p];
-    const int rank = pr.rank[mat];
-    float* tout = const_cast<float*>(pr.t[mat]);
-    const int k = pr.k, m = min(pr.m, a.m_pad), m_pad = a.m_pad;
-    const int k0 = chunk * kLorcChunk;
-    if (rank > 0 && tout != nullptr && k0 < k && chunk < a.chunks) {
-      const int kc = min(kLorcChunk, k - k0);
-      const uint8_t* uc = pr.ucodes[mat];
-      const float* us = pr.uscales[mat];
-      const float* ur = pr.ureal[mat];
-      const int gpr = (rank + 63) / 64;
-      const uint32_t* act = reinterpret_cast<const uint32_t*>(pr.act);
-#pragma unroll 4
-      for (int v = tid; v < 16 * (kLorcChunk / 2); v += kLorcThreads) {
-        const int r = v / (kLorcChunk / 2), kp = v % (kLorcChunk / 2);
-        s_act[r][kp] = (r < m && 2 * kp < kc) ? act[act_word(m_pad, r, k0 + 2 * kp)] : 0u;
-      }
-      float* part = a.partial + ((int64_t)item * a.chunks + chunk) * m_pad * a.rank_max;
-      // thread -> (rank column jj of the pass, k eighth kq)
-      const int jj = tid & 31, kq = tid >> 5;
-      for (int jb = 0; jb < rank; jb += kLorcRanks) {
-        const int jn = min(kLorcRanks, rank - jb);
-        __syncthreads();
-#pragma unroll 4
-        for (int v = tid; v < kLorcChunk * kLorcRanks; v += kLorcThreads) {
-          const int kk = v / kLorcRanks, j = v % kLorcRanks;
-          float u = 0.0f;
-          if (kk < kc && j < jn) {
-            const int64_t row = k0 + kk, col = jb + j;
-            if (uc) {
-              const float step = us[row * gpr + (col >> 6)] * (2.0f / 7.0f);
-              u = step * ((float)uc[row * rank + col] - 4.0f);
-            } else {
-              u = ur[row * rank + col];
-            }
-          }
-          s_u[kk][j] = u;
-        }
-        __syncthreads();
-        float acc[16];
-#pragma unroll
-        for (int r = 0; r < 16; ++r) acc[r] = 0.0f;
-        for (int kp = kq * (kLorcChunk / 16); kp < (kq + 1) * (kLorcChunk / 16); ++kp) {
-          const float u0 = s_u[2 * kp][jj], u1 = s_u[2 * kp + 1][jj];
-#pragma unroll
-          for (int r = 0; r < 16; ++r) {
-            const float2 av = __half22float2(u32_as_h2(s_act[r][kp]));
-            acc[r] += av.x * u0;
-            acc[r] += av.y * u1;
-          }
-        }
-#pragma unroll
-        for (int r = 0; r < 16; ++r) s_red[kq][r][jj] = acc[r];
-        __syncthreads();
-        for (int v = tid; v < m_pad * kLorcRanks; v += kLorcThreads) {
-          const int r = v / kLorcRanks, j = v % kLorcRanks;
-          if (j < jn)
-            part[r * a.rank_max + jb + j] =
-                ((s_red[0][r][j] + s_red[1][r][j]) + (s_red[2][r][j] + s_red[3][r][j])) +
-                ((s_red[4][r][j] + s_red[5][r][j]) + (s_red[6][r][j] + s_red[7][r][j]));
-        }
-      }
-      __syncthreads();
-      if (tid == 0) {
-        __threadfence();
-        const int nch = min(a.chunks, (k + kLorcChunk - 1) / kLorcChunk);
-        s_last = (atomicAdd(&a.counters[item], 1) == nch - 1);
-      }
-      __syncthreads();
-      if (s_last) {
-        __threadfence();
-        const int nch = min(a.chunks, (k + kLorcChunk - 1) / kLorcChunk);
-        const float* base = a.partial + (int64_t)item * a.chunks * m_pad * a.rank_max;
-        for (int v = tid; v < m_pad * rank; v += kLorcThreads) {
-          const int r = v / rank, j = v % rank;
-          const float* src = base + r * a.rank_max + j;
-          const int64_t stride = (int64_t)m_pad * a.rank_max;
-          float s = 0.0f;
-          int ch = 0;
-          for (; ch + 8 <= nch; ch += 8) {  // 8 independent loads in flight, summed in order
-            float x[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) x[u] = __ldcg(src + (ch + u) * stride);
-#pragma unroll
-            for (int u = 0; u < 8; ++u) s += x[u];
-          }
-          for (; ch < nch; ++ch) s += __ldcg(src + ch * stride);
-          tout[r * rank + j] = (r < m) ? s : 0.0f;
-        }
-        if (tid == 0) a.counters[item] = 0;
-      }
-    }
-  }
-  pdl_wait();  // see above: this grid completes only after the GEMM it co-ran with
-}
-
 }  // namespace milo_dev

@@ -13,6 +13,7 @@
 #include "../../include/milo_b200.h"
 #include "gemv.cuh"
 #include "kernels.cuh"
+#include "lorc.cuh"
 #include "moe.cuh"
 
 using namespace milo_dev;
@@ -450,17 +451,21 @@ struct GroupedWs {
   using CF = GemvCfg<NT, NMAT>;
   static size_t ws_bytes(int sms) { return (size_t)sms * CF::kWarps * 2 * CF::kPartFloats * 4; }
   static size_t full_bytes(int64_t slabs) { return (size_t)slabs * CF::kPartFloats * 4; }
-  static int lorc_chunks(int64_t k) { return (int)((k + kLorcChunk - 1) / kLorcChunk); }
+  // worst case chunk count: real (f32) U rows at the largest rank
+  static int lorc_chunks(int64_t k, int rank) {
+    return (int)((k + lorc_rows(std::max(rank, 1), 4) - 1) / lorc_rows(std::max(rank, 1), 4));
+  }
   static size_t lorc_bytes(int64_t problems, int64_t k, int rank) {
-    return (size_t)problems * 2 * lorc_chunks(k) * CF::kMPad * std::max(rank, 1) * 4;
+    return (size_t)problems * 2 * lorc_chunks(k, rank) * CF::kMPad * std::max(rank, 1) * 4;
   }
 };
 
-// GEMM (weights stream, partials) -> t = A U (co-runs, PDL) -> fix-up/epilogue.
+// t = A U (lorc_t_kernel, when any rank > 0) -> GEMM with in-kernel fix-up and
+// epilogue (+ t V, SwiGLU / store).  Both PDL-chained on `stream`.
 template <int NT, int NMAT>
 milo_status run_grouped(const GemvProblem* problems, const int32_t* n_problems,
-                        int64_t problems_max, int64_t slabs_max, int64_t k_max, int rank_max,
-                        float* ws, float* full, float* lorc_partial, int32_t* lorc_counters,
+                        int64_t problems_max, int64_t k_max, int rank_max, float* ws, float* full,
+                        int32_t* slab_counters, float* lorc_partial, int32_t* lorc_counters,
                         cudaStream_t stream, int sms, int prof_kind) {
   using CF = GemvCfg<NT, NMAT>;
   static thread_local int configured_dev = -1;
@@ -468,19 +473,8 @@ milo_status run_grouped(const GemvProblem* problems, const int32_t* n_problems,
   cudaGetDevice(&dev);
   if (configured_dev != dev) {
     CUDA_TRY(set_smem(gemv_w3a16_kernel<NT, NMAT>, CF::kBytes));
+    CUDA_TRY(set_smem(lorc_t_kernel, kLorcDynSmem));
     configured_dev = dev;
-  }
-  GemvArgs ga{};
-  ga.problems = problems;
-  ga.n_problems = n_problems;
-  ga.ws = ws;
-  ga.full = full;
-  ga.gw = sms * CF::kWarps;
-  ga.pdl_trigger_early = rank_max > 0 ? 1 : 0;
-  {
-    ProfScope ps(prof_kind, stream);
-    CUDA_TRY(launch(gemv_w3a16_kernel<NT, NMAT>, dim3(sms), dim3(32 * CF::kWarps), CF::kBytes,
-                    stream, true, ga));
   }
   if (rank_max > 0) {
     LorcArgs la{};
@@ -489,17 +483,22 @@ milo_status run_grouped(const GemvProblem* problems, const int32_t* n_problems,
     la.partial = lorc_partial;
     la.counters = lorc_counters;
     la.m_pad = CF::kMPad;
-    la.chunks = GroupedWs<NT, NMAT>::lorc_chunks(k_max);
+    la.chunks_max = GroupedWs<NT, NMAT>::lorc_chunks(k_max, rank_max);
     la.rank_max = rank_max;
     ProfScope ps(kProfLorc, stream);
-    CUDA_TRY(launch(lorc_t_kernel, dim3((unsigned)(problems_max * 2), la.chunks),
-                    dim3(kLorcThreads), 0, stream, true, la));
+    CUDA_TRY(launch(lorc_t_kernel, dim3((unsigned)(problems_max * 2), la.chunks_max),
+                    dim3(kLorcThreads), kLorcDynSmem, stream, true, la));
   }
-  {
-    ProfScope ps(kProfOther, stream);
-    CUDA_TRY(launch(gemv_epilogue_kernel<NT, NMAT>, dim3((unsigned)slabs_max), dim3(256), 0,
-                    stream, true, ga));
-  }
+  GemvArgs ga{};
+  ga.problems = problems;
+  ga.n_problems = n_problems;
+  ga.ws = ws;
+  ga.full = full;
+  ga.counters = slab_counters;
+  ga.gw = sms * CF::kWarps;
+  ProfScope ps(prof_kind, stream);
+  CUDA_TRY(launch(gemv_w3a16_kernel<NT, NMAT>, dim3(sms), dim3(32 * CF::kWarps), CF::kBytes,
+                  stream, true, ga));
   return MILO_OK;
 }
 
@@ -567,6 +566,7 @@ extern "C" milo_status milo_gemm_w3a16(const milo_weight* w, const milo_comp* co
     const size_t o_full = ar.take(full_b);
     const size_t o_part = ar.take(part_b);
     const size_t o_tc = ar.take((size_t)blocks * 2 * 4);
+    const size_t o_sc = ar.take((size_t)slabs * 4);
     void* mem = nullptr;
     CUDA_TRY(cudaMallocAsync(&mem, ar.size, stream));
     uint8_t* base = static_cast<uint8_t*>(mem);
@@ -601,8 +601,8 @@ extern "C" milo_status milo_gemm_w3a16(const milo_weight* w, const milo_comp* co
     lp.out_block_elems = (int64_t)m_pad * n;
     lp.problems = reinterpret_cast<GemvProblem*>(base + o_prob);
     lp.n_problems = reinterpret_cast<int32_t*>(base + o_np);
-    lp.counters = nullptr;
-    lp.n_counters = 0;
+    lp.counters = reinterpret_cast<int32_t*>(base + o_sc);
+    lp.n_counters = (int32_t)slabs;
     lp.t_counters = reinterpret_cast<int32_t*>(base + o_tc);
     lp.n_t_counters = blocks * 2;
     const int64_t prep_threads = (int64_t)blocks * m_pad * (k / 2);
@@ -616,10 +616,10 @@ extern "C" milo_status milo_gemm_w3a16(const milo_weight* w, const milo_comp* co
     float* full = reinterpret_cast<float*>(base + o_full);
     float* part = reinterpret_cast<float*>(base + o_part);
     int32_t* tc = lp.t_counters;
-    st = nt == 1 ? run_grouped<1, 1>(lp.problems, lp.n_problems, blocks, slabs, k, rank, ws, full,
-                                     part, tc, stream, props.sms, kProfGemv1)
-                 : run_grouped<2, 1>(lp.problems, lp.n_problems, blocks, slabs, k, rank, ws, full,
-                                     part, tc, stream, props.sms, kProfGemv1);
+    st = nt == 1 ? run_grouped<1, 1>(lp.problems, lp.n_problems, blocks, k, rank, ws, full,
+                                     lp.counters, part, tc, stream, props.sms, kProfGemv1)
+                 : run_grouped<2, 1>(lp.problems, lp.n_problems, blocks, k, rank, ws, full,
+                                     lp.counters, part, tc, stream, props.sms, kProfGemv1);
     cudaFreeAsync(mem, stream);
     if (st != MILO_OK) return st;
     done += mm;
@@ -793,7 +793,7 @@ milo_status moe_run(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype, co
   const size_t o_ws = ar.take(std::max(GroupedWs<NT, 2>::ws_bytes(sms), GroupedWs<NT, 1>::ws_bytes(sms)));
   const size_t o_full1 = ar.take(GroupedWs<NT, 2>::full_bytes(slabs1));
   const size_t o_full2 = ar.take(GroupedWs<NT, 1>::full_bytes(slabs2));
-  const int64_t n_zero = 4 * blocks_max;
+  const int64_t n_zero = 4 * blocks_max + slabs1 + slabs2;  // lorc + slab fix-up counters
   const size_t o_zero = ar.take((size_t)n_zero * 4);
   const size_t o_Y = ar.take((size_t)(m * K + S * m) * d * 4);
   void* mem = nullptr;
@@ -803,6 +803,8 @@ milo_status moe_run(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype, co
   int32_t* zero = reinterpret_cast<int32_t*>(base + o_zero);
   int32_t* tc1 = zero;
   int32_t* tc2 = tc1 + 2 * blocks_max;
+  int32_t* sc1 = tc2 + 2 * blocks_max;
+  int32_t* sc2 = sc1 + slabs1;
 
   MoeRouteArgs ra{};
   ra.ids = ids;
@@ -835,19 +837,19 @@ milo_status moe_run(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype, co
   milo_status st = MILO_OK;
   cudaError_t e = launch(moe_route_kernel, dim3(1), dim3(kRouteThreads), 0, stream, true, ra);
   if (e == cudaSuccess)
-    e = launch(moe_gather_kernel, dim3((unsigned)blocks_max), dim3(256), 0, stream, true, x,
+    e = launch(moe_gather_kernel, dim3((unsigned)blocks_max, m_pad), dim3(128), 0, stream, true, x,
                x_dtype, d, K, m, (const int32_t*)ra.elist, (const int32_t*)ra.block_start,
                (const int32_t*)ra.block_expert, (const int32_t*)ra.n_p1, E, m_pad, ra.act_pool,
                (const GemvProblem*)ra.p1);
   if (e != cudaSuccess) st = fail(MILO_ERR_CUDA, "launch failed: %s", cudaGetErrorString(e));
   float* ws = reinterpret_cast<float*>(base + o_ws);
   if (st == MILO_OK)
-    st = run_grouped<NT, 2>(ra.p1, ra.n_p1, blocks_max, slabs1, d, r1, ws,
-                            reinterpret_cast<float*>(base + o_full1),
+    st = run_grouped<NT, 2>(ra.p1, ra.n_p1, blocks_max, d, r1, ws,
+                            reinterpret_cast<float*>(base + o_full1), sc1,
                             reinterpret_cast<float*>(base + o_pa1), tc1, stream, sms, kProfGemv1);
   if (st == MILO_OK)
-    st = run_grouped<NT, 1>(ra.p2, ra.n_p2, blocks_max, slabs2, f_max, r2, ws,
-                            reinterpret_cast<float*>(base + o_full2),
+    st = run_grouped<NT, 1>(ra.p2, ra.n_p2, blocks_max, f_max, r2, ws,
+                            reinterpret_cast<float*>(base + o_full2), sc2,
                             reinterpret_cast<float*>(base + o_pa2), tc2, stream, sms, kProfGemv2);
   if (st == MILO_OK) {
     const int64_t total = m * (d / 4);

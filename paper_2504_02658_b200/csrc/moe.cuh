@@ -281,30 +281,35 @@ __global__ void moe_gather_kernel(const void* __restrict__ x, int32_t x_dtype, i
                                   const int32_t* __restrict__ block_expert,
                                   const int32_t* __restrict__ n_blocks, int32_t n_routed,
                                   int32_t m_pad, uint8_t* act_pool, const GemvProblem* __restrict__ p1) {
+  // grid (block, row): one row of one block per CTA, 16-byte chunks (8 binary16)
   pdl_wait();
-  const int blk = blockIdx.x;
+  const int blk = blockIdx.x, r = blockIdx.y;
   if (blk >= *n_blocks) return;
-  const GemvProblem& pr = p1[blk];
-  const int rows = pr.m;
-  const int32_t* list = elist + block_start[blk];
-  const bool shared = block_expert[blk] >= n_routed;
-  uint32_t* act = reinterpret_cast<uint32_t*>(act_pool + (int64_t)blk * (d / 32) * m_pad * 64);
-  const int64_t kw = d / 2;
-  for (int64_t i = threadIdx.x; i < (int64_t)m_pad * kw; i += blockDim.x) {
-    const int r = (int)(i / kw);
-    const int64_t w = i % kw;
-    __half2 v = __floats2half2_rn(0.0f, 0.0f);
-    if (r < rows) {
-      const int32_t entry = list[r];
-      const int64_t tok = shared ? (entry - m * K) % m : entry / K;
+  const int rows = p1[blk].m;
+  int32_t tok = -1;
+  if (r < rows) {
+    const int32_t entry = elist[block_start[blk] + r];
+    tok = block_expert[blk] >= n_routed ? (int32_t)((entry - m * K) % m) : entry / K;
+  }
+  uint4* act = reinterpret_cast<uint4*>(act_pool + (int64_t)blk * (d / 32) * m_pad * 64);
+  const int chunks = (int)(d / 8);  // 4 per 32-wide k tile
+  const int sw = (r >> 1) & 3;      // act-tile swizzle moves whole 16-byte chunks
+  for (int c = threadIdx.x; c < chunks; c += blockDim.x) {
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (tok >= 0) {
       if (x_dtype == 0) {
-        const float2 f = reinterpret_cast<const float2*>(x)[(tok * d) / 2 + w];
-        v = __floats2half2_rn(f.x, f.y);
+        const float4* src = reinterpret_cast<const float4*>(x) + ((int64_t)tok * d) / 4 + 2 * c;
+        const float4 a = src[0], b = src[1];
+        v.x = h2_as_u32(__floats2half2_rn(a.x, a.y));
+        v.y = h2_as_u32(__floats2half2_rn(a.z, a.w));
+        v.z = h2_as_u32(__floats2half2_rn(b.x, b.y));
+        v.w = h2_as_u32(__floats2half2_rn(b.z, b.w));
       } else {
-        v = reinterpret_cast<const __half2*>(x)[(tok * d) / 2 + w];
+        v = reinterpret_cast<const uint4*>(x)[((int64_t)tok * d) / 8 + c];
       }
     }
-    act[act_word(m_pad, r, (int)(2 * w))] = h2_as_u32(v);
+    const int kt = c >> 2, ch = c & 3;
+    act[(int64_t)kt * (m_pad * 4) + r * 4 + (ch ^ sw)] = v;
   }
   pdl_launch_dependents();
 }
