@@ -82,8 +82,7 @@ struct GemvCfg {
   static constexpr int kWarpBytes = kSlots * kSlotBytes;
   static constexpr int kPartFloats = NMAT * 64 * kMPad;
   static constexpr int kScratchFloats = 64 * (kMPad + 1);  // per-warp epilogue scratch
-  static constexpr int kBytes = kWarps * kWarpBytes + kWarps * kScratchFloats * 4 +
-                                kWarps * kSlots * 8 +
+  static constexpr int kBytes = kWarps * kWarpBytes + kWarps * kSlots * 8 +
                                 2 * (kMaxProblems + 1) * 4 + 64;
 };
 
@@ -279,7 +278,6 @@ __global__ void __launch_bounds__(32 * GemvCfg<NT, NMAT>::kWarps, 1)
   int32_t* pre_u = reinterpret_cast<int32_t*>(smem + kWarpsPerCta * CF::kWarpBytes +
                                               kWarpsPerCta * kSlots * 8);
   int32_t* pre_s = pre_u + kMaxProblems + 1;
-  float* scratch = reinterpret_cast<float*>(pre_s + kMaxProblems + 1) + warp * CF::kScratchFloats;
 
   if (lane == 0)
     for (int s = 0; s < kSlots; ++s) mbar_init(&bars[s], 1);
@@ -405,50 +403,87 @@ __global__ void __launch_bounds__(32 * GemvCfg<NT, NMAT>::kWarps, 1)
       if (lane == 0 && p_left > 0) issue(slot);
       if (++slot == kSlots) { slot = 0; phase ^= 1; }
     }
-    const int64_t seg_begin = pos;
     pos = seg_end;
 
-    // ---- fix-up ----
-    // Whole slab in this warp: finish in registers.  Otherwise the slab's first
-    // contributor w0 (for which the slab is its LAST segment, reached at the
-    // end of its range) is the finisher: every other contributor stores its
-    // partial and releases a counter increment without waiting; w0 waits for
-    // the count, adds the others' partials to its own registers in warp order
-    // (deterministic) and runs the epilogue.  A warp only ever waits at the end
-    // of its range, for warps that never wait: no deadlock.
-    const int slab_id = pre_s[p] + (int)s;
-    if (!(seg_begin == sb && seg_end == se)) {
-      const int64_t w0 = owner_of(sb, T, G), w1 = owner_of(se - 1, T, G);
-      if (gw != w0) {
-        // segment partial -> ws ([mat][n 64][m_pad]), fragment order
-        float* dst = partial_ptr(args.ws, args.full, gw, T, G, sb, se, slab_id, CF::kPartFloats);
+    // ---- segment partial -> ws / full ([mat][n 64][m_pad], fragment order) ----
+    // Plain stores: the fix-up kernel that reads them is the next grid.
+    float* dst = partial_ptr(args.ws, args.full, gw, T, G, sb, se, pre_s[p] + (int)s,
+                             CF::kPartFloats);
 #pragma unroll
-        for (int mat = 0; mat < NMAT; ++mat)
+    for (int mat = 0; mat < NMAT; ++mat)
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int nt = 0; nt < NT; ++nt) {
-              float* d0 = dst + (mat * 64 + 16 * i + g) * kMPad + 8 * nt + 2 * q;
-              __stcg(reinterpret_cast<float2*>(d0), make_float2(acc[mat][i][nt][0], acc[mat][i][nt][1]));
-              __stcg(reinterpret_cast<float2*>(d0 + 8 * kMPad),
-                     make_float2(acc[mat][i][nt][2], acc[mat][i][nt][3]));
-            }
-        __syncwarp();
-        if (lane == 0) {
-          __threadfence();  // release this warp's partial
-          atomicAdd(&args.counters[slab_id], 1);
+        for (int nt = 0; nt < NT; ++nt) {
+          float* d0 = dst + (mat * 64 + 16 * i + g) * kMPad + 8 * nt + 2 * q;
+          __stcg(reinterpret_cast<float2*>(d0), make_float2(acc[mat][i][nt][0], acc[mat][i][nt][1]));
+          __stcg(reinterpret_cast<float2*>(d0 + 8 * kMPad),
+                 make_float2(acc[mat][i][nt][2], acc[mat][i][nt][3]));
         }
-        continue;
-      }
-      if (lane == 0) {
-        const int need = (int)(w1 - w0);
-        while (ld_acquire_gpu(&args.counters[slab_id]) < need) __nanosleep(64);
-        args.counters[slab_id] = 0;  // every increment has landed: ready for the next launch
-      }
-      __syncwarp();
-      for (int64_t w = w0 + 1; w <= w1; ++w) {
-        const float* src = partial_ptr(args.ws, args.full, w, T, G, sb, se, slab_id,
-                                       CF::kPartFloats);
+  }
+  pdl_launch_dependents();
+}
+
+// ---------------------------------------------------------------------------
+// Fix-up + epilogue: one WARP per slab (8 per CTA).  Sums the slab's
+// contributor partials in warp order (deterministic), then slab_epilogue
+// (+ t V, SwiGLU / store).  Every contributor's loads for a slab are issued
+// before any is consumed.
+// ---------------------------------------------------------------------------
+constexpr int kEpiWarps = 8;
+
+template <int NT, int NMAT>
+__global__ void __launch_bounds__(32 * kEpiWarps) gemv_epilogue_kernel(GemvArgs args) {
+  using CF = GemvCfg<NT, NMAT>;
+  constexpr int kMPad = CF::kMPad;
+  __shared__ int32_t pre_u[kMaxProblems + 1];
+  __shared__ int32_t pre_s[kMaxProblems + 1];
+  __shared__ float scratch_all[kEpiWarps][CF::kScratchFloats];
+  pdl_wait();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int P = min(*args.n_problems, kMaxProblems);
+  if (warp == 0) problem_prefix(args.problems, P, pre_u, pre_s, lane);
+  __syncthreads();
+  const int slab_id = blockIdx.x * kEpiWarps + warp;
+  if (slab_id >= pre_s[P]) return;
+  int lo = 0, hi = P - 1;  // problem of this slab (binary search over pre_s)
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (pre_s[mid] <= slab_id) lo = mid; else hi = mid - 1;
+  }
+  const GemvProblem& pr = args.problems[lo];
+  const int kts = pr.k / kTileK;
+  const int s = slab_id - pre_s[lo];
+  const int64_t T = pre_u[P];
+  const int64_t G = min((int64_t)args.gw, T);
+  const int64_t sb = (int64_t)pre_u[lo] + (int64_t)s * kts, se = sb + kts;
+  const int64_t w0 = owner_of(sb, T, G), w1 = owner_of(se - 1, T, G);
+  const int g = lane >> 2, q = lane & 3;
+  // Contributor pointers first (lane c computes contributor w0 + c), then all
+  // lanes load every contributor's fragment values: for each chunk of up to
+  // 8 contributors the loads are issued before the in-order adds.
+  const int nc = (int)(w1 - w0 + 1);
+  float acc[NMAT][4][NT][4];
+#pragma unroll
+  for (int mat = 0; mat < NMAT; ++mat)
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[mat][i][nt][e] = 0.0f;
+  for (int c0 = 0; c0 < nc; c0 += 32) {
+    const float* myp = nullptr;
+    if (c0 + lane < nc)
+      myp = partial_ptr(args.ws, args.full, w0 + c0 + lane, T, G, sb, se, slab_id, CF::kPartFloats);
+    const int cn = min(32, nc - c0);
+    constexpr int kU = (NT * NMAT >= 4) ? 1 : (NT * NMAT == 2 ? 2 : 4);  // loads in flight
+    for (int cb = 0; cb < cn; cb += kU) {
+      float2 v[kU][NMAT][4][NT][2];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const float* src = reinterpret_cast<const float*>(
+            __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(myp), min(cb + u, cn - 1)));
 #pragma unroll
         for (int mat = 0; mat < NMAT; ++mat)
 #pragma unroll
@@ -456,17 +491,30 @@ __global__ void __launch_bounds__(32 * GemvCfg<NT, NMAT>::kWarps, 1)
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt) {
               const float* s0 = src + (mat * 64 + 16 * i + g) * kMPad + 8 * nt + 2 * q;
-              const float2 a = __ldcg(reinterpret_cast<const float2*>(s0));
-              const float2 b = __ldcg(reinterpret_cast<const float2*>(s0 + 8 * kMPad));
-              acc[mat][i][nt][0] += a.x;
-              acc[mat][i][nt][1] += a.y;
-              acc[mat][i][nt][2] += b.x;
-              acc[mat][i][nt][3] += b.y;
+              if (cb + u < cn) {
+                v[u][mat][i][nt][0] = __ldcg(reinterpret_cast<const float2*>(s0));
+                v[u][mat][i][nt][1] = __ldcg(reinterpret_cast<const float2*>(s0 + 8 * kMPad));
+              } else {
+                v[u][mat][i][nt][0] = v[u][mat][i][nt][1] = make_float2(0.0f, 0.0f);
+              }
             }
       }
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+#pragma unroll
+        for (int mat = 0; mat < NMAT; ++mat)
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+              acc[mat][i][nt][0] += v[u][mat][i][nt][0].x;
+              acc[mat][i][nt][1] += v[u][mat][i][nt][0].y;
+              acc[mat][i][nt][2] += v[u][mat][i][nt][1].x;
+              acc[mat][i][nt][3] += v[u][mat][i][nt][1].y;
+            }
     }
-    slab_epilogue<NT, NMAT>(acc, pr, (int)s * kTileN, g, q, lane, scratch);
   }
+  slab_epilogue<NT, NMAT>(acc, pr, s * kTileN, g, q, lane, scratch_all[warp]);
   pdl_launch_dependents();
 }
 

@@ -25,7 +25,7 @@ namespace milo_dev {
 
 constexpr int kLorcThreads = 256;
 constexpr int kLorcSmemU = 32 * 1024;  // bytes of U rows per chunk
-constexpr int kLorcMaxRows = 512;
+constexpr int kLorcMaxRows = 64;       // many small chunks: latency, not throughput, matters
 
 struct LorcArgs {
   const GemvProblem* problems;
@@ -148,22 +148,43 @@ __global__ void __launch_bounds__(kLorcThreads) lorc_t_kernel(LorcArgs a) {
   __syncthreads();
   if (!s_last) return;
   __threadfence();
+  // Sum the nch chunk partials of the m x rank valid values: `groups` thread
+  // groups each sum a contiguous run of chunks (8 loads in flight), then the
+  // group sums are added in group order (fixed: deterministic).
   const float* base = a.partial + (int64_t)item * a.chunks_max * m_pad * a.rank_max;
   const int64_t stride = (int64_t)m_pad * a.rank_max;
-  for (int v = tid; v < m_pad * rank; v += kLorcThreads) {
-    const int r = v / rank, j = v % rank;
-    const float* src = base + r * a.rank_max + j;
-    float s = 0.0f;
-    int ch = 0;
-    for (; ch + 8 <= nch; ch += 8) {  // 8 independent loads in flight, summed in order
-      float x[8];
+  float* s_grp = &s_red[0][0][0];  // reused: [8][256]
+  const int nv = m * rank;
+  // depends on rank (not m) so every row's summation order is independent of
+  // the batch size: padded and unpadded runs stay bit-identical
+  const int groups = max(1, min(8, kLorcThreads / rank));
+  const int per_pass = kLorcThreads / groups;
+  for (int vb = 0; vb < nv; vb += per_pass) {
+    const int vl = tid % per_pass, gi = tid / per_pass, v = vb + vl;
+    if (v < nv && gi < groups) {
+      const int r = v / rank, j = v % rank;
+      const float* src = base + r * a.rank_max + j;
+      const int c0 = gi * nch / groups, c1 = (gi + 1) * nch / groups;
+      float s = 0.0f;
+      int ch = c0;
+      for (; ch + 8 <= c1; ch += 8) {
+        float x[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) x[u] = __ldcg(src + (ch + u) * stride);
+        for (int u = 0; u < 8; ++u) x[u] = __ldcg(src + (ch + u) * stride);
 #pragma unroll
-      for (int u = 0; u < 8; ++u) s += x[u];
+        for (int u = 0; u < 8; ++u) s += x[u];
+      }
+      for (; ch < c1; ++ch) s += __ldcg(src + ch * stride);
+      s_grp[gi * 256 + vl] = s;
     }
-    for (; ch < nch; ++ch) s += __ldcg(src + ch * stride);
-    tout[r * rank + j] = (r < m) ? s : 0.0f;
+    __syncthreads();
+    if (tid < per_pass && vb + tid < nv) {
+      float s = 0.0f;
+      for (int gg = 0; gg < groups; ++gg) s += s_grp[gg * 256 + tid];
+      const int v = vb + tid;
+      tout[(v / rank) * rank + v % rank] = s;
+    }
+    __syncthreads();
   }
   if (tid == 0) a.counters[item] = 0;
 }

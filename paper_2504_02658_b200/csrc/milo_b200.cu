@@ -464,7 +464,8 @@ struct GroupedWs {
 // epilogue (+ t V, SwiGLU / store).  Both PDL-chained on `stream`.
 template <int NT, int NMAT>
 milo_status run_grouped(const GemvProblem* problems, const int32_t* n_problems,
-                        int64_t problems_max, int64_t k_max, int rank_max, float* ws, float* full,
+                        int64_t problems_max, int64_t slabs_max, int64_t k_max, int rank_max,
+                        float* ws, float* full,
                         int32_t* slab_counters, float* lorc_partial, int32_t* lorc_counters,
                         cudaStream_t stream, int sms, int prof_kind) {
   using CF = GemvCfg<NT, NMAT>;
@@ -496,9 +497,15 @@ milo_status run_grouped(const GemvProblem* problems, const int32_t* n_problems,
   ga.full = full;
   ga.counters = slab_counters;
   ga.gw = sms * CF::kWarps;
-  ProfScope ps(prof_kind, stream);
-  CUDA_TRY(launch(gemv_w3a16_kernel<NT, NMAT>, dim3(sms), dim3(32 * CF::kWarps), CF::kBytes,
-                  stream, true, ga));
+  {
+    ProfScope ps(prof_kind, stream);
+    CUDA_TRY(launch(gemv_w3a16_kernel<NT, NMAT>, dim3(sms), dim3(32 * CF::kWarps), CF::kBytes,
+                    stream, true, ga));
+  }
+  ProfScope ps(kProfOther, stream);
+  CUDA_TRY(launch(gemv_epilogue_kernel<NT, NMAT>,
+                  dim3((unsigned)((slabs_max + kEpiWarps - 1) / kEpiWarps)), dim3(32 * kEpiWarps),
+                  0, stream, true, ga));
   return MILO_OK;
 }
 
@@ -616,9 +623,9 @@ extern "C" milo_status milo_gemm_w3a16(const milo_weight* w, const milo_comp* co
     float* full = reinterpret_cast<float*>(base + o_full);
     float* part = reinterpret_cast<float*>(base + o_part);
     int32_t* tc = lp.t_counters;
-    st = nt == 1 ? run_grouped<1, 1>(lp.problems, lp.n_problems, blocks, k, rank, ws, full,
+    st = nt == 1 ? run_grouped<1, 1>(lp.problems, lp.n_problems, blocks, slabs, k, rank, ws, full,
                                      lp.counters, part, tc, stream, props.sms, kProfGemv1)
-                 : run_grouped<2, 1>(lp.problems, lp.n_problems, blocks, k, rank, ws, full,
+                 : run_grouped<2, 1>(lp.problems, lp.n_problems, blocks, slabs, k, rank, ws, full,
                                      lp.counters, part, tc, stream, props.sms, kProfGemv1);
     cudaFreeAsync(mem, stream);
     if (st != MILO_OK) return st;
@@ -764,9 +771,9 @@ extern "C" milo_status milo_router_topk(const float* logits, int64_t m, int32_t 
 namespace {
 
 template <int NT>
-milo_status moe_run(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype, const int32_t* ids,
-                    const float* wts, void* out, int32_t out_dtype, cudaStream_t stream,
-                    int sms) {
+milo_status moe_run(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype,
+                    const float* logits, int32_t* ids, float* wts, void* out, int32_t out_dtype,
+                    cudaStream_t stream, int sms) {
   constexpr int m_pad = 8 * NT;
   const int K = moe->K, E = moe->E, S = moe->n_shared;
   const int64_t d = moe->d, f_max = moe->f_max;
@@ -834,8 +841,13 @@ milo_status moe_run(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype, co
   ra.Y = reinterpret_cast<float*>(base + o_Y);
   ra.zero_ptr = zero;
   ra.zero_count = n_zero;
+  ra.logits = logits;
+  ra.ids_out = ids;
+  ra.wts_out = wts;
+  ra.score_mode = moe->score_mode;
   milo_status st = MILO_OK;
-  cudaError_t e = launch(moe_route_kernel, dim3(1), dim3(kRouteThreads), 0, stream, true, ra);
+  const int route_threads = (int)std::min<int64_t>(kRouteThreads, std::max<int64_t>(128, (m + 31) / 32 * 32));
+  cudaError_t e = launch(moe_route_kernel, dim3(1), dim3(route_threads), 0, stream, true, ra);
   if (e == cudaSuccess)
     e = launch(moe_gather_kernel, dim3((unsigned)blocks_max, m_pad), dim3(128), 0, stream, true, x,
                x_dtype, d, K, m, (const int32_t*)ra.elist, (const int32_t*)ra.block_start,
@@ -844,11 +856,11 @@ milo_status moe_run(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype, co
   if (e != cudaSuccess) st = fail(MILO_ERR_CUDA, "launch failed: %s", cudaGetErrorString(e));
   float* ws = reinterpret_cast<float*>(base + o_ws);
   if (st == MILO_OK)
-    st = run_grouped<NT, 2>(ra.p1, ra.n_p1, blocks_max, d, r1, ws,
+    st = run_grouped<NT, 2>(ra.p1, ra.n_p1, blocks_max, slabs1, d, r1, ws,
                             reinterpret_cast<float*>(base + o_full1), sc1,
                             reinterpret_cast<float*>(base + o_pa1), tc1, stream, sms, kProfGemv1);
   if (st == MILO_OK)
-    st = run_grouped<NT, 1>(ra.p2, ra.n_p2, blocks_max, f_max, r2, ws,
+    st = run_grouped<NT, 1>(ra.p2, ra.n_p2, blocks_max, slabs2, f_max, r2, ws,
                             reinterpret_cast<float*>(base + o_full2), sc2,
                             reinterpret_cast<float*>(base + o_pa2), tc2, stream, sms, kProfGemv2);
   if (st == MILO_OK) {
@@ -864,10 +876,13 @@ milo_status moe_run(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype, co
 
 }  // namespace
 
-extern "C" milo_status milo_moe_forward_routed(milo_moe* moe, const void* x, int64_t m,
-                                               int32_t x_dtype, const int32_t* ids,
-                                               const float* wts, void* out, int32_t out_dtype,
-                                               void* stream_) {
+namespace {
+
+// logits != nullptr: the route kernel computes the top-k into ids / wts
+// (outputs); otherwise ids / wts are the given routing (inputs).
+milo_status moe_forward_impl(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype,
+                             const float* logits, int32_t* ids, float* wts, void* out,
+                             int32_t out_dtype, void* stream_) {
   if (!moe) return fail(MILO_ERR_ARGUMENT, "null moe");
   if (m < 0) return fail(MILO_ERR_SHAPE, "negative token count");
   if (m == 0) return MILO_OK;
@@ -888,13 +903,25 @@ extern "C" milo_status milo_moe_forward_routed(milo_moe* moe, const void* x, int
     const size_t xs = x_dtype == 0 ? 4 : 2, os = out_dtype == 0 ? 4 : 2;
     const void* xc = static_cast<const uint8_t*>(x) + t0 * moe->d * xs;
     void* oc = static_cast<uint8_t*>(out) + t0 * moe->d * os;
-    const int32_t* ic = ids ? ids + t0 * moe->K : nullptr;
-    const float* wc = wts ? wts + t0 * moe->K : nullptr;
-    milo_status st = nt == 1 ? moe_run<1>(moe, xc, mm, x_dtype, ic, wc, oc, out_dtype, stream, props.sms)
-                             : moe_run<2>(moe, xc, mm, x_dtype, ic, wc, oc, out_dtype, stream, props.sms);
+    int32_t* ic = ids ? ids + t0 * moe->K : nullptr;
+    float* wc = wts ? wts + t0 * moe->K : nullptr;
+    const float* lc = logits ? logits + t0 * moe->E : nullptr;
+    milo_status st =
+        nt == 1 ? moe_run<1>(moe, xc, mm, x_dtype, lc, ic, wc, oc, out_dtype, stream, props.sms)
+                : moe_run<2>(moe, xc, mm, x_dtype, lc, ic, wc, oc, out_dtype, stream, props.sms);
     if (st != MILO_OK) return st;
   }
   return MILO_OK;
+}
+
+}  // namespace
+
+extern "C" milo_status milo_moe_forward_routed(milo_moe* moe, const void* x, int64_t m,
+                                               int32_t x_dtype, const int32_t* ids,
+                                               const float* wts, void* out, int32_t out_dtype,
+                                               void* stream) {
+  return moe_forward_impl(moe, x, m, x_dtype, nullptr, const_cast<int32_t*>(ids),
+                          const_cast<float*>(wts), out, out_dtype, stream);
 }
 
 extern "C" milo_status milo_moe_forward(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype,
@@ -902,6 +929,7 @@ extern "C" milo_status milo_moe_forward(milo_moe* moe, const void* x, int64_t m,
                                         int32_t* topk_ids, float* topk_w, void* stream_) {
   if (!moe) return fail(MILO_ERR_ARGUMENT, "null moe");
   if (m <= 0) return m == 0 ? MILO_OK : fail(MILO_ERR_SHAPE, "negative token count");
+  if (moe->K > 0 && !logits) return fail(MILO_ERR_ARGUMENT, "null router logits");
   cudaStream_t stream = (cudaStream_t)stream_;
   int32_t* ids = topk_ids;
   float* w = topk_w;
@@ -911,9 +939,8 @@ extern "C" milo_status milo_moe_forward(milo_moe* moe, const void* x, int64_t m,
     ids = static_cast<int32_t*>(mem);
     w = reinterpret_cast<float*>(ids + m * moe->K);
   }
-  milo_status st = MILO_OK;
-  if (moe->K > 0) st = milo_router_topk(logits, m, moe->E, moe->K, moe->score_mode, ids, w, stream);
-  if (st == MILO_OK) st = milo_moe_forward_routed(moe, x, m, x_dtype, ids, w, out, out_dtype, stream);
+  milo_status st = moe_forward_impl(moe, x, m, x_dtype, moe->K > 0 ? logits : nullptr, ids, w,
+                                    out, out_dtype, stream);
   if (mem) cudaFreeAsync(mem, stream);
   return st;
 }

@@ -25,14 +25,11 @@ namespace milo_dev {
 // ---------------------------------------------------------------------------
 // router
 // ---------------------------------------------------------------------------
-__global__ void router_topk_kernel(const float* __restrict__ logits, int64_t m, int E, int K,
-                                   int score_mode, int32_t* __restrict__ ids,
-                                   float* __restrict__ wts) {
-  const int warps = blockDim.x >> 5;
-  const int64_t t = (int64_t)blockIdx.x * warps + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (t >= m) return;
-  const float* l = logits + t * E;
+// One warp: top-K of one token's logits (descending, ties -> lower id) and
+// its routing weights; lane 0 writes ids/wts[t*K ...].
+__device__ __forceinline__ void topk_warp(const float* __restrict__ l, int64_t t, int E, int K,
+                                          int score_mode, int32_t* __restrict__ ids,
+                                          float* __restrict__ wts, int lane) {
   int sel[16];
   for (int k = 0; k < K; ++k) {
     float best = -INFINITY;
@@ -81,6 +78,15 @@ __global__ void router_topk_kernel(const float* __restrict__ logits, int64_t m, 
   }
 }
 
+__global__ void router_topk_kernel(const float* __restrict__ logits, int64_t m, int E, int K,
+                                   int score_mode, int32_t* __restrict__ ids,
+                                   float* __restrict__ wts) {
+  const int warps = blockDim.x >> 5;
+  const int64_t t = (int64_t)blockIdx.x * warps + (threadIdx.x >> 5);
+  if (t >= m) return;
+  topk_warp(logits + t * E, t, E, K, score_mode, ids, wts, threadIdx.x & 31);
+}
+
 // ---------------------------------------------------------------------------
 // routing -> problem tables
 // ---------------------------------------------------------------------------
@@ -124,6 +130,11 @@ struct MoeRouteArgs {
   int32_t* zero_ptr;         // counters to clear
   int64_t zero_count;
   int32_t* n_blocks_out;
+  // fused router (optional): logits m x E -> ids / wts (then a.ids == ids_out)
+  const float* logits;
+  int32_t* ids_out;
+  float* wts_out;
+  int32_t score_mode;
 };
 
 constexpr int kRouteThreads = 1024;
@@ -139,6 +150,11 @@ __global__ void __launch_bounds__(kRouteThreads) moe_route_kernel(MoeRouteArgs a
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int E = a.E, K = a.K;
   const int ET = E + a.n_shared;
+  if (a.logits != nullptr) {  // router: one warp per token
+    for (int64_t t = warp; t < a.m; t += blockDim.x >> 5)
+      topk_warp(a.logits + t * E, t, E, K, a.score_mode, a.ids_out, a.wts_out, lane);
+    __syncthreads();  // ids_out is read back below (block-visible after the barrier)
+  }
   for (int64_t i = tid; i < a.zero_count; i += blockDim.x) a.zero_ptr[i] = 0;
   for (int e = tid; e < ET; e += blockDim.x) {
     cnt[e] = e < E ? 0 : (int32_t)a.m;
@@ -163,7 +179,7 @@ __global__ void __launch_bounds__(kRouteThreads) moe_route_kernel(MoeRouteArgs a
       }
       __syncthreads();
     }
-    for (int64_t r0 = 0; r0 < a.m; r0 += kRouteThreads) {
+    for (int64_t r0 = 0; r0 < a.m; r0 += blockDim.x) {
       const int64_t t = r0 + tid;
       int32_t my[16];
       for (int k = 0; k < K; ++k) my[k] = (t < a.m) ? a.ids[t * K + k] : -1;
@@ -179,7 +195,7 @@ __global__ void __launch_bounds__(kRouteThreads) moe_route_kernel(MoeRouteArgs a
       if (pass == 0) {
         for (int e = tid; e < E; e += blockDim.x) {
           int32_t s = 0;
-          for (int w = 0; w < 32; ++w) s += wtot[w][e];
+          for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += wtot[w][e];
           cnt[e] += s;
         }
       } else {
@@ -196,7 +212,7 @@ __global__ void __launch_bounds__(kRouteThreads) moe_route_kernel(MoeRouteArgs a
         __syncthreads();
         for (int e = tid; e < E; e += blockDim.x) {
           int32_t s = 0;
-          for (int w = 0; w < 32; ++w) s += wtot[w][e];
+          for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += wtot[w][e];
           base[e] += s;
         }
       }

@@ -35,7 +35,7 @@ evs.sort(key=lambda e: e.time_range.start)
 # last iteration
 groups, cur = [], []
 for e in evs:
-    if "router_topk" in e.name and cur:
+    if "moe_route" in e.name and cur:
         groups.append(cur); cur = []
     cur.append(e)
 groups.append(cur)
