@@ -1,0 +1,1199 @@
+// K2': the decode-regime MoE layer (and single linear) in ONE persistent launch.
+//
+// Reference semantics, per matrix: milo::gemm_w3a16 (proj/src/gemm.cpp:117-199)
+//   C = half(A) * dequant(W) + (half(A) U) V, fp32 accumulation,
+// composed into the top-k routed expert layer defined in SURVEY.md section 8b
+// (the reference has no MoE layer):
+//   h_e = half(silu(x W1_e + t1 V1_e) * (x W3_e + t3 V3_e)),  y_e = h_e W2_e + t2 V2_e,
+//   out[t] = sum_k w[t,k] y_{e(t,k)}[t] + sum_shared y_s[t].
+//
+// Grid = one CTA per SM (cooperative launch: all CTAs co-resident).  A CTA has
+// C consumer warps and one producer warp whose lane c feeds consumer c's ring
+// of cp.async.bulk slots (full / empty mbarriers per slot).  A call:
+//
+//  stage 0  every CTA, redundantly: router top-k (or the given routing), the
+//           block table (one block per touched expert, tokens ascending;
+//           shared experts: all tokens) and the per-phase problem tables.
+//  phase 1  warp-level stream-K over the units of
+//             [LoRC pseudo-slabs: t = x U, 16 rank columns x 32 k per unit]
+//             [w1|w3 slabs: 64 n x 32 k per unit, both matrices per unit]
+//           Activations are copied per token row straight from x (binary16).
+//           A slab's last-arriving contributor (atomic counter) sums the
+//           contributors' partials in warp order (deterministic) and
+//           finishes it: pseudo -> t (t-ready flag when all its chunks are
+//           in); real -> + t V (tensor cores, fp32-exact split), SwiGLU -> the
+//           block's h tiles (block-ready flag when all its slabs are in).
+//  phase 2  the same over [t2 = h U2 pseudo-slabs][w2 slabs] -> y rows; the
+//           last block finishing a d-slab runs the weighted combine -> out.
+// The units of a phase are split evenly over all consumer warps of the grid
+// whatever the mix of experts / ranks.  The producer never blocks: it issues
+// phase-2 weight copies while phase 1 drains and adds each unit's activation
+// copy once that block's h is published.
+//
+// Waits never form a cycle: consumers finish all pseudo units (which wait for
+// nothing) before any real unit, and all of phase 1 (finisher duty included)
+// before any phase-2 unit; the producer only polls.  Spin waits are bounded
+// and trap instead of hanging.
+//
+// LoRC on the tensor cores without losing fp32 accuracy: U / V codes are
+// exact binary16 integers c - 4; the fp32 side (x * step for t = x U, and t for
+// t V) is split into hi + lo binary16 halves, two MMAs, fp32 accumulation.
+// Real-storage factors are split hi + lo instead.
+#pragma once
+#include <cstdint>
+#include <cuda_fp16.h>
+
+#include "gemv.cuh"
+#include "layout.cuh"
+#include "ptx.cuh"
+
+namespace milo_dev {
+
+constexpr int kDecMaxBlocks = 64;
+constexpr int kDecMaxTok = 16;                    // MoE decode path: m <= 16
+constexpr int kDecMaxProbs = 3 * kDecMaxBlocks;   // per phase
+constexpr int kDecKC = 4;                         // k-tiles (32 k each) per unit
+constexpr int kDecSlotW = 8192;                   // weight / pseudo-tile bytes per slot
+constexpr int kPseudoInt3Bytes = 640;             // 512 B codes + 32 f32 steps
+constexpr int kPseudoRealBytes = 2048;            // hi / lo binary16 fragments
+constexpr int kVftInt3Bytes = 1024;               // per (slab, 16-rank step)
+constexpr int kVftRealBytes = 4096;
+
+// One quantized matrix + compensator in device layout (built at create time).
+//   upt  : U pseudo tiles [r16/16][k/32], fragment-native A operand (rows =
+//          16 rank columns, cols = 32 k): int3 -> per lane 16 code bytes
+//          [ks][reg][2] then 32 f32 steps (s * 2/7 of the 64-group); real ->
+//          per lane [ks][hi 4 regs][lo 4 regs].
+//   vft  : V^T fragment tiles [n/64][r16/16]: per lane [i 0..3][8 code bytes]
+//          (int3) or [i][hi 4][lo 4] (real); rows = n, cols = rank.
+//   vstep: [n][gpr] f32 steps of V (int3 only).
+struct DecMat {
+  const uint8_t* w;
+  const uint8_t* upt;
+  const uint8_t* vft;
+  const float* vstep;
+  int32_t k, n, rank, r16, gpr, real, mode, pad;
+};
+
+struct DecExpert {
+  DecMat m[3];  // w1, w3, w2 (single linear: m[0])
+};
+
+struct DecWs {
+  float* part;          // [2 phases][G warps][2 segments][part_stride]
+  float* t;             // [blocks][3][m_pad][r16_max]
+  __half* h;            // [blocks][m_pad][f_max] row-major (phase-2 activations)
+  float* Y;             // [m*K + S*m][d]
+  __half* xrep;         // [grid][m][d] CTA-private binary16 copies of x (null: read x directly)
+  int32_t* cnt1;        // phase-1 slab counters
+  int32_t* cnt2;        // phase-2 slab counters
+  int32_t* tcnt;        // [blocks][3]
+  int32_t* bcnt;        // [blocks]
+  int32_t* ccnt;        // [d/64]
+  int32_t* tflag;       // [blocks][3]   (epoch-valued)
+  int32_t* bflag;       // [blocks]
+  int64_t part_stride;  // floats per (phase, warp, segment)
+  int32_t r16_max;
+  int32_t f_max;
+};
+
+struct DecArgs {
+  int32_t moe;                 // 1: MoE layer, 0: single linear
+  int32_t m;                   // token rows of this call
+  int32_t epoch;
+  int32_t gw;                  // consumer warps of the grid
+  // MoE
+  const float* logits;         // m x E (router) or null (routing given)
+  const int32_t* ids_in;       // m x K given routing (-1 = unused slot)
+  const float* wts_in;
+  int32_t* ids_out;            // optional routing outputs
+  float* wts_out;
+  int32_t E, K, S, score_mode;
+  const DecExpert* experts;    // E routed then S shared (device); linear: null, uses lin
+  DecExpert lin;               // the single linear's matrix (m[0])
+  // activations / output
+  const void* x;               // rows of x (x_dtype) -- binary16 when xrep is null
+  int32_t x_dtype;             // 0 f32, 1 f16
+  int32_t d;                   // MoE hidden size (linear: k)
+  int64_t ldx;
+  void* out;
+  int32_t out_dtype;
+  int64_t ldo;
+  DecWs ws;
+  long long* dbg;              // optional per-warp timeline (globaltimer ns), [warp][16]
+  int32_t dbg_flags;           // bit 0: skip unit compute (memory-pipeline measurement)
+};
+
+struct DProb {
+  const uint8_t* src[2];  // pseudo: U tiles; real: weight tiles of matrix 0 / 1
+  int32_t u0, s0;         // exclusive prefix of units / slabs within the phase
+  int32_t n_slabs;        // 0 = empty entry (rank-0 compensator)
+  int16_t kind, mat;      // kind 0 pseudo, 1 real; mat = matrix index 0..2
+  int16_t b, kts;         // block; units per slab (= ceil(ktiles / KC))
+  int16_t ktiles, tb;     // 32-k tiles per slab; bytes per tile (896 real, 640 / 2048 pseudo)
+};
+
+struct DBlock {
+  int32_t e;
+  int32_t rows;
+  int16_t xrow[kDecMaxTok];  // x row of each block row (MoE: token; linear: row)
+  int16_t slot[kDecMaxTok];  // output row (MoE: Y slot; linear: C row)
+};
+
+template <int NT, int NMAT1>
+struct DecCfg {
+  static constexpr int kMPad = 8 * NT;
+  static constexpr int kCons = (NT == 1 && NMAT1 == 1) ? 12 : 8;  // warps (each feeds its own ring)
+  static constexpr int kWarps = kCons;
+  static constexpr int kSlotBytes = kDecSlotW;
+  static constexpr int kSlots = kCons == 12 ? 2 : 3;
+  static constexpr int kRing = kCons * kSlots * kSlotBytes;
+  static constexpr int kPartMax = 2 * 64 * kMPad;  // floats of the largest partial
+  // smem carve-up
+  static constexpr int kOffBars = kRing;  // full [kCons][kSlots]
+  static constexpr int kOffProbs = kOffBars + kCons * kSlots * 8;
+  static constexpr int kOffBlocks = kOffProbs + 2 * kDecMaxProbs * (int)sizeof(DProb);
+  static constexpr int kOffRoute = kOffBlocks + kDecMaxBlocks * (int)sizeof(DBlock);
+  static constexpr int kRouteBytes = kDecMaxTok * 16 * 4 * 2 + 256 * 4 + 64;
+  static constexpr int kBytes = kOffRoute + kRouteBytes;
+};
+
+// ---------------------------------------------------------------- helpers
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+  return d;
+}
+// two u8 codes (bytes 0,1 or 2,3 of w) -> half2 (c0 - 4, c1 - 4), exact.
+__device__ __forceinline__ uint32_t codes_h2(uint32_t w, bool upper) {
+  const uint32_t v = prmt(w, 0x64646464u, upper ? 0x4342u : 0x4140u);  // 1024 + c
+  return h2_as_u32(__hadd2(u32_as_h2(v), __float2half2_rn(-1028.0f)));
+}
+// fp32 pair -> binary16 hi + lo with hi + lo == (a, b) to ~2^-22.
+__device__ __forceinline__ void split_h2(float a, float b, uint32_t& hi, uint32_t& lo) {
+  const __half2 h = __floats2half2_rn(a, b);
+  const float2 f = __half22float2(h);
+  hi = h2_as_u32(h);
+  lo = h2_as_u32(__floats2half2_rn(a - f.x, b - f.y));
+}
+
+#ifndef DEC_TIMERS
+#define DEC_TIMERS 0  // per-warp cycle counters in the debug timeline (tools/dbg_timeline.py)
+#endif
+
+__device__ __forceinline__ long long globaltimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define DEC_DBG(i)                                                                     \
+  do {                                                                                 \
+    if (a.dbg != nullptr && (threadIdx.x & 31) == 0)                                   \
+      a.dbg[((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 16 + (i)] = \
+          globaltimer();                                                               \
+  } while (0)
+
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int atom_add_acqrel_gpu(int* p, int v) {
+  int old;
+  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ int ld_relaxed_gpu(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+// Bounded spin until *p == v (relaxed polls, one acquiring load at the end).
+// Traps after ~2 s instead of hanging.
+__device__ __forceinline__ void spin_until(const int* p, int v) {
+  if (ld_relaxed_gpu(p) != v) {
+    const long long t0 = clock64();
+    while (ld_relaxed_gpu(p) != v) {
+      __nanosleep(32);
+      if (clock64() - t0 > 4000000000LL) __trap();
+    }
+  }
+  (void)ld_acquire_gpu(p);
+}
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+// B fragments of one 32-k tile, loaded straight from the activation rows
+// (binary16, row-major, L1/L2 resident): v[j][nt] = {x[row][k + 16 j + 2q .. +1],
+// x[row][k + 16 j + 2q + 8 .. +9]}, row = 8 nt + g.  rowp[nt] == nullptr -> padding
+// row (zeros).
+template <int NT>
+struct BTile {
+  uint32_t v[2][NT][2];
+};
+template <int NT>
+__device__ __forceinline__ void load_btile(BTile<NT>& b, const __half* const (&rowp)[NT], int k, bool on, int q) {
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      uint32_t b0 = 0u, b1 = 0u;
+      if (on && rowp[nt] != nullptr) {
+        const __half* p = rowp[nt] + k + 16 * j + 2 * q;
+        b0 = *reinterpret_cast<const uint32_t*>(p);
+        b1 = *reinterpret_cast<const uint32_t*>(p + 8);
+      }
+      b.v[j][nt][0] = b0;
+      b.v[j][nt][1] = b1;
+    }
+}
+
+// One k-tile of a real unit: NMAT macro tiles (matrix mat's tile at tile + mat * mstride).
+template <int NT, int NMAT, int NA>
+__device__ __forceinline__ void tile_real(const uint8_t* tile0, int mstride, const BTile<NT>& b,
+                                          float (&acc)[NA][4][NT][4], const DqConsts& dq, int lane) {
+  const int q = lane & 3;
+#pragma unroll
+  for (int mat = 0; mat < NMAT; ++mat) {
+    const uint8_t* tile = tile0 + mat * mstride;
+    const uint4 pa = *reinterpret_cast<const uint4*>(tile + kPlaneAOff + lane * 16);
+    const uint2 pb = *reinterpret_cast<const uint2*>(tile + kPlaneBOff + lane * 8);
+    const uint4 m0 = *reinterpret_cast<const uint4*>(tile + kMetaOff + q * 32);
+    const uint4 m1 = *reinterpret_cast<const uint4*>(tile + kMetaOff + q * 32 + 16);
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const uint4 mm = j == 0 ? m0 : m1;
+      const uint32_t S[2] = {mm.x, mm.z}, O[2] = {mm.y, mm.w};
+      uint32_t wv[16];
+      unit_dequant(j == 0 ? pa.x : pa.z, j == 0 ? pa.y : pa.w, j == 0 ? pb.x : pb.y, S, O, dq, wv);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) mma_16816(acc[mat][i][nt], &wv[4 * i], b.v[j][nt][0], b.v[j][nt][1]);
+    }
+  }
+}
+
+// One k-tile of a pseudo unit: t chunk (16 rank cols x tokens) += U^T chunk (16 x 32 k) * x.
+template <int NT, int NA>
+__device__ __forceinline__ void tile_pseudo(const uint8_t* st, bool real, const BTile<NT>& b,
+                                            float (&acc)[NA][4][NT][4], int lane) {
+  const int q = lane & 3;
+  if (!real) {
+    const uint4 cw = *reinterpret_cast<const uint4*>(st + lane * 16);
+    const float* steps = reinterpret_cast<const float*>(st + 512);
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const uint32_t w0 = j == 0 ? cw.x : cw.z, w1 = j == 0 ? cw.y : cw.w;
+      const uint32_t A[4] = {codes_h2(w0, false), codes_h2(w0, true), codes_h2(w1, false), codes_h2(w1, true)};
+      const float2 s0 = *reinterpret_cast<const float2*>(steps + 16 * j + 2 * q);
+      const float2 s1 = *reinterpret_cast<const float2*>(steps + 16 * j + 2 * q + 8);
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const float2 x0 = __half22float2(u32_as_h2(b.v[j][nt][0]));
+        const float2 x1 = __half22float2(u32_as_h2(b.v[j][nt][1]));
+        uint32_t h0, l0, h1, l1;
+        split_h2(x0.x * s0.x, x0.y * s0.y, h0, l0);
+        split_h2(x1.x * s1.x, x1.y * s1.y, h1, l1);
+        mma_16816(acc[0][0][nt], A, h0, h1);
+        mma_16816(acc[0][0][nt], A, l0, l1);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const uint4 hi = *reinterpret_cast<const uint4*>(st + lane * 64 + j * 32);
+      const uint4 lo = *reinterpret_cast<const uint4*>(st + lane * 64 + j * 32 + 16);
+      const uint32_t AH[4] = {hi.x, hi.y, hi.z, hi.w}, AL[4] = {lo.x, lo.y, lo.z, lo.w};
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        mma_16816(acc[0][0][nt], AH, b.v[j][nt][0], b.v[j][nt][1]);
+        mma_16816(acc[0][0][nt], AL, b.v[j][nt][0], b.v[j][nt][1]);
+      }
+    }
+  }
+}
+
+// acc[i][nt][e] += (t V)^T of the slab's 64 columns:  t = [m_pad][r16max] fp32
+// (global), V fragment tiles of the slab.  int3: per 64-rank group g_r,
+// D = c'(V) * split(t) on the tensor cores, then acc += step[n][g_r] * D.
+// All loads of a group are issued before its MMAs (one round trip per group).
+template <int NT>
+__device__ __forceinline__ void add_tv(float (&acc)[4][NT][4], const DecMat& M, const float* t,
+                                       int r16max, int slab, int lane) {
+  const int g = lane >> 2, q = lane & 3;
+  const int nks = M.r16 >> 4;
+  const int n0 = slab * 64;
+  const uint8_t* vb = M.vft + (int64_t)slab * nks * (M.real ? kVftRealBytes : kVftInt3Bytes);
+  constexpr int kB = 4 / NT;  // rank steps whose loads are in flight together
+  for (int kb = 0; kb * kB < nks; ++kb) {
+    const int gr = (kb * kB) >> 2;  // 64-rank group of this batch
+    const int nk = min(kB, nks - kb * kB);
+    float D[4][NT][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) D[i][nt][e] = 0.0f;
+    float sv[8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        sv[2 * i + h] = M.real ? 1.0f : __ldg(M.vstep + (int64_t)(n0 + 16 * i + g + 8 * h) * M.gpr + gr);
+    if (!M.real) {
+      float2 tv[kB][NT][2];
+      uint4 cv[kB][2];
+#pragma unroll
+      for (int kk = 0; kk < kB; ++kk) {
+        if (kk >= nk) continue;
+        const int ks = kb * kB + kk;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const float* tr = t + (8 * nt + g) * r16max + 16 * ks + 2 * q;
+          tv[kk][nt][0] = __ldcg(reinterpret_cast<const float2*>(tr));
+          tv[kk][nt][1] = __ldcg(reinterpret_cast<const float2*>(tr + 8));
+        }
+        const uint4* src = reinterpret_cast<const uint4*>(vb + (int64_t)ks * kVftInt3Bytes + lane * 32);
+        cv[kk][0] = __ldg(src);
+        cv[kk][1] = __ldg(src + 1);
+      }
+#pragma unroll
+      for (int kk = 0; kk < kB; ++kk) {
+        if (kk >= nk) continue;
+        uint32_t bh[NT][2], bl[NT][2];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          split_h2(tv[kk][nt][0].x, tv[kk][nt][0].y, bh[nt][0], bl[nt][0]);
+          split_h2(tv[kk][nt][1].x, tv[kk][nt][1].y, bh[nt][1], bl[nt][1]);
+        }
+        const uint32_t cw[8] = {cv[kk][0].x, cv[kk][0].y, cv[kk][0].z, cv[kk][0].w,
+                                cv[kk][1].x, cv[kk][1].y, cv[kk][1].z, cv[kk][1].w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint32_t A[4] = {codes_h2(cw[2 * i], false), codes_h2(cw[2 * i], true),
+                                 codes_h2(cw[2 * i + 1], false), codes_h2(cw[2 * i + 1], true)};
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            mma_16816(D[i][nt], A, bh[nt][0], bh[nt][1]);
+            mma_16816(D[i][nt], A, bl[nt][0], bl[nt][1]);
+          }
+        }
+      }
+    } else {
+      for (int kk = 0; kk < nk; ++kk) {
+        const int ks = kb * kB + kk;
+        uint32_t bh[NT][2], bl[NT][2];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const float* tr = t + (8 * nt + g) * r16max + 16 * ks + 2 * q;
+          const float2 v0 = __ldcg(reinterpret_cast<const float2*>(tr));
+          const float2 v1 = __ldcg(reinterpret_cast<const float2*>(tr + 8));
+          split_h2(v0.x, v0.y, bh[nt][0], bl[nt][0]);
+          split_h2(v1.x, v1.y, bh[nt][1], bl[nt][1]);
+        }
+        const uint4* src = reinterpret_cast<const uint4*>(vb + (int64_t)ks * kVftRealBytes + lane * 128);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint4 hi = __ldg(src + 2 * i), lo = __ldg(src + 2 * i + 1);
+          const uint32_t AH[4] = {hi.x, hi.y, hi.z, hi.w}, AL[4] = {lo.x, lo.y, lo.z, lo.w};
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            mma_16816(D[i][nt], AH, bh[nt][0], bh[nt][1]);
+            mma_16816(D[i][nt], AH, bl[nt][0], bl[nt][1]);
+            mma_16816(D[i][nt], AL, bh[nt][0], bh[nt][1]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          acc[i][nt][2 * h] += sv[2 * i + h] * D[i][nt][2 * h];
+          acc[i][nt][2 * h + 1] += sv[2 * i + h] * D[i][nt][2 * h + 1];
+        }
+  }
+}
+
+// Top-k of one token's logits by one warp (descending, ties -> lower id) and
+// its routing weights (score_mode 0: softmax over the top-k, Mixtral; 1:
+// softmax over all experts, DeepSeek).  E <= 256: 8 logits per lane.
+__device__ __forceinline__ void topk_regs(const float* __restrict__ l, int E, int K, int score_mode,
+                                          int32_t* ids, float* wts, int lane) {
+  float v[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int e = lane + 32 * i;
+    v[i] = e < E ? __ldg(l + e) : -INFINITY;
+  }
+  float mx_all = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) mx_all = fmaxf(mx_all, v[i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx_all = fmaxf(mx_all, __shfl_xor_sync(0xffffffffu, mx_all, o));
+  uint32_t used = 0u;  // bit i: v[i] of this lane taken
+  // the selected (value, id) of step k stay on lane k (K <= 16 < 32): no local arrays
+  float my_v = -INFINITY;
+  int my_e = -1;
+  for (int k = 0; k < K; ++k) {
+    float best = -INFINITY;
+    int bid = 0x7fffffff;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int e = lane + 32 * i;
+      if (e < E && !(used >> i & 1u) && (bid == 0x7fffffff || v[i] > best)) {
+        best = v[i];
+        bid = e;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oid = __shfl_xor_sync(0xffffffffu, bid, o);
+      if (oid != 0x7fffffff && (bid == 0x7fffffff || ov > best || (ov == best && oid < bid))) {
+        best = ov;
+        bid = oid;
+      }
+    }
+    if ((bid & 31) == lane) used |= 1u << (bid >> 5);
+    if (lane == k) {
+      my_v = best;
+      my_e = bid;
+    }
+  }
+  // weights: lane k < K owns selection k (Mixtral: softmax over the top-k;
+  // DeepSeek: softmax over all experts)
+  const float top0 = __shfl_sync(0xffffffffu, my_v, 0);
+  float num, denom;
+  if (score_mode == 0) {
+    num = lane < K ? expf(my_v - top0) : 0.0f;
+    denom = num;
+  } else {
+    num = lane < K ? expf(my_v - mx_all) : 0.0f;
+    denom = 0.0f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (lane + 32 * i < E) denom += expf(v[i] - mx_all);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) denom += __shfl_xor_sync(0xffffffffu, denom, o);
+  if (lane < K) {
+    ids[lane] = my_e;
+    wts[lane] = num / denom;
+  }
+}
+
+// ---------------------------------------------------------------- stage 0
+// Every CTA, redundantly: routing (or the given routing), the block table and
+// the per-phase problem tables in shared memory.  Ends with __syncthreads().
+template <int NT, int NMAT1, bool MOE>
+__device__ __noinline__ void dec_stage0(const DecArgs& a) {
+  using CF = DecCfg<NT, NMAT1>;
+  constexpr int kMPad = CF::kMPad;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  DProb* probs = reinterpret_cast<DProb*>(smem + CF::kOffProbs);
+  DBlock* blocks = reinterpret_cast<DBlock*>(smem + CF::kOffBlocks);
+  int32_t* r_ids = reinterpret_cast<int32_t*>(smem + CF::kOffRoute);
+  float* r_wts = reinterpret_cast<float*>(r_ids + kDecMaxTok * 16);
+  uint32_t* emask = reinterpret_cast<uint32_t*>(r_wts + kDecMaxTok * 16);
+  int32_t* sc = reinterpret_cast<int32_t*>(emask + 256);
+  const DecExpert* experts = MOE ? a.experts : &a.lin;
+  const int m = a.m;
+  if (MOE) {
+    const int K = a.K, E = a.E;
+    for (int e = tid; e < 256; e += blockDim.x) emask[e] = 0u;
+    DEC_DBG(9);
+    if (a.logits != nullptr) {
+      for (int t = warp; t < m; t += blockDim.x >> 5)
+        topk_regs(a.logits + (int64_t)t * E, E, K, a.score_mode, r_ids + t * K, r_wts + t * K, lane);
+      DEC_DBG(10);
+    } else {
+      for (int i = tid; i < m * K; i += blockDim.x) {
+        r_ids[i] = a.ids_in[i];
+        r_wts[i] = a.wts_in[i];
+      }
+    }
+    __syncthreads();
+    DEC_DBG(8);
+    if (blockIdx.x == 0 && a.logits != nullptr && a.ids_out != nullptr)
+      for (int i = tid; i < m * K; i += blockDim.x) {
+        a.ids_out[i] = r_ids[i];
+        a.wts_out[i] = r_wts[i];
+      }
+    for (int i = tid; i < m * K; i += blockDim.x) {
+      const int e = r_ids[i];
+      if (e >= 0 && e < E) atomicOr(&emask[e], 1u << (i / K));
+    }
+    __syncthreads();
+    if (warp == 0) {  // touched experts ascending, then shared experts
+      int nb = 0;
+      for (int e0 = 0; e0 < E; e0 += 32) {
+        const int e = e0 + lane;
+        const bool on = e < E && emask[e] != 0u;
+        const uint32_t bal = __ballot_sync(0xffffffffu, on);
+        if (on) blocks[nb + __popc(bal & ((1u << lane) - 1u))].e = e;
+        nb += __popc(bal);
+      }
+      for (int s = lane; s < a.S; s += 32) blocks[nb + s].e = E + s;
+      if (lane == 0) sc[0] = nb + a.S;
+    }
+    __syncthreads();
+    const int nb = sc[0];
+    for (int b = tid; b < nb; b += blockDim.x) {
+      DBlock& B = blocks[b];
+      const int e = B.e;
+      const uint32_t mask = e < E ? emask[e] : ((1u << m) - 1u);
+      int r = 0;
+      for (int t = 0; t < m; ++t) {
+        if (!(mask >> t & 1u)) continue;
+        int slot;
+        if (e < E) {
+          int kk = 0;
+          for (int k = 0; k < K; ++k)
+            if (r_ids[t * K + k] == e) kk = k;
+          slot = t * K + kk;
+        } else {
+          slot = m * K + (e - E) * m + t;
+        }
+        B.xrow[r] = (int16_t)t;
+        B.slot[r] = (int16_t)slot;
+        ++r;
+      }
+      B.rows = r;
+      for (; r < kDecMaxTok; ++r) B.xrow[r] = B.slot[r] = -1;
+    }
+  } else {
+    const int nb = (m + kMPad - 1) / kMPad;
+    if (tid == 0) sc[0] = nb;
+    for (int b = tid; b < nb; b += blockDim.x) {
+      DBlock& B = blocks[b];
+      B.e = 0;
+      B.rows = min(kMPad, m - b * kMPad);
+      for (int r = 0; r < kDecMaxTok; ++r) {
+        const bool on = r < B.rows;
+        B.xrow[r] = on ? (int16_t)(b * kMPad + r) : (int16_t)-1;
+        B.slot[r] = B.xrow[r];
+      }
+    }
+  }
+  __syncthreads();
+  const int nb = sc[0];
+  // problem entries, one thread each: phase 1 [pseudo (b, mat)][real b], phase 2
+  // [pseudo b][real b]; rank-0 pseudo entries stay as empty (n_slabs = 0) entries.
+  // kts = units per slab (KC k-tiles each, the last one possibly shorter).
+  const int nm1 = MOE ? 2 : 1;
+  const int np1 = nb * (nm1 + 1), np2 = MOE ? nb * 2 : 0;
+  for (int i = tid; i < np1 + np2; i += blockDim.x) {
+    const int ph = i < np1 ? 0 : 1;
+    const int j = ph == 0 ? i : i - np1;
+    DProb& P = probs[ph * kDecMaxProbs + j];
+    int b, mat, kind;
+    if (ph == 0) {
+      kind = j < nb * nm1 ? 0 : 1;
+      b = kind == 0 ? j / nm1 : j - nb * nm1;
+      mat = kind == 0 ? j % nm1 : 0;
+    } else {
+      kind = j < nb ? 0 : 1;
+      b = kind == 0 ? j : j - nb;
+      mat = 2;
+    }
+    const DecExpert& X = experts[blocks[b].e];
+    const DecMat& M = X.m[mat];
+    P.kind = (int16_t)kind;
+    P.mat = (int16_t)mat;
+    P.b = (int16_t)b;
+    P.ktiles = (int16_t)(M.k / kTileK);
+    P.kts = (int16_t)((P.ktiles + kDecKC - 1) / kDecKC);
+    if (kind == 0) {
+      P.n_slabs = M.rank > 0 ? M.r16 / 16 : 0;
+      P.src[0] = M.upt;
+      P.src[1] = nullptr;
+      P.tb = (int16_t)(M.real ? kPseudoRealBytes : kPseudoInt3Bytes);
+    } else {
+      P.n_slabs = M.n / kTileN;
+      P.src[0] = M.w;
+      P.src[1] = (MOE && ph == 0) ? X.m[1].w : nullptr;
+      P.tb = (int16_t)kTileBytes;
+    }
+  }
+  __syncthreads();
+  if (warp < 2) {  // exclusive prefix of units / slabs per phase (warp ph)
+    const int ph = warp;
+    const int n = ph == 0 ? np1 : np2;
+    DProb* PP = probs + ph * kDecMaxProbs;
+    int cu = 0, cs = 0;
+    for (int base = 0; base < n; base += 32) {
+      const int i = base + lane;
+      const int s = i < n ? PP[i].n_slabs : 0;
+      const int u = i < n ? s * PP[i].kts : 0;
+      int iu = u, is = s;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int tu = __shfl_up_sync(0xffffffffu, iu, o);
+        const int ts = __shfl_up_sync(0xffffffffu, is, o);
+        if (lane >= o) {
+          iu += tu;
+          is += ts;
+        }
+      }
+      if (i < n) {
+        PP[i].u0 = cu + iu - u;
+        PP[i].s0 = cs + is - s;
+      }
+      cu += __shfl_sync(0xffffffffu, iu, 31);
+      cs += __shfl_sync(0xffffffffu, is, 31);
+    }
+    if (lane == 0) {
+      sc[1 + ph] = n;
+      sc[3 + ph] = cu;
+    }
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------- segment end
+// A warp's segment of slab s of problem p ended with partial accumulators accl
+// ([NMAT1][4][NT][4], local memory).  Publishes the partial (or keeps it when the
+// warp covered the whole slab); the slab's last contributor sums all partials in
+// warp order and finishes the slab.
+template <int NT, int NMAT1, bool MOE, int NM>
+__device__ __noinline__ void dec_finish(const DecArgs& a, float* accs, int ph, int p, int s, int start,
+                                        int end, int Gp, int Tp, int gw, int G) {
+  using CF = DecCfg<NT, NMAT1>;
+  constexpr int kMPad = CF::kMPad;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  // the segment's accumulators, parked in the warp's just-consumed ring slot
+  float acc[NM][4][NT][4];
+#pragma unroll
+  for (int x = 0; x < NM; ++x)
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[x][i][nt][e] = accs[(((x * 4 + i) * NT + nt) * 4 + e) * 32 + lane];
+  const DProb& P = reinterpret_cast<const DProb*>(smem + CF::kOffProbs)[ph * kDecMaxProbs + p];
+  const DBlock* blocks = reinterpret_cast<const DBlock*>(smem + CF::kOffBlocks);
+  const int32_t* r_ids = reinterpret_cast<const int32_t*>(smem + CF::kOffRoute);
+  const float* r_wts = reinterpret_cast<const float*>(r_ids + kDecMaxTok * 16);
+  const int32_t* sc = reinterpret_cast<const int32_t*>(r_wts + kDecMaxTok * 16 + 256);
+  const DecExpert* experts = MOE ? a.experts : &a.lin;
+  const DecWs& W = a.ws;
+  const int epoch = a.epoch;
+  const int d = a.d;
+  const bool pseudo = P.kind == 0;
+  const int nmat = pseudo ? 1 : NM;
+  const int ni = pseudo ? 1 : 4;
+  const int sb = P.u0 + s * P.kts, se = sb + P.kts;
+  float* part_base = W.part + (int64_t)ph * G * 2 * W.part_stride;
+  if (!(start <= sb && end >= se)) {  // not the sole contributor
+    const int w0 = (int)owner_of(sb, Tp, Gp), w1 = (int)owner_of(se - 1, Tp, Gp);
+    float* dst = part_base + ((int64_t)gw * 2 + (start > sb ? 0 : 1)) * W.part_stride;
+#pragma unroll
+    for (int mat = 0; mat < NM; ++mat)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          if (mat >= nmat || i >= ni) continue;
+          float* d0 = dst + (mat * 64 + 16 * i + g) * kMPad + 8 * nt + 2 * q;
+          __stcg(reinterpret_cast<float2*>(d0), make_float2(acc[mat][i][nt][0], acc[mat][i][nt][1]));
+          __stcg(reinterpret_cast<float2*>(d0 + 8 * kMPad), make_float2(acc[mat][i][nt][2], acc[mat][i][nt][3]));
+        }
+    __syncwarp();
+    int last = 0;
+    if (lane == 0) {
+      int* cnt = (ph == 0 ? W.cnt1 : W.cnt2) + P.s0 + s;
+      last = atom_add_acqrel_gpu(cnt, 1) == (w1 - w0);
+      if (last) *cnt = 0;
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (!last) return;
+#pragma unroll
+    for (int mat = 0; mat < NM; ++mat)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc[mat][i][nt][e] = 0.0f;
+    constexpr int kU = NM * NT <= 2 ? 2 : 1;  // contributors whose loads are in flight together
+    for (int w = w0; w <= w1; w += kU) {  // warp order: deterministic
+      float2 v[kU][NM][4][NT][2];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int ww = min(w + u, w1);
+        const int rs = (int)((int64_t)ww * Tp / Gp);
+        const float* src = part_base + ((int64_t)ww * 2 + (rs > sb ? 0 : 1)) * W.part_stride;
+#pragma unroll
+        for (int mat = 0; mat < NM; ++mat)
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+              if (mat >= nmat || i >= ni) continue;
+              const float* s0 = src + (mat * 64 + 16 * i + g) * kMPad + 8 * nt + 2 * q;
+              v[u][mat][i][nt][0] = __ldcg(reinterpret_cast<const float2*>(s0));
+              v[u][mat][i][nt][1] = __ldcg(reinterpret_cast<const float2*>(s0 + 8 * kMPad));
+            }
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        if (w + u > w1) continue;
+#pragma unroll
+        for (int mat = 0; mat < NM; ++mat)
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+              if (mat >= nmat || i >= ni) continue;
+              acc[mat][i][nt][0] += v[u][mat][i][nt][0].x;
+              acc[mat][i][nt][1] += v[u][mat][i][nt][0].y;
+              acc[mat][i][nt][2] += v[u][mat][i][nt][1].x;
+              acc[mat][i][nt][3] += v[u][mat][i][nt][1].y;
+            }
+      }
+    }
+  }
+
+  const DBlock& B = blocks[P.b];
+  const DecExpert& X = experts[B.e];
+  if (pseudo) {
+    // t[b][mat][row][16 s + j]: D rows = rank j (g, g + 8), cols = token rows
+    const DecMat& M = X.m[P.mat];
+    float* tb = W.t + ((int64_t)P.b * 3 + P.mat) * kMPad * W.r16_max;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int j = 16 * s + g + 8 * (e >> 1), row = 8 * nt + 2 * q + (e & 1);
+        __stcg(tb + row * W.r16_max + j, acc[0][0][nt][e]);
+      }
+    __syncwarp();
+    if (lane == 0) {
+      int* cnt = W.tcnt + P.b * 3 + P.mat;
+      if (atom_add_acqrel_gpu(cnt, 1) == M.r16 / 16 - 1) {
+        *cnt = 0;
+        st_release_gpu(W.tflag + P.b * 3 + P.mat, epoch);
+      }
+    }
+    return;
+  }
+  // real slab: + t V for each matrix with a compensator
+  const int nmr = NM;
+  if (lane == 0)
+    for (int mat = 0; mat < nmr; ++mat) {
+      const int mi = ph == 0 ? mat : 2;
+      if (X.m[mi].rank > 0) spin_until(W.tflag + P.b * 3 + mi, epoch);
+    }
+  __syncwarp();
+#pragma unroll
+  for (int mat = 0; mat < NM; ++mat) {
+    if (mat >= nmr) continue;
+    const int mi = ph == 0 ? mat : 2;
+    const DecMat& M = X.m[mi];
+    if (M.rank <= 0) continue;
+    add_tv<NT>(acc[mat], M, W.t + ((int64_t)P.b * 3 + mi) * kMPad * W.r16_max, W.r16_max, s, lane);
+  }
+  const int n0 = s * kTileN;
+  if (!MOE) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int row = 8 * nt + 2 * q + (e & 1);
+          if (row >= B.rows) continue;
+          const int64_t off = (int64_t)B.slot[row] * a.ldo + n0 + 16 * i + g + 8 * (e >> 1);
+          if (a.out_dtype == 0)
+            reinterpret_cast<float*>(a.out)[off] = acc[0][i][nt][e];
+          else
+            reinterpret_cast<__half*>(a.out)[off] = __float2half_rn(acc[0][i][nt][e]);
+        }
+  } else if (ph == 0) {
+    // SwiGLU -> h rows of block b (k' = n), padding rows zero
+    __half* hb = W.h + (int64_t)P.b * kMPad * W.f_max;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int row = 8 * nt + 2 * q + (e & 1);
+          float h = silu_f(acc[0][i][nt][e]) * acc[NM - 1][i][nt][e];
+          if (row >= B.rows) h = 0.0f;
+          const float h_next = __shfl_down_sync(0xffffffffu, h, 4);  // column n + 1
+          if ((g & 1) == 0) {
+            const int n = n0 + 16 * i + g + 8 * (e >> 1);
+            __stcg(reinterpret_cast<unsigned int*>(hb + (int64_t)row * W.f_max + n),
+                   h2_as_u32(__floats2half2_rn(h, h_next)));
+          }
+        }
+    __syncwarp();
+    if (lane == 0) {
+      if (atom_add_acqrel_gpu(W.bcnt + P.b, 1) == P.n_slabs - 1) {
+        W.bcnt[P.b] = 0;
+        st_release_gpu(W.bflag + P.b, epoch);
+      }
+    }
+  } else {
+    // y rows -> Y slots; the last block of this d-slab runs the combine
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int row = 8 * nt + 2 * q + (e & 1);
+          if (row >= B.rows) continue;
+          __stcg(W.Y + (int64_t)B.slot[row] * d + n0 + 16 * i + g + 8 * (e >> 1), acc[0][i][nt][e]);
+        }
+    __syncwarp();
+    const int nb = sc[0];
+    int last = 0;
+    if (lane == 0) {
+      last = atom_add_acqrel_gpu(W.ccnt + s, 1) == nb - 1;
+      if (last) W.ccnt[s] = 0;
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last) {
+      const int K = a.K, m = a.m;
+      const int n = n0 + 2 * lane;
+      for (int t = 0; t < m; ++t) {
+        float2 o = make_float2(0.0f, 0.0f);
+        for (int k = 0; k < K; ++k) {
+          if (r_ids[t * K + k] < 0) continue;
+          const float wk = r_wts[t * K + k];
+          const float2 y = __ldcg(reinterpret_cast<const float2*>(W.Y + (int64_t)(t * K + k) * d + n));
+          o.x += wk * y.x;
+          o.y += wk * y.y;
+        }
+        for (int sh = 0; sh < a.S; ++sh) {
+          const float2 y = __ldcg(reinterpret_cast<const float2*>(W.Y + (int64_t)(m * K + sh * m + t) * d + n));
+          o.x += 1.0f * y.x;
+          o.y += 1.0f * y.y;
+        }
+        if (a.out_dtype == 0)
+          *reinterpret_cast<float2*>(static_cast<float*>(a.out) + (int64_t)t * a.ldo + n) = o;
+        else
+          *reinterpret_cast<__half2*>(static_cast<__half*>(a.out) + (int64_t)t * a.ldo + n) =
+              __floats2half2_rn(o.x, o.y);
+      }
+    }
+  }
+}
+
+// Per-warp producer (lane 0): walks the warp's units of both phases and issues
+// their weight copies (one bulk copy per matrix per unit) into the warp's ring.
+// Weights never depend on other warps, so the producer never waits.
+template <int NT, int NMAT1, bool MOE>
+struct Prod {
+  using CF = DecCfg<NT, NMAT1>;
+  uint8_t* ring;
+  uint64_t* fb;
+  const uint8_t* base0;
+  const uint8_t* base1;
+  int ph, p, s, ku, left, kts, ktiles, tb, nm, nslabs, nphase;
+
+  __device__ __forceinline__ void load(const DProb* probs, int rel) {  // unit rel of problem p
+    const DProb& P = probs[ph * kDecMaxProbs + p];
+    kts = P.kts;
+    ktiles = P.ktiles;
+    tb = P.tb;
+    nm = P.kind == 1 && ph == 0 ? NMAT1 : 1;
+    nslabs = P.n_slabs;
+    base0 = P.src[0];
+    base1 = P.src[1];
+    s = rel / kts;
+    ku = rel - s * kts;
+  }
+  __device__ __forceinline__ void seek(const DProb* probs, int ph_, int T0, int T1, int G, int gw) {
+    ph = ph_;
+    left = 0;
+    const int Tp = ph == 0 ? T0 : T1;
+    const int Gp = min(G, Tp);
+    if (gw >= Gp) return;
+    const int st = (int)((int64_t)gw * Tp / Gp), en = (int)((int64_t)(gw + 1) * Tp / Gp);
+    left = en - st;
+    const DProb* P = probs + ph * kDecMaxProbs;
+    int q = 0;
+    while (P[q].u0 + P[q].n_slabs * P[q].kts <= st) ++q;
+    p = q;
+    load(probs, st - P[q].u0);
+  }
+  __device__ __forceinline__ bool norm(const DProb* probs, int T0, int T1, int G, int gw) {
+    while (left == 0) {
+      if (ph + 1 >= nphase) return false;
+      seek(probs, ph + 1, T0, T1, G, gw);
+    }
+    return true;
+  }
+  __device__ __forceinline__ void issue(const DProb* probs, int sl) {
+    uint8_t* dst = ring + sl * CF::kSlotBytes;
+    const int t0 = ku * kDecKC;
+    const int kc = min(kDecKC, ktiles - t0);
+    const uint32_t bytes = (uint32_t)(kc * tb);
+    mbar_arrive_expect_tx(&fb[sl], bytes * (uint32_t)nm);
+    const int64_t off = ((int64_t)s * ktiles + t0) * tb;
+    bulk_g2s(dst, base0 + off, bytes, &fb[sl]);
+    if (nm == 2) bulk_g2s(dst + bytes, base1 + off, bytes, &fb[sl]);
+    --left;
+    if (++ku == kts) {
+      ku = 0;
+      if (++s == nslabs && left > 0) {
+        const DProb* P = probs + ph * kDecMaxProbs;
+        do ++p; while (P[p].n_slabs == 0);
+        load(probs, 0);
+      }
+    }
+  }
+};
+
+struct PhaseState {
+  int slot;
+  uint32_t parity;
+  long long t_wait, t_fin, t_issue, n_units;
+};
+
+// Activation rows of block B for the phase: phase 1 -> x rows (binary16,
+// row-major, ldx), phase 2 -> the block's h rows; null for padding rows.
+template <int NT>
+__device__ __forceinline__ void block_rows(const __half* (&rowp)[NT], const DBlock& B, int ph, int bidx,
+                                           const __half* xact, int64_t ldxa, const DecWs& W, int g) {
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    const int row = 8 * nt + g;
+    if (row >= B.rows) {
+      rowp[nt] = nullptr;
+    } else if (ph == 0) {
+      rowp[nt] = xact + (int64_t)B.xrow[row] * ldxa;
+    } else {
+      rowp[nt] = W.h + ((int64_t)bidx * (8 * NT) + row) * W.f_max;
+    }
+  }
+}
+
+// One phase of a warp's units: stream-K segments, each accumulated in registers
+// (NM matrices per unit) and handed to dec_finish.  B fragments for unit i + 1
+// are loaded while unit i computes.
+template <int NT, int NMAT1, bool MOE, int NM, int PH>
+__device__ __forceinline__ void run_phase(const DecArgs& a, Prod<NT, NMAT1, MOE>& pr, PhaseState& ps,
+                                          const DProb* probs, const DBlock* blocks, const DecExpert* experts,
+                                          uint8_t* ring, uint64_t* fb, const __half* xact, int64_t ldxa,
+                                          int T0, int T1, int G, int gw) {
+  using CF = DecCfg<NT, NMAT1>;
+  constexpr int kS = CF::kSlots;
+  const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  const DProb* PP = probs + PH * kDecMaxProbs;
+  const int Tp = PH == 0 ? T0 : T1;
+  const int Gp = min(G, Tp);
+  if (gw >= Gp) return;
+  const int start = (int)((int64_t)gw * Tp / Gp), end = (int)((int64_t)(gw + 1) * Tp / Gp);
+  int p = 0;
+  int pos = start;
+  DEC_DBG(PH == 0 ? 2 : 5);
+  while (pos < end) {
+    while (PP[p].u0 + PP[p].n_slabs * PP[p].kts <= pos) ++p;
+    const DProb& P = PP[p];
+    const int s = (pos - P.u0) / P.kts;
+    int ku = pos - P.u0 - s * P.kts;
+    const int seg_end = min(end, P.u0 + (s + 1) * P.kts);
+    const bool pseudo = P.kind == 0;
+    const DecMat& M = experts[blocks[P.b].e].m[P.mat];
+    const DqConsts dq = make_dq_consts(M.mode);
+    const bool preal = pseudo && M.real;
+    const int ptb = P.tb;
+    const int ktiles = P.ktiles;
+    if (PH == 1) {  // the block's h rows must be published
+      if (lane == 0) spin_until(a.ws.bflag + P.b, a.epoch);
+      __syncwarp();
+    }
+    const __half* rowp[NT];
+    block_rows<NT>(rowp, blocks[P.b], PH, P.b, xact, ldxa, a.ws, g);
+
+    float acc[NM][4][NT][4];
+#pragma unroll
+    for (int x = 0; x < NM; ++x)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc[x][i][nt][e] = 0.0f;
+
+    // k-tile pipeline over the segment: B fragments of tile t + 1 load while tile t computes
+    const int kend = ktiles * 32;
+    int k = ku * kDecKC * 32;
+    BTile<NT> bc;
+    load_btile<NT>(bc, rowp, k, true, q);
+    for (int left = seg_end - pos; left > 0; --left, ++ku) {
+      const int slot = ps.slot;
+      const int kc = min(kDecKC, ktiles - ku * kDecKC);
+      if (DEC_TIMERS) {
+        const long long tw0 = clock64();
+        mbar_wait(&fb[slot], ps.parity);
+        ps.t_wait += clock64() - tw0;
+        ++ps.n_units;
+      } else {
+        mbar_wait(&fb[slot], ps.parity);
+      }
+      const uint8_t* st = ring + slot * CF::kSlotBytes;
+#pragma unroll 1
+      for (int kk = 0; kk < kc; ++kk, k += 32) {
+        BTile<NT> bn;
+        load_btile<NT>(bn, rowp, k + 32, k + 32 < kend, q);
+        if (pseudo)
+          tile_pseudo<NT, NM>(st + kk * ptb, preal, bc, acc, lane);
+        else
+          tile_real<NT, NM, NM>(st + kk * kTileBytes, kc * kTileBytes, bc, acc, dq, lane);
+        bc = bn;
+      }
+      __syncwarp();
+      if (left == 1) break;  // the segment's last slot is the finisher's scratch (issued below)
+      if (DEC_TIMERS) {
+        const long long ti0 = clock64();
+        if (lane == 0 && pr.norm(probs, T0, T1, G, gw)) pr.issue(probs, slot);
+        ps.t_issue += clock64() - ti0;
+      } else if (lane == 0 && pr.norm(probs, T0, T1, G, gw)) {
+        pr.issue(probs, slot);
+      }
+      if (++ps.slot == kS) {
+        ps.slot = 0;
+        ps.parity ^= 1u;
+      }
+    }
+    // park the accumulators in the consumed slot, finish, then refill the slot
+    {
+      const int slot = ps.slot;
+      float* accs = reinterpret_cast<float*>(ring + slot * CF::kSlotBytes);
+#pragma unroll
+      for (int x = 0; x < NM; ++x)
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) accs[(((x * 4 + i) * NT + nt) * 4 + e) * 32 + lane] = acc[x][i][nt][e];
+      __syncwarp();
+      pos = seg_end;
+      if (pos == end) DEC_DBG(3 + 3 * PH);
+      const long long tf0 = DEC_TIMERS ? clock64() : 0;
+      dec_finish<NT, NMAT1, MOE, NM>(a, accs, PH, p, s, start, end, Gp, Tp, gw, G);
+      if (DEC_TIMERS) ps.t_fin += clock64() - tf0;
+      __syncwarp();
+      fence_proxy_async();  // generic smem use of the slot before the next bulk copy into it
+      if (lane == 0 && pr.norm(probs, T0, T1, G, gw)) pr.issue(probs, slot);
+      if (++ps.slot == kS) {
+        ps.slot = 0;
+        ps.parity ^= 1u;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- the kernel
+template <int NT, int NMAT1, bool MOE>
+__global__ void __launch_bounds__(32 * DecCfg<NT, NMAT1>::kWarps, 1)
+    decode_kernel(const __grid_constant__ DecArgs a) {
+  using CF = DecCfg<NT, NMAT1>;
+  constexpr int kC = CF::kCons, kS = CF::kSlots;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  uint64_t* full_bars = reinterpret_cast<uint64_t*>(smem + CF::kOffBars);  // [kC][kS]
+  const DProb* probs = reinterpret_cast<const DProb*>(smem + CF::kOffProbs);
+  const DBlock* blocks = reinterpret_cast<const DBlock*>(smem + CF::kOffBlocks);
+  const int32_t* sc = reinterpret_cast<const int32_t*>(smem + CF::kOffRoute) + kDecMaxTok * 32 + 256;
+  const DecWs& W = a.ws;
+  const DecExpert* experts = MOE ? a.experts : &a.lin;
+
+  for (int i = tid; i < kC * kS; i += blockDim.x) mbar_init(&full_bars[i], 1);
+  fence_barrier_init();
+  pdl_wait();
+  DEC_DBG(0);
+  if (W.xrep != nullptr) {
+    // CTA-private binary16 copy of x (the phase-1 activation rows, read from L1)
+    __half* xr = W.xrep + (int64_t)blockIdx.x * a.m * a.d;
+    const int n8 = a.m * (a.d / 8);
+    for (int i = tid; i < n8; i += blockDim.x) {
+      const int r = i / (a.d / 8), c = (i % (a.d / 8)) * 8;
+      uint4 v;
+      if (a.x_dtype == 0) {
+        const float4* src = reinterpret_cast<const float4*>(static_cast<const float*>(a.x) + (int64_t)r * a.ldx + c);
+        const float4 p0 = __ldg(src), p1 = __ldg(src + 1);
+        v = make_uint4(h2_as_u32(__floats2half2_rn(p0.x, p0.y)), h2_as_u32(__floats2half2_rn(p0.z, p0.w)),
+                       h2_as_u32(__floats2half2_rn(p1.x, p1.y)), h2_as_u32(__floats2half2_rn(p1.z, p1.w)));
+      } else {
+        v = __ldg(reinterpret_cast<const uint4*>(static_cast<const __half*>(a.x) + (int64_t)r * a.ldx + c));
+      }
+      *reinterpret_cast<uint4*>(xr + (int64_t)r * a.d + c) = v;
+    }
+  }
+  DEC_DBG(15);
+  dec_stage0<NT, NMAT1, MOE>(a);
+  DEC_DBG(1);
+  const __half* xact = W.xrep != nullptr ? W.xrep + (int64_t)blockIdx.x * a.m * a.d
+                                         : static_cast<const __half*>(a.x);
+  const int64_t ldxa = W.xrep != nullptr ? a.d : a.ldx;
+
+  const int G = a.gw;
+  const int T0 = sc[3], T1 = sc[4];
+  const int gw = blockIdx.x * kC + warp;
+  uint8_t* ring = smem + warp * kS * CF::kSlotBytes;
+  uint64_t* fb = full_bars + warp * kS;
+
+  Prod<NT, NMAT1, MOE> pr;
+  pr.ring = ring;
+  pr.fb = fb;
+  pr.nphase = MOE ? 2 : 1;
+  if (lane == 0) {
+    pr.seek(probs, 0, T0, T1, G, gw);
+    for (int sl = 0; sl < kS && pr.norm(probs, T0, T1, G, gw); ++sl) pr.issue(probs, sl);
+  }
+  __syncwarp();
+
+  PhaseState st{0, 0u, 0, 0, 0, 0};
+  run_phase<NT, NMAT1, MOE, NMAT1, 0>(a, pr, st, probs, blocks, experts, ring, fb, xact, ldxa, T0, T1, G, gw);
+  DEC_DBG(4);
+  if (MOE)
+    run_phase<NT, NMAT1, MOE, 1, 1>(a, pr, st, probs, blocks, experts, ring, fb, xact, ldxa, T0, T1, G, gw);
+  DEC_DBG(7);
+  if (DEC_TIMERS && a.dbg != nullptr && lane == 0) {
+    long long* o = a.dbg + ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * 16;
+    o[11] = st.t_wait; o[12] = st.t_fin; o[13] = st.t_issue; o[14] = st.n_units;
+  }
+  pdl_launch_dependents();
+}
+
+// f32 rows -> binary16 rows (the decode kernel's activation input).
+__global__ void rows_to_half_kernel(const float* __restrict__ x, int64_t rows, int64_t cols,
+                                    int64_t ldx, __half* __restrict__ y) {
+  const int64_t n4 = rows * (cols / 4);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / (cols / 4), c = (i % (cols / 4)) * 4;
+    const float4 v = *reinterpret_cast<const float4*>(x + r * ldx + c);
+    __half2* o = reinterpret_cast<__half2*>(y + r * cols + c);
+    o[0] = __floats2half2_rn(v.x, v.y);
+    o[1] = __floats2half2_rn(v.z, v.w);
+  }
+}
+
+}  // namespace milo_dev

@@ -5,16 +5,22 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
+#include <utility>
 #include <vector>
+
+#include <cuda_fp16.h>
 
 #include "../../include/milo_b200.h"
 #include "gemv.cuh"
 #include "kernels.cuh"
 #include "lorc.cuh"
 #include "moe.cuh"
+#include "decode.cuh"
 
 using namespace milo_dev;
 
@@ -128,6 +134,15 @@ struct Arena {
   }
 };
 
+// MILO_LEGACY=1 selects the multi-launch decode path (A/B comparisons only).
+bool legacy_path() {
+  static const bool v = [] {
+    const char* e = getenv("MILO_LEGACY");
+    return e != nullptr && e[0] == '1';
+  }();
+  return v;
+}
+
 bool tile_allowed(int tk, int tn) {
   return (tk == 64 && tn == 256) || (tk == 128 && tn == 128) || (tk == 256 && tn == 64);
 }
@@ -158,7 +173,107 @@ struct milo_comp {
   float* ureal = nullptr;     // k x rank
   float* vreal = nullptr;     // n x rank (V^T)
   int32_t gpr = 0;
+  // decode-kernel layouts (decode.cuh): U pseudo tiles, V^T fragment tiles, V steps
+  void* dmem = nullptr;
+  uint8_t* upt = nullptr;
+  uint8_t* vft = nullptr;
+  float* vstep = nullptr;
+  int32_t r16 = 0;
 };
+
+// ---------------------------------------------------------------------------
+// Compensator layouts of the decode kernel (decode.cuh), built on the host once
+// per compensator.  U pseudo tiles: A operand of t = x U (rows = 16 rank
+// columns, cols = 32 k); V fragment tiles: A operand of t V (rows = 64 n of a
+// slab, cols = 16 ranks per step).  int3: exact codes (pad code 4 == 0.0) and
+// fp32 steps s * (2/7) (lowrank.cpp:122-134, the same fp32 expression);
+// real: binary16 hi + lo split of the fp32 factors (pad 0).
+// ---------------------------------------------------------------------------
+namespace {
+
+uint16_t h16(float f) {
+  const __half h = __float2half_rn(f);
+  return *reinterpret_cast<const uint16_t*>(&h);
+}
+float f16f(uint16_t b) {
+  __half h;
+  *reinterpret_cast<uint16_t*>(&h) = b;
+  return __half2float(h);
+}
+
+cudaError_t build_decode_layouts(milo_comp* c, const milo_comp_desc* d) {
+  const uint64_t k = d->rows, n = d->cols, r = d->rank;
+  const bool real = d->storage != 1;
+  const uint64_t r16 = (r + 15) / 16 * 16, nks = r16 / 16, gpr = (r + 63) / 64;
+  c->r16 = (int32_t)r16;
+  if (k % 32 != 0 || n % 64 != 0) return cudaSuccess;  // not a GEMM shape: no decode layout
+  const uint64_t upt_b = nks * (k / 32) * (real ? kPseudoRealBytes : kPseudoInt3Bytes);
+  const uint64_t vft_b = (n / 64) * nks * (real ? kVftRealBytes : kVftInt3Bytes);
+  const uint64_t vst_b = real ? 0 : n * gpr * 4;
+  std::vector<uint8_t> host(upt_b + vft_b + vst_b, 0);
+  uint8_t* upt = host.data();
+  uint8_t* vft = upt + upt_b;
+  float* vst = reinterpret_cast<float*>(vft + vft_b);
+  auto ucode = [&](uint64_t kk, uint64_t j) -> uint8_t { return j < r ? d->qu_codes[kk * r + j] : 4; };
+  auto vcode = [&](uint64_t nn, uint64_t j) -> uint8_t { return j < r ? d->qvt_codes[nn * r + j] : 4; };
+  auto uval = [&](uint64_t kk, uint64_t j) -> float { return j < r ? d->U[kk * r + j] : 0.0f; };
+  auto vval = [&](uint64_t nn, uint64_t j) -> float { return j < r ? d->V[j * n + nn] : 0.0f; };
+  auto put_split = [](uint8_t* dst, float v) {  // hi at dst, lo at dst + 16
+    const uint16_t hi = h16(v);
+    const uint16_t lo = h16(v - f16f(hi));
+    memcpy(dst, &hi, 2);
+    memcpy(dst + 16, &lo, 2);
+  };
+  for (uint64_t rc = 0; rc < nks; ++rc)
+    for (uint64_t kt = 0; kt < k / 32; ++kt) {
+      uint8_t* tile = upt + (rc * (k / 32) + kt) * (real ? kPseudoRealBytes : kPseudoInt3Bytes);
+      for (int lane = 0; lane < 32; ++lane)
+        for (int ks = 0; ks < 2; ++ks)
+          for (int a = 0; a < 4; ++a)
+            for (int h = 0; h < 2; ++h) {
+              const int g = lane >> 2, q = lane & 3;
+              const uint64_t j = rc * 16 + g + 8 * (a & 1);
+              const uint64_t kk = kt * 32 + 16 * ks + 2 * q + 8 * (a >> 1) + h;
+              if (!real)
+                tile[lane * 16 + ks * 8 + 2 * a + h] = ucode(kk, j);
+              else
+                put_split(tile + lane * 64 + ks * 32 + a * 4 + h * 2, uval(kk, j));
+            }
+      if (!real) {
+        float* st = reinterpret_cast<float*>(tile + 512);
+        const uint64_t grp = (rc * 16) / 64;
+        for (int i = 0; i < 32; ++i) st[i] = d->qu_scales[(kt * 32 + i) * gpr + grp] * (2.0f / 7.0f);
+      }
+    }
+  for (uint64_t slab = 0; slab < n / 64; ++slab)
+    for (uint64_t ks = 0; ks < nks; ++ks) {
+      uint8_t* tile = vft + (slab * nks + ks) * (real ? kVftRealBytes : kVftInt3Bytes);
+      for (int lane = 0; lane < 32; ++lane)
+        for (int i = 0; i < 4; ++i)
+          for (int a = 0; a < 4; ++a)
+            for (int h = 0; h < 2; ++h) {
+              const int g = lane >> 2, q = lane & 3;
+              const uint64_t nn = slab * 64 + 16 * i + g + 8 * (a & 1);
+              const uint64_t j = 16 * ks + 2 * q + 8 * (a >> 1) + h;
+              if (!real)
+                tile[lane * 32 + i * 8 + 2 * a + h] = vcode(nn, j);
+              else
+                put_split(tile + lane * 128 + i * 32 + a * 4 + h * 2, vval(nn, j));
+            }
+    }
+  if (!real)
+    for (uint64_t nn = 0; nn < n; ++nn)
+      for (uint64_t gg = 0; gg < gpr; ++gg) vst[nn * gpr + gg] = d->qvt_scales[nn * gpr + gg] * (2.0f / 7.0f);
+  cudaError_t e = cudaMalloc(&c->dmem, host.size());
+  if (e != cudaSuccess) return e;
+  e = cudaMemcpy(c->dmem, host.data(), host.size(), cudaMemcpyHostToDevice);
+  c->upt = static_cast<uint8_t*>(c->dmem);
+  c->vft = c->upt + upt_b;
+  c->vstep = real ? nullptr : reinterpret_cast<float*>(c->vft + vft_b);
+  return e;
+}
+
+}  // namespace
 
 extern "C" {
 
@@ -410,8 +525,10 @@ milo_status milo_comp_create(const milo_comp_desc* d, milo_comp** out) {
     e = cudaMemcpy(c->ureal, d->U, k * r * 4, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(c->vreal, vt.data(), n * r * 4, cudaMemcpyHostToDevice);
   }
+  if (e == cudaSuccess) e = build_decode_layouts(c, d);
   if (e != cudaSuccess) {
     cudaFree(c->mem);
+    if (c->dmem) cudaFree(c->dmem);
     delete c;
     return fail(MILO_ERR_CUDA, "upload failed: %s", cudaGetErrorString(e));
   }
@@ -422,6 +539,7 @@ milo_status milo_comp_create(const milo_comp_desc* d, milo_comp** out) {
 milo_status milo_comp_destroy(milo_comp* c) {
   if (!c) return MILO_OK;
   if (c->mem) cudaFree(c->mem);
+  if (c->dmem) cudaFree(c->dmem);
   delete c;
   return MILO_OK;
 }
@@ -534,6 +652,158 @@ milo_status validate_gemm(const milo_weight* w, const milo_comp* comp, const mil
 
 }  // namespace
 
+
+// ---------------------------------------------------------------------------
+// Decode kernel (decode.cuh): per-(device, stream) workspace and launcher.
+// ---------------------------------------------------------------------------
+namespace {
+
+DecMat make_decmat(const milo_weight* w, const milo_comp* c) {
+  DecMat M{};
+  M.w = w->tiles;
+  M.k = (int32_t)w->rows;
+  M.n = (int32_t)w->cols;
+  M.mode = w->mode;
+  if (c && c->rank > 0 && c->upt) {
+    M.upt = c->upt;
+    M.vft = c->vft;
+    M.vstep = c->vstep;
+    M.rank = (int32_t)c->rank;
+    M.r16 = c->r16;
+    M.gpr = c->gpr;
+    M.real = c->storage != 1;
+  }
+  return M;
+}
+
+constexpr int kCntCap = 1 << 17;   // slab counters per phase
+constexpr int kCCntCap = 4096;     // d-slab (combine) counters
+// control block (int32, zeroed once; counters return to zero after every call,
+// flags hold the epoch of the call that set them)
+constexpr size_t kCtrlInts = 2 * (size_t)kCntCap + kDecMaxBlocks * 3 + kDecMaxBlocks + kCCntCap +
+                             kDecMaxBlocks * 3 + kDecMaxBlocks;
+
+struct DecodeWs {
+  int32_t* ctrl = nullptr;
+  void* data = nullptr;
+  size_t data_bytes = 0;
+  int epoch = 0;
+};
+std::mutex g_ws_mu;
+long long* g_dbg = nullptr;  // milo_debug_timeline
+int g_dbg_flags = 0;
+std::map<std::pair<int, cudaStream_t>, DecodeWs> g_ws;
+
+// Returns the workspace of (device, stream) with >= data_bytes of data space and
+// the epoch of this call.  Stream-ordered: a grown buffer frees the old one on
+// the same stream.
+milo_status get_ws(cudaStream_t stream, size_t data_bytes, DecodeWs** out, int* epoch) {
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(g_ws_mu);
+  DecodeWs& w = g_ws[{dev, stream}];
+  if (!w.ctrl) {
+    CUDA_TRY(cudaMalloc(&w.ctrl, kCtrlInts * 4));
+    CUDA_TRY(cudaMemset(w.ctrl, 0, kCtrlInts * 4));
+  }
+  if (w.data_bytes < data_bytes) {
+    if (w.data) CUDA_TRY(cudaFreeAsync(w.data, stream));
+    w.data = nullptr;
+    w.data_bytes = 0;
+    CUDA_TRY(cudaMallocAsync(&w.data, data_bytes, stream));
+    w.data_bytes = data_bytes;
+  }
+  *epoch = ++w.epoch;
+  *out = &w;
+  return MILO_OK;
+}
+
+template <int NT, int NMAT1, bool MOE>
+milo_status launch_decode(DecArgs a, const void* x, int32_t x_dtype, int64_t ldx, int nb_max,
+                          int f_max, int r16_max, int64_t y_rows, cudaStream_t stream, int sms) {
+  using CF = DecCfg<NT, NMAT1>;
+  static thread_local int configured_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured_dev != dev) {
+    CUDA_TRY(set_smem(decode_kernel<NT, NMAT1, MOE>, CF::kBytes));
+    configured_dev = dev;
+  }
+  const int G = sms * CF::kCons;
+  const int m_pad = CF::kMPad;
+  Arena ar;
+  const int64_t part_stride = CF::kPartMax;
+  const size_t o_part = ar.take((size_t)2 * G * 2 * part_stride * 4);
+  const size_t o_t = ar.take((size_t)nb_max * 3 * m_pad * std::max(r16_max, 16) * 4);
+  const size_t o_h = ar.take(MOE ? (size_t)nb_max * m_pad * f_max * 2 : 0);
+  const size_t o_y = ar.take(MOE ? (size_t)y_rows * a.d * 4 : 0);
+  const bool replicate = a.m <= 16;  // CTA-private x copies (decode.cuh)
+  const size_t o_x = ar.take(replicate ? (size_t)sms * a.m * a.d * 2
+                                       : (x_dtype == 0 ? (size_t)a.m * a.d * 2 : 0));
+  DecodeWs* w = nullptr;
+  int epoch = 0;
+  milo_status st = get_ws(stream, ar.size, &w, &epoch);
+  if (st != MILO_OK) return st;
+  uint8_t* base = static_cast<uint8_t*>(w->data);
+  int32_t* c = w->ctrl;
+  DecWs& W = a.ws;
+  W.part = reinterpret_cast<float*>(base + o_part);
+  W.t = reinterpret_cast<float*>(base + o_t);
+  W.h = reinterpret_cast<__half*>(base + o_h);
+  W.Y = reinterpret_cast<float*>(base + o_y);
+  W.cnt1 = c;
+  W.cnt2 = c + kCntCap;
+  W.tcnt = W.cnt2 + kCntCap;
+  W.bcnt = W.tcnt + kDecMaxBlocks * 3;
+  W.ccnt = W.bcnt + kDecMaxBlocks;
+  W.tflag = W.ccnt + kCCntCap;
+  W.bflag = W.tflag + kDecMaxBlocks * 3;
+  W.part_stride = part_stride;
+  W.r16_max = std::max(r16_max, 16);
+  W.f_max = f_max;
+  a.epoch = epoch;
+  a.gw = G;
+  a.dbg = g_dbg;
+  a.dbg_flags = g_dbg_flags;
+  W.xrep = nullptr;
+  a.x = x;
+  a.x_dtype = x_dtype;
+  a.ldx = ldx;
+  if (replicate) {
+    W.xrep = reinterpret_cast<__half*>(base + o_x);
+  } else if (x_dtype == 0) {  // the kernel reads binary16 rows: round f32 rows once (gemm.cpp:144-146)
+    __half* x16 = reinterpret_cast<__half*>(base + o_x);
+    const int64_t n4 = (int64_t)a.m * (a.d / 4);
+    const int grid = (int)std::min<int64_t>((n4 + 255) / 256, (int64_t)sms * 4);
+    CUDA_TRY(launch(rows_to_half_kernel, dim3(std::max(grid, 1)), dim3(256), 0, stream, false,
+                    static_cast<const float*>(x), (int64_t)a.m, (int64_t)a.d, ldx, x16));
+    a.x = x16;
+    a.x_dtype = 1;
+    a.ldx = a.d;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(sms);
+  cfg.blockDim = dim3(32 * CF::kWarps);
+  cfg.dynamicSmemBytes = CF::kBytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  ++g_launches;
+  ProfScope ps(kProfGemv1, stream);
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, decode_kernel<NT, NMAT1, MOE>, a));
+  return MILO_OK;
+}
+
+}  // namespace
+
+// Debug hook (not in the public header): per-warp globaltimer stamps of the
+// next decode launches, [grid warps][8] int64 on the device; NULL disables.
+extern "C" void milo_debug_timeline(long long* dev_ptr) { g_dbg = dev_ptr; }
+extern "C" void milo_debug_flags(int flags) { g_dbg_flags = flags; }
+
 extern "C" milo_status milo_gemm_w3a16(const milo_weight* w, const milo_comp* comp,
                                        const milo_gemm_config* cfg, const void* A, int64_t m,
                                        int64_t a_cols, int32_t a_dtype, void* C, int32_t c_dtype,
@@ -553,6 +823,30 @@ extern "C" milo_status milo_gemm_w3a16(const milo_weight* w, const milo_comp* co
   const int nt = m <= 8 ? 1 : 2;
   const int m_pad = 8 * nt;
   const int64_t k = (int64_t)w->rows, n = (int64_t)w->cols;
+  if (!legacy_path()) {
+    DecArgs a{};
+    a.moe = 0;
+    a.lin.m[0] = make_decmat(w, comp);
+    a.d = (int32_t)k;
+    a.out_dtype = c_dtype;
+    a.ldo = n;
+    const int r16 = a.lin.m[0].r16;
+    const int64_t per_block_slabs = n / 64 + r16 / 16;
+    const int64_t max_blocks = std::max<int64_t>(1, std::min<int64_t>(kDecMaxBlocks, kCntCap / per_block_slabs));
+    const size_t xs = a_dtype == 0 ? 4 : 2, cs = c_dtype == 0 ? 4 : 2;
+    for (int64_t done = 0; done < m;) {
+      const int64_t mm = std::min<int64_t>(m - done, max_blocks * m_pad);
+      a.m = (int32_t)mm;
+      const void* xa = static_cast<const uint8_t*>(A) + done * a_cols * xs;
+      a.out = static_cast<uint8_t*>(C) + done * n * cs;
+      const int nb = (int)((mm + m_pad - 1) / m_pad);
+      st = nt == 1 ? launch_decode<1, 1, false>(a, xa, a_dtype, a_cols, nb, 0, r16, 0, stream, props.sms)
+                   : launch_decode<2, 1, false>(a, xa, a_dtype, a_cols, nb, 0, r16, 0, stream, props.sms);
+      if (st != MILO_OK) return st;
+      done += mm;
+    }
+    return MILO_OK;
+  }
   const int rank = (comp && comp->rank > 0) ? (int)comp->rank : 0;
   int64_t done = 0;
   while (done < m) {
@@ -666,6 +960,8 @@ struct milo_moe {
   int32_t E = 0, n_shared = 0, K = 0, score_mode = 0;
   int32_t d = 0, f_max = 0, rank1_max = 0, rank2_max = 0;
   ExpertDev* dev_experts = nullptr;  // E + n_shared entries
+  DecExpert* dec_experts = nullptr;  // decode-kernel view of the same experts
+  int32_t r16_max = 0;
 };
 
 extern "C" milo_status milo_moe_create(const milo_expert_desc* experts, int32_t n_experts,
@@ -680,6 +976,7 @@ extern "C" milo_status milo_moe_create(const milo_expert_desc* experts, int32_t 
     return fail(MILO_ERR_CONFIG, "top_k must be in [1, min(16, n_experts)]");
   if (score_mode != 0 && score_mode != 1) return fail(MILO_ERR_CONFIG, "unknown score mode");
   std::vector<ExpertDev> host(n_experts + n_shared);
+  std::vector<DecExpert> dhost(n_experts + n_shared);
   auto* moe = new milo_moe();
   moe->E = n_experts;
   moe->n_shared = n_shared;
@@ -709,6 +1006,10 @@ extern "C" milo_status milo_moe_create(const milo_expert_desc* experts, int32_t 
       return fail(MILO_ERR_CONFIG, "expert %d: w1 and w3 modes differ", i);
     }
     ExpertDev& e = host[i];
+    for (int j = 0; j < 3; ++j) {
+      dhost[i].m[j] = make_decmat(w[j], c[j]);
+      moe->r16_max = std::max(moe->r16_max, dhost[i].m[j].r16);
+    }
     e.f = (int32_t)f;
     e.mode = w[0]->mode;
     moe->f_max = std::max(moe->f_max, (int32_t)f);
@@ -740,8 +1041,13 @@ extern "C" milo_status milo_moe_create(const milo_expert_desc* experts, int32_t 
   if (err == cudaSuccess)
     err = cudaMemcpy(moe->dev_experts, host.data(), host.size() * sizeof(ExpertDev),
                      cudaMemcpyHostToDevice);
+  if (err == cudaSuccess) err = cudaMalloc(&moe->dec_experts, dhost.size() * sizeof(DecExpert));
+  if (err == cudaSuccess)
+    err = cudaMemcpy(moe->dec_experts, dhost.data(), dhost.size() * sizeof(DecExpert),
+                     cudaMemcpyHostToDevice);
   if (err != cudaSuccess) {
     cudaFree(moe->dev_experts);
+    cudaFree(moe->dec_experts);
     delete moe;
     return fail(MILO_ERR_CUDA, "expert table upload failed: %s", cudaGetErrorString(err));
   }
@@ -752,6 +1058,7 @@ extern "C" milo_status milo_moe_create(const milo_expert_desc* experts, int32_t 
 extern "C" milo_status milo_moe_destroy(milo_moe* moe) {
   if (!moe) return MILO_OK;
   cudaFree(moe->dev_experts);
+  cudaFree(moe->dec_experts);
   delete moe;
   return MILO_OK;
 }
@@ -892,6 +1199,32 @@ milo_status moe_forward_impl(milo_moe* moe, const void* x, int64_t m, int32_t x_
   DeviceProps props = device_props();
   if (!props.ok || props.major != 10) return fail(MILO_ERR_CUDA, "no sm_100 device");
   cudaStream_t stream = (cudaStream_t)stream_;
+  const int64_t nb_dec = std::min<int64_t>(moe->E, m * moe->K) + moe->n_shared;
+  if (!legacy_path() && m <= kDecMaxTok && nb_dec <= kDecMaxBlocks && moe->E <= 256 &&
+      moe->K <= 16 && moe->d / 64 <= 4096) {
+    DecArgs a{};
+    a.moe = 1;
+    a.m = (int32_t)m;
+    a.logits = logits;
+    a.ids_in = logits ? nullptr : ids;
+    a.wts_in = logits ? nullptr : wts;
+    a.ids_out = logits ? ids : nullptr;
+    a.wts_out = logits ? wts : nullptr;
+    a.E = moe->E;
+    a.K = moe->K;
+    a.S = moe->n_shared;
+    a.score_mode = moe->score_mode;
+    a.experts = moe->dec_experts;
+    a.d = moe->d;
+    a.out = out;
+    a.out_dtype = out_dtype;
+    a.ldo = moe->d;
+    const int64_t y_rows = m * moe->K + (int64_t)moe->n_shared * m;
+    return m <= 8 ? launch_decode<1, 2, true>(a, x, x_dtype, moe->d, (int)nb_dec, moe->f_max,
+                                              moe->r16_max, y_rows, stream, props.sms)
+                  : launch_decode<2, 2, true>(a, x, x_dtype, moe->d, (int)nb_dec, moe->f_max,
+                                              moe->r16_max, y_rows, stream, props.sms);
+  }
   // Token chunks keep every launch under the problem-table bound.
   const int nt = m <= 8 ? 1 : 2;
   const int m_pad = 8 * nt;
