@@ -21,6 +21,7 @@
 #include "lorc.cuh"
 #include "moe.cuh"
 #include "decode.cuh"
+#include "prefill.cuh"
 
 using namespace milo_dev;
 
@@ -799,6 +800,56 @@ milo_status launch_decode(DecArgs a, const void* x, int32_t x_dtype, int64_t ldx
 
 }  // namespace
 
+
+// ---------------------------------------------------------------------------
+// Prefill (tcgen05) path: activation images + pf_gemm_kernel.
+// ---------------------------------------------------------------------------
+namespace {
+
+int prefill_min_rows() {
+  static const int v = [] {
+    const char* e = getenv("MILO_PF_MIN");
+    return e ? atoi(e) : 64;
+  }();
+  return v;
+}
+
+template <int NMAT>
+milo_status launch_prefill(const PfProblem* host_probs, int n_probs, cudaStream_t stream, int sms,
+                           uint8_t* scratch) {
+  using CF = PfCfg<NMAT>;
+  static thread_local int configured_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured_dev != dev) {
+    CUDA_TRY(set_smem(pf_gemm_kernel<NMAT>, CF::kBytes));
+    configured_dev = dev;
+  }
+  std::vector<int32_t> starts(n_probs + 1, 0);
+  for (int i = 0; i < n_probs; ++i) {
+    const PfProblem& P = host_probs[i];
+    starts[i + 1] = starts[i] + (P.n / kPfM) * ((P.rows + kPfN - 1) / kPfN);
+  }
+  // problem table + starts travel in the scratch buffer (stream-ordered upload)
+  const size_t pb = (size_t)n_probs * sizeof(PfProblem);
+  CUDA_TRY(cudaMemcpyAsync(scratch, host_probs, pb, cudaMemcpyHostToDevice, stream));
+  CUDA_TRY(cudaMemcpyAsync(scratch + ((pb + 255) & ~size_t(255)), starts.data(), starts.size() * 4,
+                           cudaMemcpyHostToDevice, stream));
+  PfArgs a{};
+  a.dbg = g_dbg;
+  a.flags = g_dbg_flags;
+  a.problems = reinterpret_cast<const PfProblem*>(scratch);
+  a.item_start = reinterpret_cast<const int32_t*>(scratch + ((pb + 255) & ~size_t(255)));
+  a.n_problems = n_probs;
+  a.n_items = starts[n_probs];
+  if (a.n_items == 0) return MILO_OK;
+  const int grid = std::min(a.n_items, sms);
+  CUDA_TRY(launch(pf_gemm_kernel<NMAT>, dim3(grid), dim3(kPfThreads), CF::kBytes, stream, false, a));
+  return MILO_OK;
+}
+
+}  // namespace
+
 // Debug hook (not in the public header): per-warp globaltimer stamps of the
 // next decode launches, [grid warps][8] int64 on the device; NULL disables.
 extern "C" void milo_debug_timeline(long long* dev_ptr) { g_dbg = dev_ptr; }
@@ -823,6 +874,34 @@ extern "C" milo_status milo_gemm_w3a16(const milo_weight* w, const milo_comp* co
   const int nt = m <= 8 ? 1 : 2;
   const int m_pad = 8 * nt;
   const int64_t k = (int64_t)w->rows, n = (int64_t)w->cols;
+  if (!legacy_path() && m >= prefill_min_rows() && !(comp && comp->rank > 0)) {
+    // tcgen05 path: activation images (binary16, SW128) then the grouped GEMM
+    const int64_t tiles = (m + kPfN - 1) / kPfN, ks = k / kPfK;
+    void* mem = nullptr;
+    const size_t img_b = (size_t)tiles * ks * kPfImg;
+    CUDA_TRY(cudaMallocAsync(&mem, img_b + 4096, stream));
+    uint8_t* img = static_cast<uint8_t*>(mem);
+    cudaError_t e = launch(pf_image_kernel, dim3((unsigned)(tiles * ks)), dim3(256), 0, stream, false, A,
+                           a_dtype, (int64_t)a_cols, (const int32_t*)nullptr, (int32_t)m, (int32_t)k, img);
+    if (e != cudaSuccess) {
+      cudaFreeAsync(mem, stream);
+      return fail(MILO_ERR_CUDA, "launch failed: %s", cudaGetErrorString(e));
+    }
+    PfProblem P{};
+    P.w[0] = w->tiles;
+    P.act = img;
+    P.k = (int32_t)k;
+    P.n = (int32_t)n;
+    P.rows = (int32_t)m;
+    P.mode = w->mode;
+    P.kind = 0;
+    P.out_dtype = c_dtype;
+    P.ldo = n;
+    P.out = C;
+    st = launch_prefill<1>(&P, 1, stream, props.sms, img + img_b);
+    cudaFreeAsync(mem, stream);
+    return st;
+  }
   if (!legacy_path()) {
     DecArgs a{};
     a.moe = 0;

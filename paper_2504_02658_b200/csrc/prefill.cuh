@@ -1,0 +1,537 @@
+// K3: the prefill-regime W3A16 + LoRC GEMM on the 5th-generation tensor cores
+// (tcgen05.mma, accumulators in TMEM), for token counts where the weights are
+// worth reusing across many tokens (m_e >= ~64 per matrix).
+//
+// Reference semantics, per matrix: milo::gemm_w3a16 (proj/src/gemm.cpp:117-199)
+//   C = half(A) * dequant(W) + (half(A) U) V, fp32 accumulation.
+//
+// Per work item (problem p, n-tile of 128 output columns = 2 slabs, token tile
+// of 128 rows) one CTA computes D[128 n][128 tok] = W^T X^T in TMEM:
+//   * producer warp : cp.async.bulk of the packed INT3 macro tiles (2 slabs x
+//                     2 k-tiles per 64-k stage) and of the stage's activation
+//                     "image" (16 KB, already binary16, SW128 K-major, built by
+//                     pf_image_kernel), and of the LoRC images;
+//   * dequant warps : packed tiles -> bit-exact binary16 weights written into
+//                     the A operand (128 n rows x 64 k, SW128 K-major);
+//   * MMA thread    : 4 x tcgen05.mma.kind::f16 (K = 16) per stage, then
+//                     tcgen05.commit to release the stage;
+//   * epilogue warps: tcgen05.ld (32 lanes x 32 columns) -> C rows / SwiGLU.
+// The compensator term (t V) runs as extra K stages of the same accumulator:
+// A = V^T image (hi or lo binary16 half of the fp32 values), B = t image (hi
+// or lo), three MMAs per 64-rank chunk (hi.hi + hi.lo + lo.hi), i.e. fp32-level
+// accuracy on the tensor cores.
+#pragma once
+#include <cstdint>
+#include <cuda_fp16.h>
+
+#include "layout.cuh"
+#include "ptx.cuh"
+
+namespace milo_dev {
+
+constexpr int kPfM = 128;              // output columns per tile (UMMA M)
+constexpr int kPfN = 128;              // tokens per tile (UMMA N, TMEM columns)
+constexpr int kPfK = 64;               // k per stage (128 B of binary16 per operand row)
+constexpr int kPfImg = kPfN * kPfK * 2;  // 16 KB: one operand image (128 rows x 128 B)
+constexpr int kPfPackedPerMat = 2 * 2 * kTileBytes;  // 2 slabs x 2 k-tiles = 3584 B
+constexpr int kPfDeqWarps = 8;
+constexpr int kPfEpiWarps = 4;         // warps 0..3: TMEM lanes 32 w .. 32 w + 31
+constexpr int kPfProdWarp = 4;         // packed-weight producer
+constexpr int kPfMmaWarp = 5;
+constexpr int kPfBWarp = 6;            // activation / t image producer
+constexpr int kPfDeqWarp0 = 7;
+constexpr int kPfThreads = 32 * (kPfDeqWarp0 + kPfDeqWarps);  // 15 warps
+
+template <int NMAT>
+struct PfCfg {
+  static constexpr int kPS = NMAT == 1 ? 12 : 8;         // packed-weight ring (deep: HBM latency)
+  static constexpr int kAS = NMAT == 1 ? 4 : 3;          // dequantized A ring
+  static constexpr int kBS = NMAT == 1 ? 4 : 3;          // activation image ring (L2)
+  static constexpr int kStageA = NMAT * kPfImg;
+  static constexpr int kStageB = kPfImg;
+  static constexpr int kStageP = NMAT * kPfPackedPerMat;
+  static constexpr int kOffA = 0;                        // 1024-aligned images first
+  static constexpr int kOffB = kOffA + kAS * kStageA;
+  static constexpr int kOffP = kOffB + kBS * kStageB;
+  static constexpr int kOffBar = kOffP + kPS * kStageP;
+  // p_full[PS] p_empty[PS] a_full[AS] a_empty[AS] v_full[AS] b_full[BS] b_empty[BS] acc_full[2] acc_empty[2]
+  static constexpr int kNumBars = 2 * kPS + 3 * kAS + 2 * kBS + 4;
+  static constexpr int kOffTmem = kOffBar + kNumBars * 8;
+  static constexpr int kOffStage = (kOffTmem + 16 + 127) & ~127;  // epilogue transpose [4 warps][32][33] f32
+  static constexpr int kBytes = kOffStage + kPfEpiWarps * 32 * 33 * 4 + 1024;  // + alignment slack
+  static constexpr int kTmemCols = 2 * NMAT * kPfN;      // double-buffered accumulators
+};
+
+// One GEMM problem: a weight matrix (or w1|w3 pair) times a block of token rows.
+struct PfProblem {
+  const uint8_t* w[2];      // macro tiles (slab-major) of matrix 0 / 1
+  const uint8_t* act;       // activation images [tok_tiles][k/64][16 KB]
+  const uint8_t* vimg[2];   // V^T images [n/128][r64 chunks][hi, lo][16 KB] (null: no LoRC)
+  const uint8_t* timg[2];   // t images  [tok_tiles][r64 chunks][hi, lo][16 KB]
+  int32_t rchunks[2];       // 64-rank chunks of each compensator (0: none)
+  int32_t k, n, rows;       // rows = tokens of this problem
+  int32_t mode;
+  int32_t kind;             // 0: store rows (f32 / f16), 1: SwiGLU -> binary16 rows
+  int32_t out_dtype;
+  int64_t ldo;
+  void* out;                // row r of the problem -> out + row_map[r] * ldo
+  const int32_t* row_map;   // null: identity
+};
+
+struct PfArgs {
+  long long* dbg;             // optional per-CTA role timeline (globaltimer ns), [cta][8]
+  int32_t flags;              // debug: bit 0 skip dequant math, bit 1 skip MMAs
+  const PfProblem* problems;
+  int32_t n_problems;
+  const int32_t* item_start;  // exclusive prefix of work items per problem (n_problems + 1)
+  int32_t n_items;
+};
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint64_t pf_desc_sw128(uint32_t saddr) {
+  // UMMA shared-memory descriptor, K-major SWIZZLE_128B: rows of 128 B, 8-row
+  // atoms 1024 B apart (SBO = 64 x 16 B), LBO = 1, version 1 (sm_100).
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1u << 16;
+  d |= (uint64_t)64u << 32;
+  d |= (uint64_t)1u << 46;
+  d |= (uint64_t)2u << 61;
+  return d;
+}
+// Instruction descriptor: kind::f16, A/B binary16 K-major, D fp32, M = 128, N = kPfN.
+__device__ __forceinline__ uint32_t pf_idesc() {
+  return (1u << 4) | ((uint32_t)(kPfN >> 3) << 17) | ((uint32_t)(kPfM >> 4) << 24);
+}
+__device__ __forceinline__ void pf_mma(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                       uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+      ::"r"(tmem_d), "l"(da), "l"(db), "r"(idesc), "r"(accum));
+}
+__device__ __forceinline__ void pf_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+        "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+        "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+        "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ float pf_silu(float a) { return a / (1.0f + expf(-a)); }
+// Latency-critical handoffs spin on the non-blocking test (no suspend window).
+__device__ __forceinline__ void pf_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+
+// Work item -> (problem, n-tile, token tile).  Items of a problem are n-tile
+// major so consecutive items share the activation images (L2 reuse).
+__device__ __forceinline__ void pf_item(const PfArgs& a, int item, int& p, int& nt, int& tt) {
+  int lo = 0, hi = a.n_problems - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (a.item_start[mid] <= item) lo = mid; else hi = mid - 1;
+  }
+  p = lo;
+  const PfProblem P = a.problems[p];  // by value: fields live in registers
+  const int tts = (P.rows + kPfN - 1) / kPfN;
+  const int rel = item - a.item_start[p];
+  nt = rel / tts;
+  tt = rel - nt * tts;
+}
+
+// ---------------------------------------------------------------- the kernel
+// Persistent: CTA c handles items c, c + grid, ...  Three rings decouple the
+// roles: packed weights (deep, HBM latency), dequantized A, activation images.
+// Every role walks the same stage sequence: per item, k / 64 main stages then
+// 3 LoRC stages per 64-rank chunk per matrix.
+template <int NMAT>
+__global__ void __launch_bounds__(kPfThreads, 1) pf_gemm_kernel(const __grid_constant__ PfArgs a) {
+  using CF = PfCfg<NMAT>;
+  constexpr int PS = CF::kPS, AS = CF::kAS, BS = CF::kBS;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-B aligned base (SW128 atoms); pointer arithmetic keeps the shared address space
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + CF::kOffBar);
+  uint64_t* p_full = bars;
+  uint64_t* p_empty = p_full + PS;
+  uint64_t* a_full = p_empty + PS;
+  uint64_t* a_empty = a_full + AS;
+  uint64_t* v_full = a_empty + AS;
+  uint64_t* b_full = v_full + AS;
+  uint64_t* b_empty = b_full + BS;
+  uint64_t* acc_full = b_empty + BS;  // [2]
+  uint64_t* acc_empty = acc_full + 2;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + CF::kOffTmem);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < PS; ++s) {
+      mbar_init(&p_full[s], 1);
+      mbar_init(&p_empty[s], kPfDeqWarps);
+    }
+    for (int s = 0; s < AS; ++s) {
+      mbar_init(&a_full[s], kPfDeqWarps);
+      mbar_init(&a_empty[s], 1);
+      mbar_init(&v_full[s], 1);
+    }
+    for (int s = 0; s < BS; ++s) {
+      mbar_init(&b_full[s], 1);
+      mbar_init(&b_empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], kPfEpiWarps);
+    }
+    fence_barrier_init();
+  }
+  if (warp == kPfMmaWarp) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(CF::kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+  auto pf_dbg = [&](int i) {
+    if (a.dbg != nullptr) {
+      long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      a.dbg[blockIdx.x * 8 + i] = t;
+    }
+  };
+  if (threadIdx.x == 0) pf_dbg(0);
+
+  auto item_stages = [&](const PfProblem& P) {
+    return P.k / kPfK + 3 * (P.rchunks[0] + (NMAT == 2 ? P.rchunks[1] : 0));
+  };
+  // LoRC stage l (0-based after the main stages) -> matrix, chunk, V part, t part
+  auto lorc_stage = [&](const PfProblem& P, int l, int& mat, int& ch, int& vpart, int& tpart) {
+    mat = 0;
+    if (l >= 3 * P.rchunks[0]) {
+      l -= 3 * P.rchunks[0];
+      mat = 1;
+    }
+    ch = l / 3;
+    const int part = l % 3;  // 0: V_hi.t_hi, 1: V_hi.t_lo, 2: V_lo.t_hi
+    vpart = part == 2 ? 1 : 0;
+    tpart = part == 1 ? 1 : 0;
+  };
+
+  if (warp == kPfProdWarp) {
+    // ======================= packed-weight producer =======================
+    if (lane == 0) {
+      int ps = 0;
+      uint32_t pph = 0;
+      for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
+        int p, nt, tt;
+        pf_item(a, item, p, nt, tt);
+        const PfProblem P = a.problems[p];  // by value: fields live in registers
+        const int ks = P.k / kPfK, kts = P.k / kTileK;
+        for (int st = 0; st < ks; ++st) {
+          mbar_wait(&p_empty[ps], pph ^ 1);
+
+          uint8_t* sP = smem + CF::kOffP + ps * CF::kStageP;
+          mbar_arrive_expect_tx(&p_full[ps], (uint32_t)CF::kStageP);
+          for (int mat = 0; mat < NMAT; ++mat)
+            for (int sl = 0; sl < 2; ++sl) {
+              const uint8_t* src = P.w[mat] + ((int64_t)(2 * nt + sl) * kts + 2 * st) * kTileBytes;
+              bulk_g2s(sP + (mat * 2 + sl) * 2 * kTileBytes, src, 2 * kTileBytes, &p_full[ps]);
+            }
+          if (++ps == PS) {
+            ps = 0;
+            pph ^= 1;
+          }
+        }
+      }
+      pf_dbg(1);
+    }
+  } else if (warp == kPfBWarp) {
+    // ======================= activation / t image producer =======================
+    if (lane == 0) {
+      int bs = 0;
+      uint32_t bph = 0;
+      for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
+        int p, nt, tt;
+        pf_item(a, item, p, nt, tt);
+        const PfProblem P = a.problems[p];  // by value: fields live in registers
+        const int ks = P.k / kPfK, total = item_stages(P);
+        for (int st = 0; st < total; ++st) {
+          mbar_wait(&b_empty[bs], bph ^ 1);
+          uint8_t* sB = smem + CF::kOffB + bs * CF::kStageB;
+          const uint8_t* src;
+          if (st < ks) {
+            src = P.act + ((int64_t)tt * ks + st) * kPfImg;
+          } else {
+            int mat, ch, vpart, tpart;
+            lorc_stage(P, st - ks, mat, ch, vpart, tpart);
+            src = P.timg[mat] + (((int64_t)tt * P.rchunks[mat] + ch) * 2 + tpart) * kPfImg;
+          }
+          mbar_arrive_expect_tx(&b_full[bs], (uint32_t)kPfImg);
+          bulk_g2s(sB, src, kPfImg, &b_full[bs]);
+          if (++bs == BS) {
+            bs = 0;
+            bph ^= 1;
+          }
+        }
+      }
+      pf_dbg(2);
+    }
+  } else if (warp >= kPfDeqWarp0) {
+    // ======================= dequant warps =======================
+    const int dw = warp - kPfDeqWarp0;
+    const int g = lane >> 2, q = lane & 3;
+    int ps = 0, as = 0;
+    uint32_t pph = 0, aph = 0;
+    for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
+      int p, nt, tt;
+      pf_item(a, item, p, nt, tt);
+      const PfProblem P = a.problems[p];  // by value: fields live in registers
+      const int ks = P.k / kPfK, total = item_stages(P);
+      const DqConsts dq = make_dq_consts(P.mode);
+      for (int st = 0; st < total; ++st) {
+        uint8_t* sA = smem + CF::kOffA + as * CF::kStageA;
+        // warp 0 waits for the A slot, then either fetches a V image into it
+        // (LoRC stage) or just releases the other warps (v_full)
+        if (dw == 0 && lane == 0) {
+          mbar_wait(&a_empty[as], aph ^ 1);
+          if (st >= ks) {
+            int mat, ch, vpart, tpart;
+            lorc_stage(P, st - ks, mat, ch, vpart, tpart);
+            mbar_arrive_expect_tx(&v_full[as], (uint32_t)kPfImg);
+            bulk_g2s(sA + mat * kPfImg, P.vimg[mat] + (((int64_t)nt * P.rchunks[mat] + ch) * 2 + vpart) * kPfImg,
+                     kPfImg, &v_full[as]);
+          } else {
+            mbar_arrive(&v_full[as]);
+          }
+        }
+        mbar_wait(&v_full[as], aph);
+        if (st < ks) {
+          mbar_wait(&p_full[ps], pph);
+          if (dw == 0 && lane == 0 && st == 0) pf_dbg(7);
+          const uint8_t* sP = smem + CF::kOffP + ps * CF::kStageP;
+#pragma unroll
+          for (int job = 0; job < ((a.flags & 1) ? 0 : NMAT); ++job) {
+            const int jid = dw * NMAT + job;
+            const int j = jid & 1, t4 = jid >> 1;
+            const int kt = t4 & 1, sl = (t4 >> 1) & 1, mat = t4 >> 2;
+            const uint8_t* tile = sP + ((mat * 2 + sl) * 2 + kt) * kTileBytes;
+            const uint32_t* pa = reinterpret_cast<const uint32_t*>(tile + kPlaneAOff + lane * 16);
+            const uint32_t* pb = reinterpret_cast<const uint32_t*>(tile + kPlaneBOff + lane * 8);
+            const uint4 mm = *reinterpret_cast<const uint4*>(tile + kMetaOff + q * 32 + 16 * j);
+            const uint32_t S2[2] = {mm.x, mm.z}, O2[2] = {mm.y, mm.w};
+            uint32_t wv[16];
+            unit_dequant(pa[2 * j], pa[2 * j + 1], pb[j], S2, O2, dq, wv);
+            uint8_t* A = sA + mat * kPfImg;
+#pragma unroll
+            for (int pp = 0; pp < 16; ++pp) {
+              const int i = pp >> 2, r = pp & 3;
+              const int n = sl * 64 + 16 * i + g + 8 * (r & 1);
+              const int k = kt * 32 + 16 * j + 2 * q + 8 * (r >> 1);
+              const uint32_t off = (uint32_t)n * 128u + (uint32_t)(((k >> 3) ^ (n & 7)) << 4) + (uint32_t)((k & 7) * 2);
+              *reinterpret_cast<uint32_t*>(A + off) = wv[pp];
+            }
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&p_empty[ps]);
+          if (++ps == PS) {
+            ps = 0;
+            pph ^= 1;
+          }
+          fence_proxy_async();  // generic smem writes -> tensor-core (async proxy) reads
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&a_full[as]);
+        if (++as == AS) {
+          as = 0;
+          aph ^= 1;
+        }
+      }
+    }
+    if (dw == 0 && lane == 0) pf_dbg(3);
+  } else if (warp == kPfMmaWarp) {
+    // ======================= MMA issuer =======================
+    if (lane == 0) {
+      const uint32_t idesc = pf_idesc();
+      int as = 0, bs = 0;
+      uint32_t aph = 0, bph = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
+        int p, nt, tt;
+        pf_item(a, item, p, nt, tt);
+        const PfProblem P = a.problems[p];  // by value: fields live in registers
+        const int ks = P.k / kPfK, total = item_stages(P);
+        mbar_wait(&acc_empty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d0 = tmem + (uint32_t)(acc * NMAT * kPfN);
+        for (int st = 0; st < total; ++st) {
+          mbar_wait(&a_full[as], aph);
+          mbar_wait(&b_full[bs], bph);
+          tc_fence_after();
+          const uint32_t aA = smem_u32(smem + CF::kOffA + as * CF::kStageA);
+          const uint32_t aB = smem_u32(smem + CF::kOffB + bs * CF::kStageB);
+          int mat0 = 0, mat1 = NMAT;
+          if (st >= ks) {
+            int mat, ch, vpart, tpart;
+            lorc_stage(P, st - ks, mat, ch, vpart, tpart);
+            mat0 = mat;
+            mat1 = mat + 1;
+          }
+          for (int mat = mat0; mat < mat1; ++mat) {
+#pragma unroll
+            for (int k16 = 0; k16 < kPfK / 16; ++k16) {
+              const uint64_t da = pf_desc_sw128(aA + mat * kPfImg + k16 * 32);
+              const uint64_t db = pf_desc_sw128(aB + k16 * 32);
+              if (!(a.flags & 2)) pf_mma(d0 + (uint32_t)(mat * kPfN), da, db, idesc, (st > 0 || k16 > 0) ? 1u : 0u);
+            }
+          }
+          pf_commit(&a_empty[as]);
+          pf_commit(&b_empty[bs]);
+          if (++as == AS) {
+            as = 0;
+            aph ^= 1;
+          }
+          if (++bs == BS) {
+            bs = 0;
+            bph ^= 1;
+          }
+        }
+        pf_commit(&acc_full[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+      pf_dbg(4);
+    }
+  } else {
+    // ======================= epilogue warps 0..3 =======================
+    const int ew = warp;  // TMEM lanes 32 ew .. 32 ew + 31 = A rows (output columns)
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
+      int p, nt, tt;
+      pf_item(a, item, p, nt, tt);
+      const PfProblem P = a.problems[p];  // by value: fields live in registers
+      mbar_wait(&acc_full[acc], acc_phase);
+      tc_fence_after();
+      if (threadIdx.x == 0) pf_dbg(6);
+      // TMEM -> registers (thread = output column, 32 tokens per load) -> SwiGLU /
+      // identity -> smem transpose -> 16-byte row stores (8 token rows per instruction)
+      const uint32_t tbase = tmem + ((uint32_t)(32 * ew) << 16) + (uint32_t)(acc * NMAT * kPfN);
+      const int rows = P.rows, kind = P.kind, odt = P.out_dtype;
+      const int64_t ldo = P.ldo;
+      const int32_t* rmap = P.row_map;
+      float* stg = reinterpret_cast<float*>(smem + CF::kOffStage) + ew * 32 * 33;
+      const int col0 = nt * kPfM + 32 * ew + 8 * (lane & 3);  // this lane's 8 output columns
+#pragma unroll 1
+      for (int c0 = 0; c0 < kPfN; c0 += 32) {
+        uint32_t v0[32], v1[32];
+        tmem_ld32(tbase + (uint32_t)c0, v0);
+        if (NMAT == 2) tmem_ld32(tbase + (uint32_t)(kPfN + c0), v1);
+        tmem_ld_wait();
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          float x = __uint_as_float(v0[c]);
+          if (kind == 1) x = pf_silu(x) * (NMAT == 2 ? __uint_as_float(v1[c]) : 0.0f);
+          stg[c * 33 + lane] = x;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+          const int tr = 8 * it + (lane >> 2);  // token row within the chunk
+          const int row = tt * kPfN + c0 + tr;
+          if (row < rows) {
+            const int64_t orow = rmap ? rmap[row] : row;
+            const float* src = stg + tr * 33 + 8 * (lane & 3);
+            float f[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) f[u] = src[u];
+            if (kind == 0 && odt == 0) {
+              float4* dst = reinterpret_cast<float4*>(static_cast<float*>(P.out) + orow * ldo + col0);
+              dst[0] = make_float4(f[0], f[1], f[2], f[3]);
+              dst[1] = make_float4(f[4], f[5], f[6], f[7]);
+            } else {
+              uint4 h;
+              h.x = h2_as_u32(__floats2half2_rn(f[0], f[1]));
+              h.y = h2_as_u32(__floats2half2_rn(f[2], f[3]));
+              h.z = h2_as_u32(__floats2half2_rn(f[4], f[5]));
+              h.w = h2_as_u32(__floats2half2_rn(f[6], f[7]));
+              *reinterpret_cast<uint4*>(static_cast<__half*>(P.out) + orow * ldo + col0) = h;
+            }
+          }
+        }
+        __syncwarp();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  if (threadIdx.x == 0) pf_dbg(5);
+  __syncthreads();
+  if (warp == kPfMmaWarp) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(CF::kTmemCols));
+  }
+  pdl_launch_dependents();
+}
+
+// Activation images: rows (binary16 or f32 source, optional row gather) ->
+// [tok_tiles][k/64][128 rows x 128 B, SW128 K-major], zero rows past `rows`.
+__global__ void pf_image_kernel(const void* __restrict__ x, int32_t x_dtype, int64_t ldx,
+                                const int32_t* __restrict__ row_ids, int32_t rows, int32_t k,
+                                uint8_t* __restrict__ img) {
+  const int ks = k / kPfK;
+  const int tile = blockIdx.x / ks, st = blockIdx.x % ks;
+  uint8_t* dst = img + (int64_t)blockIdx.x * kPfImg;
+  for (int c = threadIdx.x; c < kPfN * 8; c += blockDim.x) {  // 16-B chunks
+    const int r = c >> 3, ch = c & 7;
+    const int row = tile * kPfN + r;
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (row < rows) {
+      const int64_t src_row = row_ids ? row_ids[row] : row;
+      const int64_t col = (int64_t)st * kPfK + ch * 8;
+      if (x_dtype == 0) {
+        const float4* s = reinterpret_cast<const float4*>(static_cast<const float*>(x) + src_row * ldx + col);
+        const float4 p0 = s[0], p1 = s[1];
+        v = make_uint4(h2_as_u32(__floats2half2_rn(p0.x, p0.y)), h2_as_u32(__floats2half2_rn(p0.z, p0.w)),
+                       h2_as_u32(__floats2half2_rn(p1.x, p1.y)), h2_as_u32(__floats2half2_rn(p1.z, p1.w)));
+      } else {
+        v = *reinterpret_cast<const uint4*>(static_cast<const __half*>(x) + src_row * ldx + col);
+      }
+    }
+    *reinterpret_cast<uint4*>(dst + r * 128 + ((ch ^ (r & 7)) << 4)) = v;
+  }
+  pdl_launch_dependents();
+}
+
+}  // namespace milo_dev
