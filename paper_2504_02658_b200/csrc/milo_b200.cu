@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <array>
 #include <map>
 #include <mutex>
 #include <string>
@@ -180,6 +181,10 @@ struct milo_comp {
   uint8_t* vft = nullptr;
   float* vstep = nullptr;
   int32_t r16 = 0;
+  // prefill (tcgen05) layout: V^T operand images [n/128][r/64][hi, lo][16 KB]
+  void* pmem = nullptr;
+  uint8_t* vimg = nullptr;
+  int32_t rch = 0;
 };
 
 // ---------------------------------------------------------------------------
@@ -271,6 +276,32 @@ cudaError_t build_decode_layouts(milo_comp* c, const milo_comp_desc* d) {
   c->upt = static_cast<uint8_t*>(c->dmem);
   c->vft = c->upt + upt_b;
   c->vstep = real ? nullptr : reinterpret_cast<float*>(c->vft + vft_b);
+  if (e != cudaSuccess || n % kPfM != 0) return e;
+  // prefill V^T images: row = output column n of the 128-tile, K = rank (64 per
+  // chunk), SW128 K-major binary16, value v = step * (c - 4) (lowrank.cpp:122-134)
+  // or real V, split into hi + lo halves
+  const uint64_t rch = (r + 63) / 64;
+  c->rch = (int32_t)rch;
+  std::vector<uint8_t> img((n / kPfM) * rch * 2 * kPfImg, 0);
+  for (uint64_t nn = 0; nn < n; ++nn)
+    for (uint64_t j = 0; j < rch * 64; ++j) {
+      float v = 0.0f;
+      if (j < r) {
+        if (!real)
+          v = (d->qvt_scales[nn * gpr + j / 64] * (2.0f / 7.0f)) * ((float)d->qvt_codes[nn * r + j] - 4.0f);
+        else
+          v = d->V[j * n + nn];
+      }
+      const uint16_t hi = h16(v), lo = h16(v - f16f(hi));
+      const uint64_t tile = nn / kPfM, row = nn % kPfM, ch = j / 64, jj = j % 64;
+      const uint64_t off = row * 128 + (((jj >> 3) ^ (row & 7)) << 4) + (jj & 7) * 2;
+      uint8_t* b = img.data() + ((tile * rch + ch) * 2) * kPfImg;
+      memcpy(b + off, &hi, 2);
+      memcpy(b + kPfImg + off, &lo, 2);
+    }
+  e = cudaMalloc(&c->pmem, img.size());
+  if (e == cudaSuccess) e = cudaMemcpy(c->pmem, img.data(), img.size(), cudaMemcpyHostToDevice);
+  c->vimg = static_cast<uint8_t*>(c->pmem);
   return e;
 }
 
@@ -541,6 +572,7 @@ milo_status milo_comp_destroy(milo_comp* c) {
   if (!c) return MILO_OK;
   if (c->mem) cudaFree(c->mem);
   if (c->dmem) cudaFree(c->dmem);
+  if (c->pmem) cudaFree(c->pmem);
   delete c;
   return MILO_OK;
 }
@@ -806,6 +838,9 @@ milo_status launch_decode(DecArgs a, const void* x, int32_t x_dtype, int64_t ldx
 // ---------------------------------------------------------------------------
 namespace {
 
+// token tile of the tcgen05 GEMM for a problem with `rows` tokens: 16 .. 128
+int pf_ntok(int64_t rows) { return (int)std::min<int64_t>(kPfN, (rows + 15) / 16 * 16); }
+
 int prefill_min_rows() {
   static const int v = [] {
     const char* e = getenv("MILO_PF_MIN");
@@ -826,9 +861,11 @@ milo_status launch_prefill(const PfProblem* host_probs, int n_probs, cudaStream_
     configured_dev = dev;
   }
   std::vector<int32_t> starts(n_probs + 1, 0);
+  int ntok_max = 16;
   for (int i = 0; i < n_probs; ++i) {
     const PfProblem& P = host_probs[i];
-    starts[i + 1] = starts[i] + (P.n / kPfM) * ((P.rows + kPfN - 1) / kPfN);
+    ntok_max = std::max(ntok_max, (int)P.ntok);
+    starts[i + 1] = starts[i] + (P.n / kPfM) * ((P.rows + P.ntok - 1) / P.ntok);
   }
   // problem table + starts travel in the scratch buffer (stream-ordered upload)
   const size_t pb = (size_t)n_probs * sizeof(PfProblem);
@@ -836,6 +873,7 @@ milo_status launch_prefill(const PfProblem* host_probs, int n_probs, cudaStream_
   CUDA_TRY(cudaMemcpyAsync(scratch + ((pb + 255) & ~size_t(255)), starts.data(), starts.size() * 4,
                            cudaMemcpyHostToDevice, stream));
   PfArgs a{};
+  a.ntok_max = ntok_max;
   a.dbg = g_dbg;
   a.flags = g_dbg_flags;
   a.problems = reinterpret_cast<const PfProblem*>(scratch);
@@ -844,7 +882,7 @@ milo_status launch_prefill(const PfProblem* host_probs, int n_probs, cudaStream_
   a.n_items = starts[n_probs];
   if (a.n_items == 0) return MILO_OK;
   const int grid = std::min(a.n_items, sms);
-  CUDA_TRY(launch(pf_gemm_kernel<NMAT>, dim3(grid), dim3(kPfThreads), CF::kBytes, stream, false, a));
+  CUDA_TRY(launch(pf_gemm_kernel<NMAT>, dim3(grid), dim3(PfRoles<NMAT>::kThreads), CF::kBytes, stream, false, a));
   return MILO_OK;
 }
 
@@ -874,15 +912,50 @@ extern "C" milo_status milo_gemm_w3a16(const milo_weight* w, const milo_comp* co
   const int nt = m <= 8 ? 1 : 2;
   const int m_pad = 8 * nt;
   const int64_t k = (int64_t)w->rows, n = (int64_t)w->cols;
-  if (!legacy_path() && m >= prefill_min_rows() && !(comp && comp->rank > 0)) {
+  const bool pf_comp_ok = !(comp && comp->rank > 0) || comp->vimg != nullptr;
+  if (!legacy_path() && m >= prefill_min_rows() && n % kPfM == 0 && pf_comp_ok) {
     // tcgen05 path: activation images (binary16, SW128) then the grouped GEMM
-    const int64_t tiles = (m + kPfN - 1) / kPfN, ks = k / kPfK;
+    const int ntok = pf_ntok(m);
+    const int64_t tiles = (m + ntok - 1) / ntok, ks = k / kPfK;
     void* mem = nullptr;
-    const size_t img_b = (size_t)tiles * ks * kPfImg;
-    CUDA_TRY(cudaMallocAsync(&mem, img_b + 4096, stream));
+    const size_t img_b = (size_t)tiles * ks * ntok * 128;
+    const bool lorc = comp && comp->rank > 0;
+    TProb tp{};
+    size_t t_img_b = 0, t_part_b = 0;
+    int t_units = 0;
+    if (lorc) {
+      tp.x = A;
+      tp.x_dtype = a_dtype;
+      tp.ldx = a_cols;
+      tp.rows = (int32_t)m;
+      tp.k = (int32_t)k;
+      tp.rank = (int32_t)comp->rank;
+      tp.gpr = comp->gpr;
+      tp.rchunks = comp->rch;
+      const int row_tiles = (int)((m + kTRows - 1) / kTRows);
+      tp.ks = std::max(1, std::min<int>((int)(k / 256), (2 * props.sms) / std::max(1, row_tiles * tp.rchunks)));
+      tp.ucodes = comp->ucodes;
+      tp.uscales = comp->uscales;
+      tp.ureal = comp->ureal;
+      t_units = row_tiles * tp.rchunks * tp.ks;
+      tp.ntok = ntok;
+      t_img_b = (size_t)tiles * tp.rchunks * 2 * ntok * 128;
+      t_part_b = (size_t)tp.ks * m * tp.rchunks * 64 * 4;
+    }
+    CUDA_TRY(cudaMallocAsync(&mem, img_b + t_img_b + t_part_b + 8192, stream));
     uint8_t* img = static_cast<uint8_t*>(mem);
+    if (lorc) {
+      tp.timg = img + img_b;
+      tp.part = reinterpret_cast<float*>(img + img_b + t_img_b);
+      TProb* dtp = reinterpret_cast<TProb*>(img + img_b + t_img_b + t_part_b + 4096);
+      CUDA_TRY(cudaMemcpyAsync(dtp, &tp, sizeof(TProb), cudaMemcpyHostToDevice, stream));
+      CUDA_TRY(launch(pf_t_kernel, dim3(t_units), dim3(256), 0, stream, false, (const TProb*)dtp, 1));
+      CUDA_TRY(launch(pf_t_images_kernel, dim3((unsigned)std::min<int64_t>(1024, (tiles * ntok * tp.rchunks * 64 + 255) / 256), 1),
+                      dim3(256), 0, stream, false, (const TProb*)dtp, 1));
+    }
     cudaError_t e = launch(pf_image_kernel, dim3((unsigned)(tiles * ks)), dim3(256), 0, stream, false, A,
-                           a_dtype, (int64_t)a_cols, (const int32_t*)nullptr, (int32_t)m, (int32_t)k, img);
+                           a_dtype, (int64_t)a_cols, (const int32_t*)nullptr, (int32_t)m, (int32_t)k,
+                           (int32_t)ntok, img);
     if (e != cudaSuccess) {
       cudaFreeAsync(mem, stream);
       return fail(MILO_ERR_CUDA, "launch failed: %s", cudaGetErrorString(e));
@@ -893,12 +966,18 @@ extern "C" milo_status milo_gemm_w3a16(const milo_weight* w, const milo_comp* co
     P.k = (int32_t)k;
     P.n = (int32_t)n;
     P.rows = (int32_t)m;
+    P.ntok = ntok;
     P.mode = w->mode;
     P.kind = 0;
     P.out_dtype = c_dtype;
     P.ldo = n;
     P.out = C;
-    st = launch_prefill<1>(&P, 1, stream, props.sms, img + img_b);
+    if (lorc) {
+      P.vimg[0] = comp->vimg;
+      P.timg[0] = tp.timg;
+      P.rchunks[0] = comp->rch;
+    }
+    st = launch_prefill<1>(&P, 1, stream, props.sms, img + img_b + t_img_b + t_part_b);
     cudaFreeAsync(mem, stream);
     return st;
   }
@@ -1041,6 +1120,10 @@ struct milo_moe {
   ExpertDev* dev_experts = nullptr;  // E + n_shared entries
   DecExpert* dec_experts = nullptr;  // decode-kernel view of the same experts
   int32_t r16_max = 0;
+  // prefill view: per expert, per matrix (w1, w3, w2) weight tiles + compensator
+  std::vector<std::array<const milo_weight*, 3>> hw;
+  std::vector<std::array<const milo_comp*, 3>> hc;
+  bool prefill_ok = true;
 };
 
 extern "C" milo_status milo_moe_create(const milo_expert_desc* experts, int32_t n_experts,
@@ -1085,6 +1168,12 @@ extern "C" milo_status milo_moe_create(const milo_expert_desc* experts, int32_t 
       return fail(MILO_ERR_CONFIG, "expert %d: w1 and w3 modes differ", i);
     }
     ExpertDev& e = host[i];
+    moe->hw.push_back({w[0], w[1], w[2]});
+    moe->hc.push_back({c[0], c[1], c[2]});
+    for (int j = 0; j < 3; ++j) {
+      const bool comp_ok = !(c[j] && c[j]->rank > 0) || c[j]->vimg != nullptr;
+      if (w[j]->cols % kPfM != 0 || w[j]->rows % kPfK != 0 || !comp_ok) moe->prefill_ok = false;
+    }
     for (int j = 0; j < 3; ++j) {
       dhost[i].m[j] = make_decmat(w[j], c[j]);
       moe->r16_max = std::max(moe->r16_max, dhost[i].m[j].r16);
@@ -1264,6 +1353,229 @@ milo_status moe_run(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype,
 
 namespace {
 
+// Prefill MoE layer on the tcgen05 GEMM (m > 16 tokens): routing on the device,
+// one host synchronization to plan the grouped GEMMs (per-expert token lists in
+// ascending token order), then per phase: activation images, t = x U, the
+// grouped W3A16 + LoRC GEMM (phase 1 with SwiGLU), and the weighted combine.
+milo_status moe_prefill(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype, const float* logits,
+                        int32_t* ids, float* wts, void* out, int32_t out_dtype, cudaStream_t stream, int sms) {
+  const int E = moe->E, K = moe->K, S = moe->n_shared;
+  const int64_t d = moe->d;
+  if (K > 0 && logits) {
+    CUDA_TRY(launch(router_topk_kernel, dim3((unsigned)((m + 7) / 8)), dim3(256), 0, stream, false, logits, m, E,
+                    K, moe->score_mode, ids, wts));
+  }
+  // ---- plan on the host (the reference composition order)
+  std::vector<int32_t> hids((size_t)m * std::max(K, 1));
+  if (K > 0) {
+    CUDA_TRY(cudaMemcpyAsync(hids.data(), ids, hids.size() * 4, cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaStreamSynchronize(stream));
+  }
+  struct Grp { int e; int64_t off, rows; };
+  std::vector<Grp> groups;
+  std::vector<int32_t> tok, slot;  // per grouped row: x row, Y slot
+  for (int e = 0; e < E + S; ++e) {
+    Grp g{e, (int64_t)tok.size(), 0};
+    for (int64_t t = 0; t < m; ++t) {
+      if (e < E) {
+        for (int k = 0; k < K; ++k)
+          if (hids[t * K + k] == e) {
+            tok.push_back((int32_t)t);
+            slot.push_back((int32_t)(t * K + k));
+          }
+      } else {
+        tok.push_back((int32_t)t);
+        slot.push_back((int32_t)(m * K + (int64_t)(e - E) * m + t));
+      }
+    }
+    g.rows = (int64_t)tok.size() - g.off;
+    if (g.rows > 0) groups.push_back(g);
+  }
+  const int64_t R = (int64_t)tok.size();  // grouped rows
+  const int64_t f_max = moe->f_max;
+  // ---- workspace
+  Arena ar;
+  const size_t o_tok = ar.take((size_t)R * 4), o_slot = ar.take((size_t)R * 4);
+  std::vector<size_t> o_img1(groups.size()), o_img2(groups.size());
+  int64_t tiles_tot = 0;
+  for (size_t gi = 0; gi < groups.size(); ++gi) {
+    const int nt = pf_ntok(groups[gi].rows);
+    const int64_t tiles = (groups[gi].rows + nt - 1) / nt;
+    tiles_tot += tiles;
+    o_img1[gi] = ar.take((size_t)tiles * (d / kPfK) * nt * 128);
+    o_img2[gi] = ar.take((size_t)tiles * (f_max / kPfK) * nt * 128);
+  }
+  const size_t o_h = ar.take((size_t)R * f_max * 2);
+  const size_t o_y = ar.take((size_t)(m * K + (int64_t)S * m) * d * 4);
+  // t problems: up to 3 per group
+  std::vector<TProb> tps[2];
+  std::vector<size_t> o_timg[3], o_part[3];
+  for (int j = 0; j < 3; ++j) {
+    o_timg[j].assign(groups.size(), 0);
+    o_part[j].assign(groups.size(), 0);
+  }
+  for (size_t gi = 0; gi < groups.size(); ++gi)
+    for (int j = 0; j < 3; ++j) {
+      const milo_comp* c = moe->hc[groups[gi].e][j];
+      if (!c || c->rank == 0) continue;
+      const int64_t rows = groups[gi].rows;
+      const int nt = pf_ntok(rows);
+      const int64_t tiles = (rows + nt - 1) / nt;
+      const int64_t kk = moe->hw[groups[gi].e][j]->rows;
+      const int row_tiles = (int)((rows + kTRows - 1) / kTRows);
+      const int ks = std::max(1, std::min<int>((int)(kk / 256), (2 * sms) / std::max(1, row_tiles * c->rch)));
+      o_timg[j][gi] = ar.take((size_t)tiles * c->rch * 2 * nt * 128);
+      o_part[j][gi] = ar.take((size_t)ks * rows * c->rch * 64 * 4);
+    }
+  const size_t o_tab = ar.take(262144);
+  void* mem = nullptr;
+  CUDA_TRY(cudaMallocAsync(&mem, ar.size, stream));
+  uint8_t* base = static_cast<uint8_t*>(mem);
+  int32_t* dtok = reinterpret_cast<int32_t*>(base + o_tok);
+  int32_t* dslot = reinterpret_cast<int32_t*>(base + o_slot);
+  __half* hbuf = reinterpret_cast<__half*>(base + o_h);
+  float* Y = reinterpret_cast<float*>(base + o_y);
+  uint8_t* tab = base + o_tab;
+  milo_status st = MILO_OK;
+  auto guard = [&](cudaError_t e) {
+    if (e != cudaSuccess && st == MILO_OK) st = fail(MILO_ERR_CUDA, "prefill: %s", cudaGetErrorString(e));
+  };
+  guard(cudaMemcpyAsync(dtok, tok.data(), (size_t)R * 4, cudaMemcpyHostToDevice, stream));
+  guard(cudaMemcpyAsync(dslot, slot.data(), (size_t)R * 4, cudaMemcpyHostToDevice, stream));
+  size_t tab_off = 0;
+  auto upload = [&](const void* src, size_t bytes) -> uint8_t* {
+    uint8_t* dst = tab + tab_off;
+    tab_off = (tab_off + bytes + 255) & ~size_t(255);
+    if (bytes && src) guard(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream));
+    return dst;
+  };
+  auto run_t = [&](int phase, const void* src, int32_t sdt, int64_t ldx, bool gather) {
+    std::vector<TProb> v;
+    int units = 0;
+    const int mats[2] = {phase == 0 ? 0 : 2, phase == 0 ? 1 : -1};
+    for (size_t gi = 0; gi < groups.size(); ++gi)
+      for (int mi : mats) {
+        if (mi < 0) continue;
+        const milo_comp* c = moe->hc[groups[gi].e][mi];
+        if (!c || c->rank == 0) continue;
+        TProb tp{};
+        const int64_t rows = groups[gi].rows;
+        tp.x = gather ? src : static_cast<const uint8_t*>(src) + groups[gi].off * ldx * 2;
+        tp.x_dtype = sdt;
+        tp.ldx = ldx;
+        tp.row_ids = gather ? dtok + groups[gi].off : nullptr;
+        tp.rows = (int32_t)rows;
+        tp.k = (int32_t)moe->hw[groups[gi].e][mi]->rows;
+        tp.rank = (int32_t)c->rank;
+        tp.gpr = c->gpr;
+        tp.rchunks = c->rch;
+        const int row_tiles = (int)((rows + kTRows - 1) / kTRows);
+        tp.ks = std::max(1, std::min<int>(tp.k / 256, (2 * sms) / std::max(1, row_tiles * c->rch)));
+        tp.ucodes = c->ucodes;
+        tp.uscales = c->uscales;
+        tp.ureal = c->ureal;
+        tp.timg = base + o_timg[mi][gi];
+        tp.part = reinterpret_cast<float*>(base + o_part[mi][gi]);
+        tp.ntok = pf_ntok(rows);
+        tp.unit0 = units;
+        units += row_tiles * tp.rchunks * tp.ks;
+        v.push_back(tp);
+      }
+    if (v.empty()) return;
+    const TProb* dv = reinterpret_cast<const TProb*>(upload(v.data(), v.size() * sizeof(TProb)));
+    guard(launch(pf_t_kernel, dim3(units), dim3(256), 0, stream, false, dv, (int)v.size()));
+    guard(launch(pf_t_images_kernel, dim3(256, (unsigned)v.size()), dim3(256), 0, stream, false, dv, (int)v.size()));
+  };
+  // ---- phase 1: x rows -> images; t1, t3; w1|w3 + LoRC + SwiGLU -> h
+  for (size_t gi = 0; gi < groups.size() && st == MILO_OK; ++gi) {
+    const int nt = pf_ntok(groups[gi].rows);
+    const int64_t tiles = (groups[gi].rows + nt - 1) / nt;
+    guard(launch(pf_image_kernel, dim3((unsigned)(tiles * (d / kPfK))), dim3(256), 0, stream, false, x, x_dtype,
+                 (int64_t)d, (const int32_t*)(dtok + groups[gi].off), (int32_t)groups[gi].rows, (int32_t)d,
+                 (int32_t)nt, base + o_img1[gi]));
+  }
+  run_t(0, x, x_dtype, d, true);
+  {
+    std::vector<PfProblem> pv;
+    for (size_t gi = 0; gi < groups.size(); ++gi) {
+      const int e = groups[gi].e;
+      PfProblem P{};
+      P.w[0] = moe->hw[e][0]->tiles;
+      P.w[1] = moe->hw[e][1]->tiles;
+      P.act = base + o_img1[gi];
+      for (int mi = 0; mi < 2; ++mi) {
+        const milo_comp* c = moe->hc[e][mi];
+        if (c && c->rank > 0) {
+          P.vimg[mi] = c->vimg;
+          P.timg[mi] = base + o_timg[mi][gi];
+          P.rchunks[mi] = c->rch;
+        }
+      }
+      P.k = (int32_t)d;
+      P.n = (int32_t)moe->hw[e][0]->cols;
+      P.rows = (int32_t)groups[gi].rows;
+      P.ntok = pf_ntok(groups[gi].rows);
+      P.mode = moe->hw[e][0]->mode;
+      P.kind = 1;
+      P.out_dtype = 1;
+      P.ldo = f_max;
+      P.out = hbuf + groups[gi].off * f_max;
+      pv.push_back(P);
+    }
+    if (st == MILO_OK)
+      st = launch_prefill<2>(pv.data(), (int)pv.size(), stream, sms,
+                             upload(nullptr, pv.size() * sizeof(PfProblem) + 4096));
+  }
+  (void)tiles_tot;
+  // ---- phase 2: h rows -> images; t2; w2 + LoRC -> Y slots
+  for (size_t gi = 0; gi < groups.size() && st == MILO_OK; ++gi) {
+    const int e = groups[gi].e;
+    const int64_t f = moe->hw[e][2]->rows;
+    const int nt = pf_ntok(groups[gi].rows);
+    const int64_t tiles = (groups[gi].rows + nt - 1) / nt;
+    guard(launch(pf_image_kernel, dim3((unsigned)(tiles * (f / kPfK))), dim3(256), 0, stream, false,
+                 (const void*)(hbuf + groups[gi].off * f_max), 1, f_max, (const int32_t*)nullptr,
+                 (int32_t)groups[gi].rows, (int32_t)f, (int32_t)nt, base + o_img2[gi]));
+  }
+  run_t(1, hbuf, 1, f_max, false);
+  if (st == MILO_OK) {
+    std::vector<PfProblem> pv;
+    for (size_t gi = 0; gi < groups.size(); ++gi) {
+      const int e = groups[gi].e;
+      PfProblem P{};
+      P.w[0] = moe->hw[e][2]->tiles;
+      P.act = base + o_img2[gi];
+      const milo_comp* c = moe->hc[e][2];
+      if (c && c->rank > 0) {
+        P.vimg[0] = c->vimg;
+        P.timg[0] = base + o_timg[2][gi];
+        P.rchunks[0] = c->rch;
+      }
+      P.k = (int32_t)moe->hw[e][2]->rows;
+      P.n = (int32_t)d;
+      P.rows = (int32_t)groups[gi].rows;
+      P.ntok = pf_ntok(groups[gi].rows);
+      P.mode = moe->hw[e][2]->mode;
+      P.kind = 0;
+      P.out_dtype = 0;
+      P.ldo = d;
+      P.out = Y;
+      P.row_map = dslot + groups[gi].off;
+      pv.push_back(P);
+    }
+    st = launch_prefill<1>(pv.data(), (int)pv.size(), stream, sms,
+                           upload(nullptr, pv.size() * sizeof(PfProblem) + 4096));
+  }
+  if (st == MILO_OK) {
+    const int64_t total = m * (d / 4);
+    const int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)sms * 8);
+    guard(launch(moe_combine_kernel, dim3(grid), dim3(256), 0, stream, false, (const float*)Y,
+                 (const int32_t*)ids, (const float*)wts, m, K, S, d, out, out_dtype));
+  }
+  cudaFreeAsync(mem, stream);
+  return st;
+}
+
 // logits != nullptr: the route kernel computes the top-k into ids / wts
 // (outputs); otherwise ids / wts are the given routing (inputs).
 milo_status moe_forward_impl(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype,
@@ -1304,6 +1616,9 @@ milo_status moe_forward_impl(milo_moe* moe, const void* x, int64_t m, int32_t x_
                   : launch_decode<2, 2, true>(a, x, x_dtype, moe->d, (int)nb_dec, moe->f_max,
                                               moe->r16_max, y_rows, stream, props.sms);
   }
+  if (!legacy_path() && moe->prefill_ok && m > kDecMaxTok && m >= prefill_min_rows() / 2 &&
+      (int64_t)m * std::max(1, moe->K) + (int64_t)moe->n_shared * m < (1 << 30))
+    return moe_prefill(moe, x, m, x_dtype, logits, ids, wts, out, out_dtype, stream, props.sms);
   // Token chunks keep every launch under the problem-table bound.
   const int nt = m <= 8 ? 1 : 2;
   const int m_pad = 8 * nt;

@@ -34,28 +34,33 @@ constexpr int kPfN = 128;              // tokens per tile (UMMA N, TMEM columns)
 constexpr int kPfK = 64;               // k per stage (128 B of binary16 per operand row)
 constexpr int kPfImg = kPfN * kPfK * 2;  // 16 KB: one operand image (128 rows x 128 B)
 constexpr int kPfPackedPerMat = 2 * 2 * kTileBytes;  // 2 slabs x 2 k-tiles = 3584 B
-constexpr int kPfDeqWarps = 8;
+constexpr int kPfGroupWarps = 4;       // warps per dequant group (one group per in-flight stage)
 constexpr int kPfEpiWarps = 4;         // warps 0..3: TMEM lanes 32 w .. 32 w + 31
 constexpr int kPfProdWarp = 4;         // packed-weight producer
 constexpr int kPfMmaWarp = 5;
 constexpr int kPfBWarp = 6;            // activation / t image producer
 constexpr int kPfDeqWarp0 = 7;
-constexpr int kPfThreads = 32 * (kPfDeqWarp0 + kPfDeqWarps);  // 15 warps
+template <int NMAT>
+struct PfRoles {
+  static constexpr int kGroups = NMAT == 1 ? 4 : 3;  // stages de-quantized concurrently
+  static constexpr int kDeqWarps = kGroups * kPfGroupWarps;
+  static constexpr int kThreads = 32 * (kPfDeqWarp0 + kDeqWarps);
+};
 
 template <int NMAT>
 struct PfCfg {
-  static constexpr int kPS = NMAT == 1 ? 12 : 8;         // packed-weight ring (deep: HBM latency)
-  static constexpr int kAS = NMAT == 1 ? 4 : 3;          // dequantized A ring
-  static constexpr int kBS = NMAT == 1 ? 4 : 3;          // activation image ring (L2)
+  static constexpr int kPS = NMAT == 1 ? 12 : 8;         // packed-weight ring (HBM latency)
+  static constexpr int kAS = NMAT == 1 ? 6 : 3;          // dequantized A ring (>= dequant groups)
+  static constexpr int kBRegion = NMAT == 1 ? 64 * 1024 : 32 * 1024;  // activation images ring
+  static constexpr int kBSMax = 16;                      // B slots = region / (ntok_max x 128), <= 16
   static constexpr int kStageA = NMAT * kPfImg;
-  static constexpr int kStageB = kPfImg;
   static constexpr int kStageP = NMAT * kPfPackedPerMat;
   static constexpr int kOffA = 0;                        // 1024-aligned images first
   static constexpr int kOffB = kOffA + kAS * kStageA;
-  static constexpr int kOffP = kOffB + kBS * kStageB;
+  static constexpr int kOffP = kOffB + kBRegion;
   static constexpr int kOffBar = kOffP + kPS * kStageP;
-  // p_full[PS] p_empty[PS] a_full[AS] a_empty[AS] v_full[AS] b_full[BS] b_empty[BS] acc_full[2] acc_empty[2]
-  static constexpr int kNumBars = 2 * kPS + 3 * kAS + 2 * kBS + 4;
+  // p_full[PS] p_empty[PS] a_full[AS] a_empty[AS] v_full[AS] b_full[BSMax] b_empty[BSMax] acc_full[2] acc_empty[2]
+  static constexpr int kNumBars = 2 * kPS + 3 * kAS + 2 * kBSMax + 4;
   static constexpr int kOffTmem = kOffBar + kNumBars * 8;
   static constexpr int kOffStage = (kOffTmem + 16 + 127) & ~127;  // epilogue transpose [4 warps][32][33] f32
   static constexpr int kBytes = kOffStage + kPfEpiWarps * 32 * 33 * 4 + 1024;  // + alignment slack
@@ -70,6 +75,7 @@ struct PfProblem {
   const uint8_t* timg[2];   // t images  [tok_tiles][r64 chunks][hi, lo][16 KB]
   int32_t rchunks[2];       // 64-rank chunks of each compensator (0: none)
   int32_t k, n, rows;       // rows = tokens of this problem
+  int32_t ntok;             // token tile (UMMA N): multiple of 16, <= 128; images are ntok x 128 B
   int32_t mode;
   int32_t kind;             // 0: store rows (f32 / f16), 1: SwiGLU -> binary16 rows
   int32_t out_dtype;
@@ -79,6 +85,7 @@ struct PfProblem {
 };
 
 struct PfArgs {
+  int32_t ntok_max;           // largest token tile of the launch: B ring slot = ntok_max x 128 B
   long long* dbg;             // optional per-CTA role timeline (globaltimer ns), [cta][8]
   int32_t flags;              // debug: bit 0 skip dequant math, bit 1 skip MMAs
   const PfProblem* problems;
@@ -99,9 +106,9 @@ __device__ __forceinline__ uint64_t pf_desc_sw128(uint32_t saddr) {
   d |= (uint64_t)2u << 61;
   return d;
 }
-// Instruction descriptor: kind::f16, A/B binary16 K-major, D fp32, M = 128, N = kPfN.
-__device__ __forceinline__ uint32_t pf_idesc() {
-  return (1u << 4) | ((uint32_t)(kPfN >> 3) << 17) | ((uint32_t)(kPfM >> 4) << 24);
+// Instruction descriptor: kind::f16, A/B binary16 K-major, D fp32, M = 128, N = ntok.
+__device__ __forceinline__ uint32_t pf_idesc(int ntok) {
+  return (1u << 4) | ((uint32_t)(ntok >> 3) << 17) | ((uint32_t)(kPfM >> 4) << 24);
 }
 __device__ __forceinline__ void pf_mma(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
                                        uint32_t accum) {
@@ -155,7 +162,7 @@ __device__ __forceinline__ void pf_item(const PfArgs& a, int item, int& p, int& 
   }
   p = lo;
   const PfProblem P = a.problems[p];  // by value: fields live in registers
-  const int tts = (P.rows + kPfN - 1) / kPfN;
+  const int tts = (P.rows + P.ntok - 1) / P.ntok;
   const int rel = item - a.item_start[p];
   nt = rel / tts;
   tt = rel - nt * tts;
@@ -167,9 +174,12 @@ __device__ __forceinline__ void pf_item(const PfArgs& a, int item, int& p, int& 
 // Every role walks the same stage sequence: per item, k / 64 main stages then
 // 3 LoRC stages per 64-rank chunk per matrix.
 template <int NMAT>
-__global__ void __launch_bounds__(kPfThreads, 1) pf_gemm_kernel(const __grid_constant__ PfArgs a) {
+__global__ void __launch_bounds__(PfRoles<NMAT>::kThreads, 1) pf_gemm_kernel(const __grid_constant__ PfArgs a) {
+  constexpr int kPfDeqGroups = PfRoles<NMAT>::kGroups;
   using CF = PfCfg<NMAT>;
-  constexpr int PS = CF::kPS, AS = CF::kAS, BS = CF::kBS;
+  constexpr int PS = CF::kPS, AS = CF::kAS;
+  const int bslot = a.ntok_max * 128;
+  const int BS = min(CF::kBSMax, CF::kBRegion / bslot);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-B aligned base (SW128 atoms); pointer arithmetic keeps the shared address space
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -180,8 +190,8 @@ __global__ void __launch_bounds__(kPfThreads, 1) pf_gemm_kernel(const __grid_con
   uint64_t* a_empty = a_full + AS;
   uint64_t* v_full = a_empty + AS;
   uint64_t* b_full = v_full + AS;
-  uint64_t* b_empty = b_full + BS;
-  uint64_t* acc_full = b_empty + BS;  // [2]
+  uint64_t* b_empty = b_full + CF::kBSMax;
+  uint64_t* acc_full = b_empty + CF::kBSMax;  // [2]
   uint64_t* acc_empty = acc_full + 2;  // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + CF::kOffTmem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -189,10 +199,10 @@ __global__ void __launch_bounds__(kPfThreads, 1) pf_gemm_kernel(const __grid_con
   if (threadIdx.x == 0) {
     for (int s = 0; s < PS; ++s) {
       mbar_init(&p_full[s], 1);
-      mbar_init(&p_empty[s], kPfDeqWarps);
+      mbar_init(&p_empty[s], kPfGroupWarps);
     }
     for (int s = 0; s < AS; ++s) {
-      mbar_init(&a_full[s], kPfDeqWarps);
+      mbar_init(&a_full[s], kPfGroupWarps);
       mbar_init(&a_empty[s], 1);
       mbar_init(&v_full[s], 1);
     }
@@ -224,6 +234,13 @@ __global__ void __launch_bounds__(kPfThreads, 1) pf_gemm_kernel(const __grid_con
     }
   };
   if (threadIdx.x == 0) pf_dbg(0);
+  auto pf_trace = [&](int stage, int role) {  // CTA 0, first 64 stages: [stage][4 roles]
+    if (a.dbg != nullptr && blockIdx.x == 0 && stage < 64) {
+      long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      a.dbg[148 * 8 + stage * 4 + role] = t;
+    }
+  };
 
   auto item_stages = [&](const PfProblem& P) {
     return P.k / kPfK + 3 * (P.rchunks[0] + (NMAT == 2 ? P.rchunks[1] : 0));
@@ -258,9 +275,12 @@ __global__ void __launch_bounds__(kPfThreads, 1) pf_gemm_kernel(const __grid_con
           mbar_arrive_expect_tx(&p_full[ps], (uint32_t)CF::kStageP);
           for (int mat = 0; mat < NMAT; ++mat)
             for (int sl = 0; sl < 2; ++sl) {
-              const uint8_t* src = P.w[mat] + ((int64_t)(2 * nt + sl) * kts + 2 * st) * kTileBytes;
+              const int kst = (st + nt * 13) % ks;  // rotated k order per n-tile (spreads L2 hot spots)
+              const uint8_t* src = P.w[mat] + ((int64_t)(2 * nt + sl) * kts + 2 * kst) * kTileBytes;
               bulk_g2s(sP + (mat * 2 + sl) * 2 * kTileBytes, src, 2 * kTileBytes, &p_full[ps]);
             }
+          if (item == (int)blockIdx.x) pf_trace(st, 0);
+
           if (++ps == PS) {
             ps = 0;
             pph ^= 1;
@@ -281,17 +301,19 @@ __global__ void __launch_bounds__(kPfThreads, 1) pf_gemm_kernel(const __grid_con
         const int ks = P.k / kPfK, total = item_stages(P);
         for (int st = 0; st < total; ++st) {
           mbar_wait(&b_empty[bs], bph ^ 1);
-          uint8_t* sB = smem + CF::kOffB + bs * CF::kStageB;
+          uint8_t* sB = smem + CF::kOffB + bs * bslot;
           const uint8_t* src;
+          const uint32_t ib = (uint32_t)P.ntok * 128u;  // one token-tile image
           if (st < ks) {
-            src = P.act + ((int64_t)tt * ks + st) * kPfImg;
+            src = P.act + ((int64_t)tt * ks + (st + nt * 13) % ks) * ib;  // same rotation as the weights
           } else {
             int mat, ch, vpart, tpart;
             lorc_stage(P, st - ks, mat, ch, vpart, tpart);
-            src = P.timg[mat] + (((int64_t)tt * P.rchunks[mat] + ch) * 2 + tpart) * kPfImg;
+            src = P.timg[mat] + (((int64_t)tt * P.rchunks[mat] + ch) * 2 + tpart) * ib;
           }
-          mbar_arrive_expect_tx(&b_full[bs], (uint32_t)kPfImg);
-          bulk_g2s(sB, src, kPfImg, &b_full[bs]);
+          mbar_arrive_expect_tx(&b_full[bs], ib);
+          bulk_g2s(sB, src, ib, &b_full[bs]);
+          if (item == (int)blockIdx.x) pf_trace(st, 3);
           if (++bs == BS) {
             bs = 0;
             bph ^= 1;
@@ -302,9 +324,12 @@ __global__ void __launch_bounds__(kPfThreads, 1) pf_gemm_kernel(const __grid_con
     }
   } else if (warp >= kPfDeqWarp0) {
     // ======================= dequant warps =======================
+    // group grp handles the stages st = grp (mod kPfDeqGroups): two stages are
+    // de-quantized concurrently; within a stage, warp gw does jobs gw, gw + 4, ...
     const int dw = warp - kPfDeqWarp0;
+    const int grp = dw / kPfGroupWarps, gw = dw % kPfGroupWarps;
     const int g = lane >> 2, q = lane & 3;
-    int ps = 0, as = 0;
+    int ps = 0, as = 0, gs = 0;
     uint32_t pph = 0, aph = 0;
     for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
       int p, nt, tt;
@@ -312,59 +337,64 @@ __global__ void __launch_bounds__(kPfThreads, 1) pf_gemm_kernel(const __grid_con
       const PfProblem P = a.problems[p];  // by value: fields live in registers
       const int ks = P.k / kPfK, total = item_stages(P);
       const DqConsts dq = make_dq_consts(P.mode);
-      for (int st = 0; st < total; ++st) {
+      for (int st = 0; st < total; ++st, ++gs) {
+        const bool mine = (gs % kPfDeqGroups) == grp;
         uint8_t* sA = smem + CF::kOffA + as * CF::kStageA;
-        // warp 0 waits for the A slot, then either fetches a V image into it
-        // (LoRC stage) or just releases the other warps (v_full)
-        if (dw == 0 && lane == 0) {
-          mbar_wait(&a_empty[as], aph ^ 1);
-          if (st >= ks) {
-            int mat, ch, vpart, tpart;
-            lorc_stage(P, st - ks, mat, ch, vpart, tpart);
-            mbar_arrive_expect_tx(&v_full[as], (uint32_t)kPfImg);
-            bulk_g2s(sA + mat * kPfImg, P.vimg[mat] + (((int64_t)nt * P.rchunks[mat] + ch) * 2 + vpart) * kPfImg,
-                     kPfImg, &v_full[as]);
-          } else {
-            mbar_arrive(&v_full[as]);
-          }
-        }
-        mbar_wait(&v_full[as], aph);
-        if (st < ks) {
-          mbar_wait(&p_full[ps], pph);
-          if (dw == 0 && lane == 0 && st == 0) pf_dbg(7);
-          const uint8_t* sP = smem + CF::kOffP + ps * CF::kStageP;
-#pragma unroll
-          for (int job = 0; job < ((a.flags & 1) ? 0 : NMAT); ++job) {
-            const int jid = dw * NMAT + job;
-            const int j = jid & 1, t4 = jid >> 1;
-            const int kt = t4 & 1, sl = (t4 >> 1) & 1, mat = t4 >> 2;
-            const uint8_t* tile = sP + ((mat * 2 + sl) * 2 + kt) * kTileBytes;
-            const uint32_t* pa = reinterpret_cast<const uint32_t*>(tile + kPlaneAOff + lane * 16);
-            const uint32_t* pb = reinterpret_cast<const uint32_t*>(tile + kPlaneBOff + lane * 8);
-            const uint4 mm = *reinterpret_cast<const uint4*>(tile + kMetaOff + q * 32 + 16 * j);
-            const uint32_t S2[2] = {mm.x, mm.z}, O2[2] = {mm.y, mm.w};
-            uint32_t wv[16];
-            unit_dequant(pa[2 * j], pa[2 * j + 1], pb[j], S2, O2, dq, wv);
-            uint8_t* A = sA + mat * kPfImg;
-#pragma unroll
-            for (int pp = 0; pp < 16; ++pp) {
-              const int i = pp >> 2, r = pp & 3;
-              const int n = sl * 64 + 16 * i + g + 8 * (r & 1);
-              const int k = kt * 32 + 16 * j + 2 * q + 8 * (r >> 1);
-              const uint32_t off = (uint32_t)n * 128u + (uint32_t)(((k >> 3) ^ (n & 7)) << 4) + (uint32_t)((k & 7) * 2);
-              *reinterpret_cast<uint32_t*>(A + off) = wv[pp];
+        if (mine) {
+          // the group's first warp waits for the A slot, then either fetches a V
+          // image into it (LoRC stage) or just releases the group (v_full)
+          if (gw == 0 && lane == 0) {
+            mbar_wait(&a_empty[as], aph ^ 1);
+            if (st >= ks) {
+              int mat, ch, vpart, tpart;
+              lorc_stage(P, st - ks, mat, ch, vpart, tpart);
+              mbar_arrive_expect_tx(&v_full[as], (uint32_t)kPfImg);
+              bulk_g2s(sA + mat * kPfImg, P.vimg[mat] + (((int64_t)nt * P.rchunks[mat] + ch) * 2 + vpart) * kPfImg,
+                       kPfImg, &v_full[as]);
+            } else {
+              mbar_arrive(&v_full[as]);
             }
           }
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&p_empty[ps]);
-          if (++ps == PS) {
-            ps = 0;
-            pph ^= 1;
+          mbar_wait(&v_full[as], aph);
+          if (st < ks) {
+            mbar_wait(&p_full[ps], pph);
+            if (gw == 0 && lane == 0 && item == (int)blockIdx.x) pf_trace(st, 1);
+            const uint8_t* sP = smem + CF::kOffP + ps * CF::kStageP;
+            constexpr int kJobs = 8 * NMAT / kPfGroupWarps;
+#pragma unroll
+            for (int jb = 0; jb < ((a.flags & 1) ? 0 : kJobs); ++jb) {
+              const int jid = gw + kPfGroupWarps * jb;
+              const int j = jid & 1, t4 = jid >> 1;
+              const int kt = t4 & 1, sl = (t4 >> 1) & 1, mat = t4 >> 2;
+              const uint8_t* tile = sP + ((mat * 2 + sl) * 2 + kt) * kTileBytes;
+              const uint32_t* pa = reinterpret_cast<const uint32_t*>(tile + kPlaneAOff + lane * 16);
+              const uint32_t* pb = reinterpret_cast<const uint32_t*>(tile + kPlaneBOff + lane * 8);
+              const uint4 mm = *reinterpret_cast<const uint4*>(tile + kMetaOff + q * 32 + 16 * j);
+              const uint32_t S2[2] = {mm.x, mm.z}, O2[2] = {mm.y, mm.w};
+              uint32_t wv[16];
+              unit_dequant(pa[2 * j], pa[2 * j + 1], pb[j], S2, O2, dq, wv);
+              uint8_t* A = sA + mat * kPfImg;
+#pragma unroll
+              for (int pp = 0; pp < 16; ++pp) {
+                const int i = pp >> 2, r = pp & 3;
+                const int n = sl * 64 + 16 * i + g + 8 * (r & 1);
+                const int k = kt * 32 + 16 * j + 2 * q + 8 * (r >> 1);
+                const uint32_t off = (uint32_t)n * 128u + (uint32_t)(((k >> 3) ^ (n & 7)) << 4) + (uint32_t)((k & 7) * 2);
+                *reinterpret_cast<uint32_t*>(A + off) = wv[pp];
+              }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&p_empty[ps]);
+            if (!(a.flags & 16)) fence_proxy_async();  // generic smem writes -> tensor-core (async proxy) reads
           }
-          fence_proxy_async();  // generic smem writes -> tensor-core (async proxy) reads
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&a_full[as]);
+
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&a_full[as]);
+        if (st < ks && ++ps == PS) {
+          ps = 0;
+          pph ^= 1;
+        }
         if (++as == AS) {
           as = 0;
           aph ^= 1;
@@ -375,7 +405,6 @@ __global__ void __launch_bounds__(kPfThreads, 1) pf_gemm_kernel(const __grid_con
   } else if (warp == kPfMmaWarp) {
     // ======================= MMA issuer =======================
     if (lane == 0) {
-      const uint32_t idesc = pf_idesc();
       int as = 0, bs = 0;
       uint32_t aph = 0, bph = 0;
       int acc = 0;
@@ -385,15 +414,17 @@ __global__ void __launch_bounds__(kPfThreads, 1) pf_gemm_kernel(const __grid_con
         pf_item(a, item, p, nt, tt);
         const PfProblem P = a.problems[p];  // by value: fields live in registers
         const int ks = P.k / kPfK, total = item_stages(P);
+        const uint32_t idesc = pf_idesc(P.ntok);
         mbar_wait(&acc_empty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d0 = tmem + (uint32_t)(acc * NMAT * kPfN);
         for (int st = 0; st < total; ++st) {
           mbar_wait(&a_full[as], aph);
+
           mbar_wait(&b_full[bs], bph);
           tc_fence_after();
           const uint32_t aA = smem_u32(smem + CF::kOffA + as * CF::kStageA);
-          const uint32_t aB = smem_u32(smem + CF::kOffB + bs * CF::kStageB);
+          const uint32_t aB = smem_u32(smem + CF::kOffB + bs * bslot);
           int mat0 = 0, mat1 = NMAT;
           if (st >= ks) {
             int mat, ch, vpart, tpart;
@@ -411,6 +442,12 @@ __global__ void __launch_bounds__(kPfThreads, 1) pf_gemm_kernel(const __grid_con
           }
           pf_commit(&a_empty[as]);
           pf_commit(&b_empty[bs]);
+          if ((a.flags & 32) && item == (int)blockIdx.x && st < 64) {  // debug: commit latency
+            pf_trace(st, 1);
+            mbar_wait(&a_empty[as], aph);
+            pf_trace(st, 3);
+          }
+          if (item == (int)blockIdx.x) pf_trace(st, 2);
           if (++as == AS) {
             as = 0;
             aph ^= 1;
@@ -449,7 +486,8 @@ __global__ void __launch_bounds__(kPfThreads, 1) pf_gemm_kernel(const __grid_con
       float* stg = reinterpret_cast<float*>(smem + CF::kOffStage) + ew * 32 * 33;
       const int col0 = nt * kPfM + 32 * ew + 8 * (lane & 3);  // this lane's 8 output columns
 #pragma unroll 1
-      for (int c0 = 0; c0 < kPfN; c0 += 32) {
+      const int ntok = P.ntok;
+      for (int c0 = 0; c0 < ntok; c0 += 32) {
         uint32_t v0[32], v1[32];
         tmem_ld32(tbase + (uint32_t)c0, v0);
         if (NMAT == 2) tmem_ld32(tbase + (uint32_t)(kPfN + c0), v1);
@@ -464,8 +502,8 @@ __global__ void __launch_bounds__(kPfThreads, 1) pf_gemm_kernel(const __grid_con
 #pragma unroll
         for (int it = 0; it < 4; ++it) {
           const int tr = 8 * it + (lane >> 2);  // token row within the chunk
-          const int row = tt * kPfN + c0 + tr;
-          if (row < rows) {
+          const int row = tt * ntok + c0 + tr;
+          if (row < rows && c0 + tr < ntok) {
             const int64_t orow = rmap ? rmap[row] : row;
             const float* src = stg + tr * 33 + 8 * (lane & 3);
             float f[8];
@@ -506,16 +544,16 @@ __global__ void __launch_bounds__(kPfThreads, 1) pf_gemm_kernel(const __grid_con
 }
 
 // Activation images: rows (binary16 or f32 source, optional row gather) ->
-// [tok_tiles][k/64][128 rows x 128 B, SW128 K-major], zero rows past `rows`.
+// [tok_tiles][k/64][ntok rows x 128 B, SW128 K-major], zero rows past `rows`.
 __global__ void pf_image_kernel(const void* __restrict__ x, int32_t x_dtype, int64_t ldx,
-                                const int32_t* __restrict__ row_ids, int32_t rows, int32_t k,
+                                const int32_t* __restrict__ row_ids, int32_t rows, int32_t k, int32_t ntok,
                                 uint8_t* __restrict__ img) {
   const int ks = k / kPfK;
   const int tile = blockIdx.x / ks, st = blockIdx.x % ks;
-  uint8_t* dst = img + (int64_t)blockIdx.x * kPfImg;
-  for (int c = threadIdx.x; c < kPfN * 8; c += blockDim.x) {  // 16-B chunks
+  uint8_t* dst = img + (int64_t)blockIdx.x * ntok * 128;
+  for (int c = threadIdx.x; c < ntok * 8; c += blockDim.x) {  // 16-B chunks
     const int r = c >> 3, ch = c & 7;
-    const int row = tile * kPfN + r;
+    const int row = tile * ntok + r;
     uint4 v = make_uint4(0u, 0u, 0u, 0u);
     if (row < rows) {
       const int64_t src_row = row_ids ? row_ids[row] : row;
@@ -532,6 +570,124 @@ __global__ void pf_image_kernel(const void* __restrict__ x, int32_t x_dtype, int
     *reinterpret_cast<uint4*>(dst + r * 128 + ((ch ^ (r & 7)) << 4)) = v;
   }
   pdl_launch_dependents();
+}
+
+}  // namespace milo_dev
+
+namespace milo_dev {
+
+// ---------------------------------------------------------------------------
+// LoRC for the prefill path: t = half(X) U on the CUDA cores (fp32, like the
+// reference's Eigen product, gemm.cpp:185-188), split over k and reduced in a
+// fixed order, then written as binary16 hi / lo operand images for the GEMM's
+// extra K stages (t V on the tensor cores).
+// ---------------------------------------------------------------------------
+struct TProb {
+  const void* x;            // activation rows (f32 or f16)
+  int32_t x_dtype;
+  int64_t ldx;
+  const int32_t* row_ids;   // x row of problem row r (null: r)
+  int32_t rows, k, rank, gpr, rchunks, ks;  // ks = k splits
+  const uint8_t* ucodes;    // k x rank symm-int3 codes (or null -> ureal)
+  const float* uscales;     // k x gpr
+  const float* ureal;       // k x rank
+  float* part;              // [ks][rows][rchunks * 64] fp32 partials
+  uint8_t* timg;            // [tok_tiles][rchunks][hi, lo][ntok x 128 B]
+  int32_t ntok;
+  int32_t unit0;            // first work unit of this problem (prefix)
+};
+
+constexpr int kTRows = 32;  // rows per t-kernel CTA
+
+__global__ void __launch_bounds__(256) pf_t_kernel(const TProb* __restrict__ probs, int n_probs) {
+  __shared__ float sx[kTRows][65];
+  __shared__ float su[64][65];
+  int lo = 0, hi = n_probs - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (probs[mid].unit0 <= (int)blockIdx.x) lo = mid; else hi = mid - 1;
+  }
+  const TProb& P = probs[lo];
+  int u = blockIdx.x - P.unit0;
+  const int tiles = (P.rows + kTRows - 1) / kTRows;
+  const int ksi = u % P.ks;
+  u /= P.ks;
+  const int ch = u % P.rchunks, tile = u / P.rchunks;
+  if (tile >= tiles) return;
+  const int kper = ((P.k / 64 + P.ks - 1) / P.ks) * 64;
+  const int k0 = ksi * kper, k1 = min(P.k, k0 + kper);
+  const int tid = threadIdx.x, j = tid & 63, rg = tid >> 6;  // rank column, row group (8 rows)
+  float acc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
+  const int rcol = ch * 64 + j;
+  for (int kb = k0; kb < k1; kb += 64) {
+    // x tile [32 rows][64 k] -> binary16-rounded fp32
+    for (int e = tid; e < kTRows * 64; e += 256) {
+      const int r = e >> 6, kk = e & 63;
+      const int row = tile * kTRows + r;
+      float v = 0.0f;
+      if (row < P.rows) {
+        const int64_t xr = P.row_ids ? P.row_ids[row] : row;
+        v = P.x_dtype == 0 ? __half2float(__float2half_rn(static_cast<const float*>(P.x)[xr * P.ldx + kb + kk]))
+                           : __half2float(static_cast<const __half*>(P.x)[xr * P.ldx + kb + kk]);
+      }
+      sx[r][kk] = v;
+    }
+    // u tile [64 k][64 ranks] = step * (c - 4) (lowrank.cpp:122-134) or real U
+    for (int e = tid; e < 64 * 64; e += 256) {
+      const int kk = e >> 6, jj = e & 63;
+      const int kr = kb + kk, rc = ch * 64 + jj;
+      float v = 0.0f;
+      if (rc < P.rank) {
+        if (P.ucodes) {
+          const float st = P.uscales[(int64_t)kr * P.gpr + rc / 64] * (2.0f / 7.0f);
+          v = st * ((float)P.ucodes[(int64_t)kr * P.rank + rc] - 4.0f);
+        } else {
+          v = P.ureal[(int64_t)kr * P.rank + rc];
+        }
+      }
+      su[kk][jj] = v;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int kk = 0; kk < 64; ++kk) {
+      const float uv = su[kk][j];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] += sx[rg * 8 + i][kk] * uv;
+    }
+    __syncthreads();
+  }
+  const int r64 = P.rchunks * 64;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int row = tile * kTRows + rg * 8 + i;
+    if (row < P.rows) P.part[((int64_t)ksi * P.rows + row) * r64 + rcol] = acc[i];
+  }
+  (void)rcol;
+}
+
+// Sums the k-split partials in split order and writes the hi / lo images.
+__global__ void pf_t_images_kernel(const TProb* __restrict__ probs, int n_probs) {
+  const TProb& P = probs[blockIdx.y];
+  const int r64 = P.rchunks * 64;
+  const int ntok = P.ntok;
+  const int tiles = (P.rows + ntok - 1) / ntok;
+  const int64_t total = (int64_t)tiles * ntok * r64;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int row = (int)(e / r64), c = (int)(e % r64);
+    float t = 0.0f;
+    if (row < P.rows)
+      for (int s = 0; s < P.ks; ++s) t += P.part[((int64_t)s * P.rows + row) * r64 + c];
+    const __half h = __float2half_rn(t);
+    const __half l = __float2half_rn(t - __half2float(h));
+    const int tile = row / ntok, r = row % ntok, ch = c / 64, jj = c % 64;
+    const int ib = ntok * 128;
+    uint8_t* base = P.timg + ((int64_t)(tile * P.rchunks + ch) * 2) * ib;
+    const uint32_t off = (uint32_t)r * 128u + (uint32_t)(((jj >> 3) ^ (r & 7)) << 4) + (uint32_t)((jj & 7) * 2);
+    *reinterpret_cast<__half*>(base + off) = h;
+    *reinterpret_cast<__half*>(base + ib + off) = l;
+  }
 }
 
 }  // namespace milo_dev

@@ -195,3 +195,47 @@ def test_c1_shape_with_rank32(gpu, oracle, m):
     got = gpu.gemm_w3a16(torch.from_numpy(A).cuda(), gpu.Weight(P), gpu.Comp(comp),
                          _cfg(gpu, 1)).cpu().numpy()
     assert rel_err(got, want) <= TOL_F32
+
+
+# ---------------------------------------------------------------------------
+# tcgen05 prefill path (m >= 64 tokens): same contract as the decode path
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("k,n,m", [(128, 128, 64), (512, 1024, 200), (640, 256, 130), (1024, 384, 512)])
+@pytest.mark.parametrize("mode", [1, 0])
+def test_prefill_gemm_matches_oracle(gpu, oracle, k, n, m, mode):
+    import torch
+    P, _ = random_quantized(oracle, k, n, seed=k + n + m + mode, mode=mode)
+    A = np.random.default_rng(m).normal(0, 1, (m, k)).astype(np.float32)
+    want = oracle.gemm_w3a16(A, P, cfg=_oc(mode))
+    W = gpu.Weight(P)
+    got = gpu.gemm_w3a16(torch.from_numpy(A).cuda(), W, cfg=_cfg(gpu, mode)).cpu().numpy()
+    assert rel_err(got, want) <= TOL_F32
+    got16 = gpu.gemm_w3a16(torch.from_numpy(A).cuda().half(), W, cfg=_cfg(gpu, mode),
+                           out_dtype=torch.float16).float().cpu().numpy()
+    assert rel_err(got16, want) <= TOL_F16
+
+
+@pytest.mark.parametrize("storage", [1, 0])
+@pytest.mark.parametrize("rank", [4, 32, 70])
+def test_prefill_gemm_with_compensator(gpu, oracle, storage, rank):
+    import torch
+    k, n, m = 512, 256, 150
+    P, _ = random_quantized(oracle, k, n, seed=41)
+    comp = random_comp(oracle, k, n, rank, seed=rank + 1, storage=storage)
+    A = np.random.default_rng(42).normal(0, 1, (m, k)).astype(np.float32)
+    want = oracle.gemm_w3a16(A, P, comp, _oc(1))
+    got = gpu.gemm_w3a16(torch.from_numpy(A).cuda(), gpu.Weight(P), gpu.Comp(comp),
+                         cfg=_cfg(gpu, 1)).cpu().numpy()
+    assert rel_err(got, want) <= TOL_F32
+
+
+def test_prefill_identity_reproduces_weights(gpu, oracle):
+    # test_gemm.cpp:55-79 on the tensor-core path: A = I (128 rows) -> C == dequant exactly
+    import torch
+    k = n = 128
+    codes = np.random.default_rng(9).integers(0, 8, (k, n), dtype=np.uint8)
+    P = oracle.pack_matrix(codes, np.full(k * n // 64, 0.25, np.float32), np.full(k * n // 64, 4.0, np.float32))
+    C = gpu.gemm_w3a16(torch.eye(k, device="cuda"), gpu.Weight(P), cfg=_cfg(gpu, 1)).cpu().numpy()
+    want = np.array([oracle.half_to_float(int(h)) for h in oracle.dequant_half(P).ravel()],
+                    np.float32).reshape(k, n)
+    assert (C == want).all()

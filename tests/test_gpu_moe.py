@@ -37,7 +37,7 @@ def _experts(oracle, gpu, E, d, f, ranks, seed, mode=1):
     return o_ex, g_ex
 
 
-@pytest.mark.parametrize("m", [1, 3, 8, 16, 33, 100])
+@pytest.mark.parametrize("m", [1, 3, 8, 16, 33, 100, 300])
 def test_mixtral_like_layer(gpu, oracle, m):
     import torch
     E, K, d, f = 8, 2, 256, 512
@@ -60,7 +60,7 @@ def test_mixtral_like_layer(gpu, oracle, m):
     assert rel_err(out16.float().cpu().numpy(), want) <= 1e-3
 
 
-@pytest.mark.parametrize("m", [1, 7, 40])
+@pytest.mark.parametrize("m", [1, 7, 40, 150])
 def test_deepseek_like_layer_with_shared_experts(gpu, oracle, m):
     import torch
     E, K, d, f = 16, 6, 256, 128
