@@ -182,6 +182,7 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--ep", action="store_true", help="expert-parallel layer (default when N > 1)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -203,13 +204,26 @@ def main():
     peaks, peaks_src = load_peaks()
 
     routed_h, shared_h = build_host_layer(spec, seed=args.seed)
-    experts = [mb.Expert(*(mb.Weight(P) for P in h.w),
-                         *((mb.Comp(c) if c is not None else None) for c in h.c)) for h in routed_h]
-    shared = [mb.Expert(*(mb.Weight(P) for P in h.w),
-                        *((mb.Comp(c) if c is not None else None) for c in h.c)) for h in shared_h]
-    layer = mb.MoELayer(experts, shared, top_k=spec.top_k, score_mode=spec.score_mode)
-    # Replicas: with N > 1 every rank runs its own layer instance on its own
-    # token batch (weak scaling).  Expert-parallel sharding is DESIGN.md section 7.
+
+    def dev_expert(h):
+        return mb.Expert(*(mb.Weight(P) for P in h.w), *((mb.Comp(c) if c is not None else None) for c in h.c))
+
+    shared = [dev_expert(h) for h in shared_h]
+    use_ep = ws > 1 or args.ep
+    if use_ep and ws == 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", local))
+    if use_ep:
+        # expert parallel: rank r owns experts [r E / N, (r + 1) E / N),
+        # tokens move over NCCL all-to-all-v; m tokens per rank (weak scaling)
+        from paper_2504_02658_b200.ep import MiloEPLayer
+        per = (spec.experts + ws - 1) // ws
+        owned = [dev_expert(h) for h in routed_h[rank * per:(rank + 1) * per]]
+        layer = MiloEPLayer(owned, shared, spec.experts, spec.top_k, spec.score_mode)
+    else:
+        experts = [dev_expert(h) for h in routed_h]
+        layer = mb.MoELayer(experts, shared, top_k=spec.top_k, score_mode=spec.score_mode)
 
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
     flush_r = torch.ones(256 * 1024 * 1024 // 4, dtype=torch.int32, device="cuda")
@@ -362,7 +376,8 @@ def main():
                 "and router logits)",
         "config": {"workload": spec.name, "batch": m, "experts": spec.experts,
                    "top_k": spec.top_k, "d": spec.d, "f": spec.f, "shared_experts": spec.shared,
-                   "ranks": list(spec.routed_ranks), "parallelism": f"replicas x{ws}",
+                   "ranks": list(spec.routed_ranks), "parallelism": f"ep{ws}" if use_ep else "single GPU",
+                   "tokens_per_rank": m,
                    "l2": "flushed between steps (256 MiB write + 256 MiB read, outside the timed events)"},
         "achieved_GBps_layer": round(tot_bytes / (value_us * 1e-6) / 1e9, 1),
         "layer_bytes": int(tot_bytes), "layer_flops": int(tot_flops),
@@ -384,7 +399,7 @@ def main():
         "sweep": sweep,
     }
     print(json.dumps(line), flush=True)
-    if ws > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 

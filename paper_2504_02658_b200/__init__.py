@@ -135,6 +135,8 @@ def lib() -> C.CDLL:
         "milo_moe_forward": [vp, vp, i64, i32, vp, vp, i32, vp, vp, vp],
         "milo_moe_forward_routed": [vp, vp, i64, i32, vp, vp, vp, i32, vp],
         "milo_moe_forward_host": [vp, f32p, i64, f32p, f32p],
+        "milo_ep_dispatch": [vp, i64, i32, i32, i32, i32, vp, i32, i64, vp, vp, vp, vp],
+        "milo_ep_combine": [vp, vp, vp, i64, i32, i64, vp, vp],
     }
     for name, args in sig.items():
         if hasattr(L, name):
@@ -407,8 +409,9 @@ class MoELayer:
         if return_routing:
             ids = torch.empty((m, self.top_k), dtype=torch.int32, device=x.device)
             w = torch.empty((m, self.top_k), dtype=torch.float32, device=x.device)
+        lg = None if router_logits is None else router_logits.contiguous().float()
         _check(lib().milo_moe_forward(self._h, _dptr(x), m, x_dt,
-                                      _dptr(router_logits.contiguous().float()), _dptr(out),
+                                      _dptr(lg) if lg is not None else None, _dptr(out),
                                       F32 if out_dtype == torch.float32 else F16,
                                       _dptr(ids) if ids is not None else None,
                                       _dptr(w) if w is not None else None, _stream_ptr(stream)))
@@ -441,3 +444,31 @@ class MoELayer:
         if h is not None and _lib is not None:
             _lib.milo_moe_destroy(h)
             self._h = None
+
+
+# ---------------------------------------------------------------- expert-parallel helpers
+def ep_dispatch(ids, x, world: int, per: int, capacity: int, stream=None):
+    """Fixed-capacity EP dispatch on the device: returns (send_x f16 [world*C, d],
+    send_meta int32 [world*C], slot int32 [m*K])."""
+    import torch
+    m, K = ids.shape
+    d = x.shape[1]
+    send_x = torch.empty((world * capacity, d), dtype=torch.float16, device=x.device)
+    send_m = torch.empty((world * capacity,), dtype=torch.int32, device=x.device)
+    slot = torch.empty((m * K,), dtype=torch.int32, device=x.device)
+    ids = ids.contiguous().int()
+    x = x.contiguous()
+    _check(lib().milo_ep_dispatch(_dptr(ids), m, K, world, per, capacity, _dptr(x),
+                                  F32 if x.dtype == torch.float32 else F16, d, _dptr(send_x),
+                                  _dptr(send_m), _dptr(slot), _stream_ptr(stream)))
+    return send_x, send_m, slot
+
+
+def ep_combine(y, slot, wts, stream=None):
+    import torch
+    m, K = wts.shape
+    d = y.shape[1]
+    out = torch.empty((m, d), dtype=torch.float32, device=y.device)
+    _check(lib().milo_ep_combine(_dptr(y.contiguous()), _dptr(slot), _dptr(wts.contiguous().float()), m, K,
+                                 d, _dptr(out), _stream_ptr(stream)))
+    return out

@@ -1672,6 +1672,31 @@ extern "C" milo_status milo_moe_forward(milo_moe* moe, const void* x, int64_t m,
   return st;
 }
 
+// Expert-parallel exchange helpers (include/milo_b200.h).
+extern "C" milo_status milo_ep_dispatch(const int32_t* ids, int64_t m, int32_t K, int32_t world,
+                                        int32_t per, int32_t capacity, const void* x, int32_t x_dtype,
+                                        int64_t d, void* send_x, int32_t* send_meta, int32_t* slot,
+                                        void* stream) {
+  if (m < 0 || K < 1 || world < 1 || per < 1 || capacity < m * K || m * K > 1024 ||
+      (int64_t)world * capacity > 8192 || d % 8 != 0)
+    return fail(MILO_ERR_CONFIG, "ep_dispatch: unsupported sizes (m K <= 1024, world x capacity <= 8192)");
+  if (m == 0) return MILO_OK;
+  CUDA_TRY(launch(ep_dispatch_kernel, dim3(1), dim3(1024), 0, (cudaStream_t)stream, false, ids,
+                  (int32_t)(m * K), K, world, per, capacity, x, x_dtype, d, static_cast<__half*>(send_x),
+                  send_meta, slot));
+  return MILO_OK;
+}
+
+extern "C" milo_status milo_ep_combine(const float* y, const int32_t* slot, const float* wts, int64_t m,
+                                       int32_t K, int64_t d, float* out, void* stream) {
+  if (m <= 0) return m == 0 ? MILO_OK : fail(MILO_ERR_SHAPE, "negative token count");
+  if (d % 4 != 0) return fail(MILO_ERR_SHAPE, "d must be a multiple of 4");
+  const int64_t total = m * (d / 4);
+  CUDA_TRY(launch(ep_combine_kernel, dim3((unsigned)std::min<int64_t>((total + 255) / 256, 1184)), dim3(256), 0,
+                  (cudaStream_t)stream, false, y, slot, wts, m, K, d, out));
+  return MILO_OK;
+}
+
 extern "C" milo_status milo_moe_forward_host(milo_moe* moe, const float* x, int64_t m,
                                              const float* logits, float* out) {
   if (!moe) return fail(MILO_ERR_ARGUMENT, "null moe");

@@ -366,3 +366,87 @@ __global__ void moe_combine_kernel(const float* __restrict__ Y, const int32_t* _
 }
 
 }  // namespace milo_dev
+
+namespace milo_dev {
+
+// ---------------------------------------------------------------------------
+// Expert-parallel fixed-capacity exchange (paper_2504_02658_b200/ep.py):
+// entry e = t K + k with expert id >= 0 goes to rank id / per, at position
+// pos = #{entries e' < e with the same destination}; row slot dest * C + pos of
+// the send buffer carries binary16 x[t] and the local expert id (-1 = unused).
+// One CTA (entries <= 1024).  slot[e] = dest * C + pos (or -1) for the combine.
+// ---------------------------------------------------------------------------
+__global__ void ep_dispatch_kernel(const int32_t* __restrict__ ids, int32_t mK, int32_t K, int32_t W,
+                                   int32_t per, int32_t C, const void* __restrict__ x, int32_t x_dtype,
+                                   int64_t d, __half* __restrict__ send_x, int32_t* __restrict__ send_meta,
+                                   int32_t* __restrict__ slot) {
+  __shared__ int32_t s_slot[1024];
+  __shared__ int32_t s_src[1024 * 8];  // slot -> entry (W * C <= 8192)
+  const int tid = threadIdx.x;
+  for (int i = tid; i < W * C; i += blockDim.x) s_src[i] = -1;
+  __syncthreads();
+  for (int e = tid; e < mK; e += blockDim.x) {
+    const int id = ids[e];
+    int sl = -1;
+    if (id >= 0) {
+      const int dest = id / per;
+      int pos = 0;
+      for (int e2 = 0; e2 < e; ++e2) {
+        const int id2 = ids[e2];
+        pos += (id2 >= 0 && id2 / per == dest);
+      }
+      sl = dest * C + pos;
+      s_src[sl] = e;
+    }
+    s_slot[e] = sl;
+    slot[e] = sl;
+  }
+  __syncthreads();
+  for (int r = tid; r < W * C; r += blockDim.x) {
+    const int e = s_src[r];
+    send_meta[r] = e >= 0 ? ids[e] - (ids[e] / per) * per : -1;
+  }
+  const int64_t d8 = d / 8;
+  for (int64_t i = tid; i < (int64_t)W * C * d8; i += blockDim.x) {
+    const int r = (int)(i / d8), c = (int)(i % d8) * 8;
+    const int e = s_src[r];
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (e >= 0) {
+      const int64_t t = e / K;
+      if (x_dtype == 0) {
+        const float4* s = reinterpret_cast<const float4*>(static_cast<const float*>(x) + t * d + c);
+        const float4 p0 = s[0], p1 = s[1];
+        v = make_uint4(h2_as_u32(__floats2half2_rn(p0.x, p0.y)), h2_as_u32(__floats2half2_rn(p0.z, p0.w)),
+                       h2_as_u32(__floats2half2_rn(p1.x, p1.y)), h2_as_u32(__floats2half2_rn(p1.z, p1.w)));
+      } else {
+        v = *reinterpret_cast<const uint4*>(static_cast<const __half*>(x) + t * d + c);
+      }
+    }
+    *reinterpret_cast<uint4*>(send_x + (int64_t)r * d + c) = v;
+  }
+  (void)s_slot;
+}
+
+// out[t] = sum_k w[t,k] y[slot[t K + k]] (k order, moe_combine semantics), f32.
+__global__ void ep_combine_kernel(const float* __restrict__ y, const int32_t* __restrict__ slot,
+                                  const float* __restrict__ wts, int64_t m, int32_t K, int64_t d,
+                                  float* __restrict__ out) {
+  const int64_t total = m * (d / 4);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = i / (d / 4), c4 = i % (d / 4);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int k = 0; k < K; ++k) {
+      const int sl = slot[t * K + k];
+      if (sl < 0) continue;
+      const float w = wts[t * K + k];
+      const float4 v = reinterpret_cast<const float4*>(y + (int64_t)sl * d)[c4];
+      acc.x += w * v.x;
+      acc.y += w * v.y;
+      acc.z += w * v.z;
+      acc.w += w * v.w;
+    }
+    reinterpret_cast<float4*>(out)[i] = acc;
+  }
+}
+
+}  // namespace milo_dev

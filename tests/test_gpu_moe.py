@@ -103,3 +103,34 @@ def test_router_ties_prefer_lower_expert(gpu):
     ids, w = gpu.router_topk(logits, 2)
     assert ids.cpu().tolist() == [[1, 2], [0, 1]]
     assert torch.allclose(w, torch.full_like(w, 0.5))
+
+
+def test_expert_parallel_layer_world1_matches_layer(gpu, oracle):
+    """MiloEPLayer (NCCL all-to-all dispatch / combine) on a world of 1 equals
+    the single-GPU layer; the 2-rank exchange logic is tests/test_ep.py (gloo)."""
+    import os
+    import socket
+    import torch
+    import torch.distributed as dist
+    from paper_2504_02658_b200.ep import MiloEPLayer
+    E, K, d, f = 8, 2, 256, 512
+    ranks = [[(8 * ((e + j) % 4)) for j in range(3)] for e in range(E)]
+    o_ex, g_ex = _experts(oracle, gpu, E, d, f, ranks, seed=700)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK="0", WORLD_SIZE="1")
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        ep = MiloEPLayer(g_ex, [], E, K, 0)
+        ref = gpu.MoELayer(g_ex, [], top_k=K)
+        for m in (1, 9, 70):
+            rng = np.random.default_rng(m)
+            x = torch.from_numpy(rng.normal(0, 1, (m, d)).astype(np.float32)).cuda()
+            lg = torch.from_numpy(rng.normal(0, 1, (m, E)).astype(np.float32)).cuda()
+            a = ep.forward(x, lg)
+            b = ref.forward(x, lg)
+            assert rel_err(a.cpu().numpy(), b.cpu().numpy()) <= 1e-5
+    finally:
+        dist.destroy_process_group()
