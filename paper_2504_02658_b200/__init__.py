@@ -105,10 +105,12 @@ def lib() -> C.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIB_PATH):
+    path = os.environ.get("MILO_B200_LIB_VARIANT")  # tools/: an experimental build of the same library
+    path = os.path.join(os.path.dirname(LIB_PATH), "variants", f"libmilo_b200_{path}.so") if path else LIB_PATH
+    if not os.path.exists(path):
         raise CudaError(f"{LIB_PATH} missing: run paper_2504_02658_b200/build.py "
                         "(there is no CPU fallback)")
-    L = C.CDLL(LIB_PATH)
+    L = C.CDLL(path)
     i32, i64, u64 = C.c_int32, C.c_int64, C.c_uint64
     L.milo_last_error.restype = C.c_char_p
     L.milo_status_name.restype = C.c_char_p

@@ -34,24 +34,31 @@ def needs_rebuild() -> bool:
     return any(os.path.getmtime(s) > t for s in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_rebuild():
+def build(force: bool = False, verbose: bool = False, variant: str = "", defines=()) -> str:
+    """Builds lib/libmilo_b200.so, or lib/variants/libmilo_b200_<variant>.so with
+    extra -D defines (experiments; selected by MILO_B200_LIB_VARIANT)."""
+    out = os.path.join(LIB_DIR, "variants", f"libmilo_b200_{variant}.so") if variant else LIB
+    if not variant and not force and not needs_rebuild():
         return LIB
-    os.makedirs(LIB_DIR, exist_ok=True)
-    cmd = [NVCC, *ARCH, *FLAGS, "-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp",
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    cmd = [NVCC, *ARCH, *FLAGS, *(f"-D{d}" for d in defines), "-I", os.path.join(ROOT, "include"), "-o", out + ".tmp",
            os.path.join(CSRC, "milo_b200.cu"), "-lcuda"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = res.stdout + res.stderr
-    with open(os.path.join(LIB_DIR, "ptxas.log"), "w") as f:
+    with open(out + ".ptxas.log" if variant else os.path.join(LIB_DIR, "ptxas.log"), "w") as f:
         f.write(log)
     if res.returncode != 0:
         sys.stderr.write(log)
         raise RuntimeError("nvcc failed")
     if verbose:
         sys.stdout.write(log)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":
+    if "--variant" in sys.argv:  # --variant NAME DEF1 DEF2 ...
+        i = sys.argv.index("--variant")
+        print(build(variant=sys.argv[i + 1], defines=sys.argv[i + 2:]))
+        sys.exit(0)
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -49,10 +49,14 @@
 
 namespace milo_dev {
 
+#ifndef DEC_SLOTS
+#define DEC_SLOTS 2  // ring slots per warp (MoE decode)
+#endif
+
 constexpr int kDecMaxBlocks = 64;
 constexpr int kDecMaxTok = 16;                    // MoE decode path: m <= 16
 constexpr int kDecMaxProbs = 3 * kDecMaxBlocks;   // per phase
-constexpr int kDecKC = 4;                         // k-tiles (32 k each) per unit
+constexpr int kDecKC = 8;                         // max k-tiles (32 k each) per ring slot
 constexpr int kDecSlotW = 8192;                   // weight / pseudo-tile bytes per slot
 constexpr int kPseudoInt3Bytes = 640;             // 512 B codes + 32 f32 steps
 constexpr int kPseudoRealBytes = 2048;            // hi / lo binary16 fragments
@@ -79,9 +83,13 @@ struct DecExpert {
   DecMat m[3];  // w1, w3, w2 (single linear: m[0])
 };
 
+// Cross-warp values (stream-K partials, LoRC t) are tagged 64-bit words
+// {f32 bits, epoch}: a naturally aligned b64 store is single-copy atomic, so a
+// reader that sees the call's epoch in a word sees its value -- no fences, no
+// counters; writers never wait.
 struct DecWs {
-  float* part;          // [2 phases][G warps][2 segments][part_stride]
-  float* t;             // [blocks][3][m_pad][r16_max]
+  uint64_t* part;       // [2 phases][G warps][2 segments][part_stride] tagged
+  uint64_t* t;          // [blocks][3][m_pad][r16_max] tagged
   __half* h;            // [blocks][m_pad][f_max] row-major (phase-2 activations)
   float* Y;             // [m*K + S*m][d]
   __half* xrep;         // [grid][m][d] CTA-private binary16 copies of x (null: read x directly)
@@ -92,6 +100,7 @@ struct DecWs {
   int32_t* ccnt;        // [d/64]
   int32_t* tflag;       // [blocks][3]   (epoch-valued)
   int32_t* bflag;       // [blocks]
+  int32_t* hflag;       // [blocks][f_max / 64]  h slab ready (epoch-valued)
   int64_t part_stride;  // floats per (phase, warp, segment)
   int32_t r16_max;
   int32_t f_max;
@@ -121,15 +130,18 @@ struct DecArgs {
   int64_t ldo;
   DecWs ws;
   long long* dbg;              // optional per-warp timeline (globaltimer ns), [warp][16]
-  int32_t dbg_flags;           // bit 0: skip unit compute (memory-pipeline measurement)
+  int32_t dbg_flags;           // experiments: bit 4 no V prefetch, bit 5 no activation loads
 };
 
+// Work of a phase = the concatenated k-tiles of its problems' slabs; warp gw
+// of Gp owns tiles [gw T / Gp, (gw + 1) T / Gp) (balanced to one tile) and
+// streams them in ring slots of <= kc tiles that never cross a slab.
 struct DProb {
   const uint8_t* src[2];  // pseudo: U tiles; real: weight tiles of matrix 0 / 1
-  int32_t u0, s0;         // exclusive prefix of units / slabs within the phase
+  int32_t t0, s0;         // exclusive prefix of tiles / slabs within the phase
   int32_t n_slabs;        // 0 = empty entry (rank-0 compensator)
   int16_t kind, mat;      // kind 0 pseudo, 1 real; mat = matrix index 0..2
-  int16_t b, kts;         // block; units per slab (= ceil(ktiles / KC))
+  int16_t b, kc;          // block; max tiles per ring slot
   int16_t ktiles, tb;     // 32-k tiles per slab; bytes per tile (896 real, 640 / 2048 pseudo)
 };
 
@@ -143,10 +155,14 @@ struct DBlock {
 template <int NT, int NMAT1>
 struct DecCfg {
   static constexpr int kMPad = 8 * NT;
+#ifdef DEC_CONS12
+  static constexpr int kCons = NT == 1 ? 12 : 8;  // warps (each feeds its own ring)
+#else
   static constexpr int kCons = (NT == 1 && NMAT1 == 1) ? 12 : 8;  // warps (each feeds its own ring)
+#endif
   static constexpr int kWarps = kCons;
   static constexpr int kSlotBytes = kDecSlotW;
-  static constexpr int kSlots = kCons == 12 ? 2 : 3;
+  static constexpr int kSlots = kCons == 12 ? 2 : DEC_SLOTS;
   static constexpr int kRing = kCons * kSlots * kSlotBytes;
   static constexpr int kPartMax = 2 * 64 * kMPad;  // floats of the largest partial
   // smem carve-up
@@ -155,7 +171,8 @@ struct DecCfg {
   static constexpr int kOffBlocks = kOffProbs + 2 * kDecMaxProbs * (int)sizeof(DProb);
   static constexpr int kOffRoute = kOffBlocks + kDecMaxBlocks * (int)sizeof(DBlock);
   static constexpr int kRouteBytes = kDecMaxTok * 16 * 4 * 2 + 256 * 4 + 64;
-  static constexpr int kBytes = kOffRoute + kRouteBytes;
+  static constexpr int kOffMats = kOffRoute + kRouteBytes;  // DecExpert per block (smem copy)
+  static constexpr int kBytes = kOffMats + kDecMaxBlocks * (int)sizeof(DecExpert);
 };
 
 // ---------------------------------------------------------------- helpers
@@ -222,6 +239,28 @@ __device__ __forceinline__ void spin_until(const int* p, int v) {
   }
   (void)ld_acquire_gpu(p);
 }
+__device__ __forceinline__ void st_tagged2(uint64_t* p, float a, float b, int epoch) {
+  const uint64_t hi = (uint64_t)(uint32_t)epoch << 32;
+  asm volatile("st.global.cg.v2.b64 [%0], {%1, %2};" ::"l"(p), "l"(hi | __float_as_uint(a)),
+               "l"(hi | __float_as_uint(b))
+               : "memory");
+}
+__device__ __forceinline__ void st_tagged1(uint64_t* p, float a, int epoch) {
+  asm volatile("st.global.cg.b64 [%0], %1;" ::"l"(p), "l"(((uint64_t)(uint32_t)epoch << 32) | __float_as_uint(a))
+               : "memory");
+}
+// Loads two tagged words; true when both carry `epoch`.
+__device__ __forceinline__ bool ld_tagged2(const uint64_t* p, int epoch, float2& v) {
+  uint64_t a, b;
+  asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+  v = make_float2(__uint_as_float((uint32_t)a), __uint_as_float((uint32_t)b));
+  return (uint32_t)(a >> 32) == (uint32_t)epoch && (uint32_t)(b >> 32) == (uint32_t)epoch;
+}
+__device__ __forceinline__ void warp_backoff(long long t0) {
+  __nanosleep(64);
+  if (clock64() - t0 > 4000000000LL) __trap();
+}
+
 __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
@@ -234,6 +273,21 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 
+// Phase 2: wait until the h slabs covering k in [k0, k1) of block b are
+// published (lane j polls slab k0 / 64 + j; relaxed polls, the h loads that
+// follow go to L2 with ld.cg and are issued only after the flags were seen).
+__device__ __forceinline__ void wait_h(const int32_t* hflag, int k0, int k1, int epoch, int lane) {
+  const int j0 = k0 >> 6, nj = ((k1 - 1) >> 6) - j0 + 1;
+  bool ok = lane >= nj || ld_relaxed_gpu(hflag + j0 + lane) == epoch;
+  if (__all_sync(0xffffffffu, ok)) return;
+  const long long t0 = clock64();
+  while (!__all_sync(0xffffffffu, ok)) {
+    __nanosleep(64);
+    ok = ok || ld_relaxed_gpu(hflag + j0 + lane) == epoch;
+    if (clock64() - t0 > 4000000000LL) __trap();
+  }
+}
+
 // B fragments of one 32-k tile, loaded straight from the activation rows
 // (binary16, row-major, L1/L2 resident): v[j][nt] = {x[row][k + 16 j + 2q .. +1],
 // x[row][k + 16 j + 2q + 8 .. +9]}, row = 8 nt + g.  rowp[nt] == nullptr -> padding
@@ -242,7 +296,7 @@ template <int NT>
 struct BTile {
   uint32_t v[2][NT][2];
 };
-template <int NT>
+template <int NT, bool CG = false>
 __device__ __forceinline__ void load_btile(BTile<NT>& b, const __half* const (&rowp)[NT], int k, bool on, int q) {
 #pragma unroll
   for (int j = 0; j < 2; ++j)
@@ -251,8 +305,13 @@ __device__ __forceinline__ void load_btile(BTile<NT>& b, const __half* const (&r
       uint32_t b0 = 0u, b1 = 0u;
       if (on && rowp[nt] != nullptr) {
         const __half* p = rowp[nt] + k + 16 * j + 2 * q;
-        b0 = *reinterpret_cast<const uint32_t*>(p);
-        b1 = *reinterpret_cast<const uint32_t*>(p + 8);
+        if (CG) {  // written by other SMs during this call: read at L2
+          b0 = __ldcg(reinterpret_cast<const unsigned int*>(p));
+          b1 = __ldcg(reinterpret_cast<const unsigned int*>(p + 8));
+        } else {
+          b0 = *reinterpret_cast<const uint32_t*>(p);
+          b1 = *reinterpret_cast<const uint32_t*>(p + 8);
+        }
       }
       b.v[j][nt][0] = b0;
       b.v[j][nt][1] = b1;
@@ -330,13 +389,13 @@ __device__ __forceinline__ void tile_pseudo(const uint8_t* st, bool real, const 
 // D = c'(V) * split(t) on the tensor cores, then acc += step[n][g_r] * D.
 // All loads of a group are issued before its MMAs (one round trip per group).
 template <int NT>
-__device__ __forceinline__ void add_tv(float (&acc)[4][NT][4], const DecMat& M, const float* t,
-                                       int r16max, int slab, int lane) {
+__device__ __forceinline__ void add_tv(float (&acc)[4][NT][4], const DecMat& M, const uint64_t* t,
+                                       int r16max, int slab, int lane, int epoch, bool dry) {
   const int g = lane >> 2, q = lane & 3;
   const int nks = M.r16 >> 4;
   const int n0 = slab * 64;
   const uint8_t* vb = M.vft + (int64_t)slab * nks * (M.real ? kVftRealBytes : kVftInt3Bytes);
-  constexpr int kB = 4 / NT;  // rank steps whose loads are in flight together
+  constexpr int kB = 2;  // rank steps whose loads are in flight together
   for (int kb = 0; kb * kB < nks; ++kb) {
     const int gr = (kb * kB) >> 2;  // 64-rank group of this batch
     const int nk = min(kB, nks - kb * kB);
@@ -360,15 +419,27 @@ __device__ __forceinline__ void add_tv(float (&acc)[4][NT][4], const DecMat& M, 
       for (int kk = 0; kk < kB; ++kk) {
         if (kk >= nk) continue;
         const int ks = kb * kB + kk;
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          const float* tr = t + (8 * nt + g) * r16max + 16 * ks + 2 * q;
-          tv[kk][nt][0] = __ldcg(reinterpret_cast<const float2*>(tr));
-          tv[kk][nt][1] = __ldcg(reinterpret_cast<const float2*>(tr + 8));
-        }
         const uint4* src = reinterpret_cast<const uint4*>(vb + (int64_t)ks * kVftInt3Bytes + lane * 32);
         cv[kk][0] = __ldg(src);
         cv[kk][1] = __ldg(src + 1);
+      }
+      // t (published by the pseudo slabs' finishers): poll the tags
+      for (long long t0 = 0;;) {
+        bool ok = true;
+#pragma unroll
+        for (int kk = 0; kk < kB; ++kk) {
+          if (kk >= nk) continue;
+          const int ks = kb * kB + kk;
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            const uint64_t* tr = t + (8 * nt + g) * r16max + 16 * ks + 2 * q;
+            ok &= ld_tagged2(tr, epoch, tv[kk][nt][0]);
+            ok &= ld_tagged2(tr + 8, epoch, tv[kk][nt][1]);
+          }
+        }
+        if (__all_sync(0xffffffffu, ok || dry)) break;
+        if (t0 == 0) t0 = clock64();
+        warp_backoff(t0);
       }
 #pragma unroll
       for (int kk = 0; kk < kB; ++kk) {
@@ -396,13 +467,23 @@ __device__ __forceinline__ void add_tv(float (&acc)[4][NT][4], const DecMat& M, 
       for (int kk = 0; kk < nk; ++kk) {
         const int ks = kb * kB + kk;
         uint32_t bh[NT][2], bl[NT][2];
+        float2 v0[NT], v1[NT];
+        for (long long t0 = 0;;) {
+          bool ok = true;
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            const uint64_t* tr = t + (8 * nt + g) * r16max + 16 * ks + 2 * q;
+            ok &= ld_tagged2(tr, epoch, v0[nt]);
+            ok &= ld_tagged2(tr + 8, epoch, v1[nt]);
+          }
+          if (__all_sync(0xffffffffu, ok || dry)) break;
+          if (t0 == 0) t0 = clock64();
+          warp_backoff(t0);
+        }
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
-          const float* tr = t + (8 * nt + g) * r16max + 16 * ks + 2 * q;
-          const float2 v0 = __ldcg(reinterpret_cast<const float2*>(tr));
-          const float2 v1 = __ldcg(reinterpret_cast<const float2*>(tr + 8));
-          split_h2(v0.x, v0.y, bh[nt][0], bl[nt][0]);
-          split_h2(v1.x, v1.y, bh[nt][1], bl[nt][1]);
+          split_h2(v0[nt].x, v0[nt].y, bh[nt][0], bl[nt][0]);
+          split_h2(v1[nt].x, v1[nt].y, bh[nt][1], bl[nt][1]);
         }
         const uint4* src = reinterpret_cast<const uint4*>(vb + (int64_t)ks * kVftRealBytes + lane * 128);
 #pragma unroll
@@ -518,11 +599,9 @@ __device__ __noinline__ void dec_stage0(const DecArgs& a) {
   if (MOE) {
     const int K = a.K, E = a.E;
     for (int e = tid; e < 256; e += blockDim.x) emask[e] = 0u;
-    DEC_DBG(9);
     if (a.logits != nullptr) {
       for (int t = warp; t < m; t += blockDim.x >> 5)
         topk_regs(a.logits + (int64_t)t * E, E, K, a.score_mode, r_ids + t * K, r_wts + t * K, lane);
-      DEC_DBG(10);
     } else {
       for (int i = tid; i < m * K; i += blockDim.x) {
         r_ids[i] = a.ids_in[i];
@@ -530,7 +609,6 @@ __device__ __noinline__ void dec_stage0(const DecArgs& a) {
       }
     }
     __syncthreads();
-    DEC_DBG(8);
     if (blockIdx.x == 0 && a.logits != nullptr && a.ids_out != nullptr)
       for (int i = tid; i < m * K; i += blockDim.x) {
         a.ids_out[i] = r_ids[i];
@@ -594,9 +672,12 @@ __device__ __noinline__ void dec_stage0(const DecArgs& a) {
   }
   __syncthreads();
   const int nb = sc[0];
+  DecExpert* bx = reinterpret_cast<DecExpert*>(smem + CF::kOffMats);
+  for (int i = tid; i < nb * 3; i += blockDim.x) bx[i / 3].m[i % 3] = experts[blocks[i / 3].e].m[i % 3];
+  __syncthreads();
   // problem entries, one thread each: phase 1 [pseudo (b, mat)][real b], phase 2
   // [pseudo b][real b]; rank-0 pseudo entries stay as empty (n_slabs = 0) entries.
-  // kts = units per slab (KC k-tiles each, the last one possibly shorter).
+  // kc = tiles per ring slot: as many as fit kDecSlotW (both matrices of a w1|w3 slab).
   const int nm1 = MOE ? 2 : 1;
   const int np1 = nb * (nm1 + 1), np2 = MOE ? nb * 2 : 0;
   for (int i = tid; i < np1 + np2; i += blockDim.x) {
@@ -613,13 +694,12 @@ __device__ __noinline__ void dec_stage0(const DecArgs& a) {
       b = kind == 0 ? j : j - nb;
       mat = 2;
     }
-    const DecExpert& X = experts[blocks[b].e];
+    const DecExpert& X = bx[b];
     const DecMat& M = X.m[mat];
     P.kind = (int16_t)kind;
     P.mat = (int16_t)mat;
     P.b = (int16_t)b;
     P.ktiles = (int16_t)(M.k / kTileK);
-    P.kts = (int16_t)((P.ktiles + kDecKC - 1) / kDecKC);
     if (kind == 0) {
       P.n_slabs = M.rank > 0 ? M.r16 / 16 : 0;
       P.src[0] = M.upt;
@@ -631,6 +711,8 @@ __device__ __noinline__ void dec_stage0(const DecArgs& a) {
       P.src[1] = (MOE && ph == 0) ? X.m[1].w : nullptr;
       P.tb = (int16_t)kTileBytes;
     }
+    const int nmu = (kind == 1 && ph == 0 && MOE) ? NMAT1 : 1;
+    P.kc = (int16_t)min(kDecKC, kDecSlotW / (P.tb * nmu));
   }
   __syncthreads();
   if (warp < 2) {  // exclusive prefix of units / slabs per phase (warp ph)
@@ -641,7 +723,7 @@ __device__ __noinline__ void dec_stage0(const DecArgs& a) {
     for (int base = 0; base < n; base += 32) {
       const int i = base + lane;
       const int s = i < n ? PP[i].n_slabs : 0;
-      const int u = i < n ? s * PP[i].kts : 0;
+      const int u = i < n ? s * PP[i].ktiles : 0;
       int iu = u, is = s;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -653,7 +735,7 @@ __device__ __noinline__ void dec_stage0(const DecArgs& a) {
         }
       }
       if (i < n) {
-        PP[i].u0 = cu + iu - u;
+        PP[i].t0 = cu + iu - u;
         PP[i].s0 = cs + is - s;
       }
       cu += __shfl_sync(0xffffffffu, iu, 31);
@@ -674,7 +756,7 @@ __device__ __noinline__ void dec_stage0(const DecArgs& a) {
 // warp order and finishes the slab.
 template <int NT, int NMAT1, bool MOE, int NM>
 __device__ __noinline__ void dec_finish(const DecArgs& a, float* accs, int ph, int p, int s, int start,
-                                        int end, int Gp, int Tp, int gw, int G) {
+                                        int end, int Gp, int Tp, int gw, int G, bool dry) {
   using CF = DecCfg<NT, NMAT1>;
   constexpr int kMPad = CF::kMPad;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -700,118 +782,128 @@ __device__ __noinline__ void dec_finish(const DecArgs& a, float* accs, int ph, i
   const int d = a.d;
   const bool pseudo = P.kind == 0;
   const int nmat = pseudo ? 1 : NM;
+  const bool fdbg = !dry && ph == 0 && end <= P.t0 + (s + 1) * P.ktiles;  // the warp's last phase-1 segment
+#define FIN_DBG(i) \
+  if (fdbg) DEC_DBG(i)
+  FIN_DBG(8);
   const int ni = pseudo ? 1 : 4;
-  const int sb = P.u0 + s * P.kts, se = sb + P.kts;
-  float* part_base = W.part + (int64_t)ph * G * 2 * W.part_stride;
-  if (!(start <= sb && end >= se)) {  // not the sole contributor
-    const int w0 = (int)owner_of(sb, Tp, Gp), w1 = (int)owner_of(se - 1, Tp, Gp);
-    float* dst = part_base + ((int64_t)gw * 2 + (start > sb ? 0 : 1)) * W.part_stride;
-#pragma unroll
-    for (int mat = 0; mat < NM; ++mat)
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          if (mat >= nmat || i >= ni) continue;
-          float* d0 = dst + (mat * 64 + 16 * i + g) * kMPad + 8 * nt + 2 * q;
-          __stcg(reinterpret_cast<float2*>(d0), make_float2(acc[mat][i][nt][0], acc[mat][i][nt][1]));
-          __stcg(reinterpret_cast<float2*>(d0 + 8 * kMPad), make_float2(acc[mat][i][nt][2], acc[mat][i][nt][3]));
-        }
-    __syncwarp();
-    int last = 0;
-    if (lane == 0) {
-      int* cnt = (ph == 0 ? W.cnt1 : W.cnt2) + P.s0 + s;
-      last = atom_add_acqrel_gpu(cnt, 1) == (w1 - w0);
-      if (last) *cnt = 0;
+  const int sb = P.t0 + s * P.ktiles, se = sb + P.ktiles;
+  uint64_t* part_base = W.part + (int64_t)ph * G * 2 * W.part_stride;
+  if (dry || !(start <= sb && end >= se)) {  // not the sole contributor
+    // The slab's finisher is fixed: the highest contributor whose range ENDS in
+    // the slab (its piece is its last work of the phase, so it is the latest
+    // to arrive; the contributor after it only holds the slab's first piece of
+    // its own range).  The others publish tagged partials and move on.
+    int w0 = (int)owner_of(sb, Tp, Gp), w1 = (int)owner_of(se - 1, Tp, Gp);
+    const int w1end = (int)((int64_t)(w1 + 1) * Tp / Gp);
+    int fin = (w1end <= se || w1 == w0) ? w1 : w1 - 1;
+    if (dry) {  // code warm-up: the finisher path with one (pretend-ready) other contributor
+      w0 = gw - 1;
+      w1 = fin = gw;
     }
-    last = __shfl_sync(0xffffffffu, last, 0);
-    if (!last) return;
+    if (gw != fin) {
+      uint64_t* dst = part_base + ((int64_t)gw * 2 + (start > sb ? 0 : 1)) * W.part_stride;
 #pragma unroll
-    for (int mat = 0; mat < NM; ++mat)
+      for (int mat = 0; mat < NM; ++mat)
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            if (mat >= nmat || i >= ni) continue;
+            uint64_t* d0 = dst + (mat * 64 + 16 * i + g) * kMPad + 8 * nt + 2 * q;
+            st_tagged2(d0, acc[mat][i][nt][0], acc[mat][i][nt][1], epoch);
+            st_tagged2(d0 + 8 * kMPad, acc[mat][i][nt][2], acc[mat][i][nt][3], epoch);
+          }
+      FIN_DBG(9);
+      return;
+    }
+    FIN_DBG(9);
+    // sum all contributors in warp order (deterministic); this warp's own
+    // accumulators are re-read from the parked copy in shared memory
+#pragma unroll
+    for (int mat = 0; mat < NM; ++mat) {
+      if (mat >= nmat) continue;
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
           for (int e = 0; e < 4; ++e) acc[mat][i][nt][e] = 0.0f;
-    constexpr int kU = NM * NT <= 2 ? 2 : 1;  // contributors whose loads are in flight together
-    for (int w = w0; w <= w1; w += kU) {  // warp order: deterministic
-      float2 v[kU][NM][4][NT][2];
-#pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const int ww = min(w + u, w1);
-        const int rs = (int)((int64_t)ww * Tp / Gp);
-        const float* src = part_base + ((int64_t)ww * 2 + (rs > sb ? 0 : 1)) * W.part_stride;
-#pragma unroll
-        for (int mat = 0; mat < NM; ++mat)
+      for (int w = w0; w <= w1; ++w) {
+        if (w == gw) {
 #pragma unroll
           for (int i = 0; i < 4; ++i)
 #pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                if (i < ni) acc[mat][i][nt][e] += accs[(((mat * 4 + i) * NT + nt) * 4 + e) * 32 + lane];
+          continue;
+        }
+        const int rs = (int)((int64_t)w * Tp / Gp);
+        const uint64_t* src = part_base + ((int64_t)w * 2 + (rs > sb ? 0 : 1)) * W.part_stride;
+        constexpr int kI = NT == 1 ? 4 : 2;  // 16-column groups polled together (registers)
+#pragma unroll
+        for (int i0 = 0; i0 < 4; i0 += kI) {
+          if (i0 >= ni) continue;
+          float2 v[kI][NT][2];
+          for (long long t0 = 0;;) {
+            bool ok = true;
+#pragma unroll
+            for (int ii = 0; ii < kI; ++ii)
+#pragma unroll
+              for (int nt = 0; nt < NT; ++nt) {
+                if (i0 + ii >= ni) continue;
+                const uint64_t* s0 = src + (mat * 64 + 16 * (i0 + ii) + g) * kMPad + 8 * nt + 2 * q;
+                ok &= ld_tagged2(s0, epoch, v[ii][nt][0]);
+                ok &= ld_tagged2(s0 + 8 * kMPad, epoch, v[ii][nt][1]);
+              }
+            if (__all_sync(0xffffffffu, ok || dry)) break;
+            if (t0 == 0) t0 = clock64();
+            warp_backoff(t0);
+          }
+#pragma unroll
+          for (int ii = 0; ii < kI; ++ii)
+#pragma unroll
             for (int nt = 0; nt < NT; ++nt) {
-              if (mat >= nmat || i >= ni) continue;
-              const float* s0 = src + (mat * 64 + 16 * i + g) * kMPad + 8 * nt + 2 * q;
-              v[u][mat][i][nt][0] = __ldcg(reinterpret_cast<const float2*>(s0));
-              v[u][mat][i][nt][1] = __ldcg(reinterpret_cast<const float2*>(s0 + 8 * kMPad));
+              if (i0 + ii >= ni) continue;
+              acc[mat][i0 + ii][nt][0] += v[ii][nt][0].x;
+              acc[mat][i0 + ii][nt][1] += v[ii][nt][0].y;
+              acc[mat][i0 + ii][nt][2] += v[ii][nt][1].x;
+              acc[mat][i0 + ii][nt][3] += v[ii][nt][1].y;
             }
-      }
-#pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        if (w + u > w1) continue;
-#pragma unroll
-        for (int mat = 0; mat < NM; ++mat)
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt) {
-              if (mat >= nmat || i >= ni) continue;
-              acc[mat][i][nt][0] += v[u][mat][i][nt][0].x;
-              acc[mat][i][nt][1] += v[u][mat][i][nt][0].y;
-              acc[mat][i][nt][2] += v[u][mat][i][nt][1].x;
-              acc[mat][i][nt][3] += v[u][mat][i][nt][1].y;
-            }
+        }
       }
     }
   }
 
+  FIN_DBG(10);
   const DBlock& B = blocks[P.b];
-  const DecExpert& X = experts[B.e];
+  const DecExpert& X = reinterpret_cast<const DecExpert*>(smem + CF::kOffMats)[P.b];
   if (pseudo) {
     // t[b][mat][row][16 s + j]: D rows = rank j (g, g + 8), cols = token rows
-    const DecMat& M = X.m[P.mat];
-    float* tb = W.t + ((int64_t)P.b * 3 + P.mat) * kMPad * W.r16_max;
+    uint64_t* tb = W.t + ((int64_t)P.b * 3 + P.mat) * kMPad * W.r16_max;
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int j = 16 * s + g + 8 * (e >> 1), row = 8 * nt + 2 * q + (e & 1);
-        __stcg(tb + row * W.r16_max + j, acc[0][0][nt][e]);
+        if (!dry) st_tagged1(tb + row * W.r16_max + j, acc[0][0][nt][e], epoch);
       }
-    __syncwarp();
-    if (lane == 0) {
-      int* cnt = W.tcnt + P.b * 3 + P.mat;
-      if (atom_add_acqrel_gpu(cnt, 1) == M.r16 / 16 - 1) {
-        *cnt = 0;
-        st_release_gpu(W.tflag + P.b * 3 + P.mat, epoch);
-      }
-    }
     return;
   }
-  // real slab: + t V for each matrix with a compensator
+  // real slab: + t V for each matrix with a compensator (t polled by tag)
   const int nmr = NM;
-  if (lane == 0)
-    for (int mat = 0; mat < nmr; ++mat) {
-      const int mi = ph == 0 ? mat : 2;
-      if (X.m[mi].rank > 0) spin_until(W.tflag + P.b * 3 + mi, epoch);
-    }
-  __syncwarp();
+  FIN_DBG(11);
 #pragma unroll
   for (int mat = 0; mat < NM; ++mat) {
     if (mat >= nmr) continue;
     const int mi = ph == 0 ? mat : 2;
     const DecMat& M = X.m[mi];
     if (M.rank <= 0) continue;
-    add_tv<NT>(acc[mat], M, W.t + ((int64_t)P.b * 3 + mi) * kMPad * W.r16_max, W.r16_max, s, lane);
+    add_tv<NT>(acc[mat], M, W.t + ((int64_t)P.b * 3 + mi) * kMPad * W.r16_max, W.r16_max, s, lane, epoch, dry);
   }
+  FIN_DBG(12);
   const int n0 = s * kTileN;
   if (!MOE) {
 #pragma unroll
@@ -821,7 +913,7 @@ __device__ __noinline__ void dec_finish(const DecArgs& a, float* accs, int ph, i
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int row = 8 * nt + 2 * q + (e & 1);
-          if (row >= B.rows) continue;
+          if (row >= B.rows || dry) continue;
           const int64_t off = (int64_t)B.slot[row] * a.ldo + n0 + 16 * i + g + 8 * (e >> 1);
           if (a.out_dtype == 0)
             reinterpret_cast<float*>(a.out)[off] = acc[0][i][nt][e];
@@ -841,19 +933,16 @@ __device__ __noinline__ void dec_finish(const DecArgs& a, float* accs, int ph, i
           float h = silu_f(acc[0][i][nt][e]) * acc[NM - 1][i][nt][e];
           if (row >= B.rows) h = 0.0f;
           const float h_next = __shfl_down_sync(0xffffffffu, h, 4);  // column n + 1
-          if ((g & 1) == 0) {
+          if ((g & 1) == 0 && !dry) {
             const int n = n0 + 16 * i + g + 8 * (e >> 1);
             __stcg(reinterpret_cast<unsigned int*>(hb + (int64_t)row * W.f_max + n),
                    h2_as_u32(__floats2half2_rn(h, h_next)));
           }
         }
     __syncwarp();
-    if (lane == 0) {
-      if (atom_add_acqrel_gpu(W.bcnt + P.b, 1) == P.n_slabs - 1) {
-        W.bcnt[P.b] = 0;
-        st_release_gpu(W.bflag + P.b, epoch);
-      }
-    }
+    FIN_DBG(14);
+    if (lane == 0 && !dry) st_release_gpu(W.hflag + P.b * (W.f_max >> 6) + s, epoch);
+    FIN_DBG(13);
   } else {
     // y rows -> Y slots; the last block of this d-slab runs the combine
 #pragma unroll
@@ -863,15 +952,15 @@ __device__ __noinline__ void dec_finish(const DecArgs& a, float* accs, int ph, i
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int row = 8 * nt + 2 * q + (e & 1);
-          if (row >= B.rows) continue;
+          if (row >= B.rows || dry) continue;
           __stcg(W.Y + (int64_t)B.slot[row] * d + n0 + 16 * i + g + 8 * (e >> 1), acc[0][i][nt][e]);
         }
     __syncwarp();
     const int nb = sc[0];
     int last = 0;
     if (lane == 0) {
-      last = atom_add_acqrel_gpu(W.ccnt + s, 1) == nb - 1;
-      if (last) W.ccnt[s] = 0;
+      last = dry ? 1 : atom_add_acqrel_gpu(W.ccnt + s, 1) == nb - 1;
+      if (last && !dry) W.ccnt[s] = 0;
     }
     last = __shfl_sync(0xffffffffu, last, 0);
     if (last) {
@@ -891,6 +980,8 @@ __device__ __noinline__ void dec_finish(const DecArgs& a, float* accs, int ph, i
           o.x += 1.0f * y.x;
           o.y += 1.0f * y.y;
         }
+        if (dry)
+          continue;
         if (a.out_dtype == 0)
           *reinterpret_cast<float2*>(static_cast<float*>(a.out) + (int64_t)t * a.ldo + n) = o;
         else
@@ -901,9 +992,11 @@ __device__ __noinline__ void dec_finish(const DecArgs& a, float* accs, int ph, i
   }
 }
 
-// Per-warp producer (lane 0): walks the warp's units of both phases and issues
-// their weight copies (one bulk copy per matrix per unit) into the warp's ring.
-// Weights never depend on other warps, so the producer never waits.
+// Per-warp producer (lane 0): walks the warp's tiles of both phases and issues
+// their weight copies (one bulk copy per matrix per slot) into the warp's ring.
+// Weights never depend on other warps, so the producer never waits.  Slot
+// chunking: min(kc, tiles left in the slab, tiles left in the warp's range),
+// exactly as run_phase consumes them.
 template <int NT, int NMAT1, bool MOE>
 struct Prod {
   using CF = DecCfg<NT, NMAT1>;
@@ -911,33 +1004,34 @@ struct Prod {
   uint64_t* fb;
   const uint8_t* base0;
   const uint8_t* base1;
-  int ph, p, s, ku, left, kts, ktiles, tb, nm, nslabs, nphase;
+  int ph, p, s, t, left, kc, ktiles, tb, nm, nslabs, nphase;
+  uint64_t pol;  // L2 evict_first
 
-  __device__ __forceinline__ void load(const DProb* probs, int rel) {  // unit rel of problem p
+  __device__ __forceinline__ void load(const DProb* probs, int rel) {  // tile rel of problem p
     const DProb& P = probs[ph * kDecMaxProbs + p];
-    kts = P.kts;
+    kc = P.kc;
     ktiles = P.ktiles;
     tb = P.tb;
     nm = P.kind == 1 && ph == 0 ? NMAT1 : 1;
     nslabs = P.n_slabs;
     base0 = P.src[0];
     base1 = P.src[1];
-    s = rel / kts;
-    ku = rel - s * kts;
+    s = rel / ktiles;
+    t = rel - s * ktiles;
   }
   __device__ __forceinline__ void seek(const DProb* probs, int ph_, int T0, int T1, int G, int gw) {
     ph = ph_;
     left = 0;
     const int Tp = ph == 0 ? T0 : T1;
-    const int Gp = min(G, Tp);
+    const int Gp = min(ph == 0 ? G - 1 : G, Tp);  // phase 1: the grid's last warp is the code warmer
     if (gw >= Gp) return;
     const int st = (int)((int64_t)gw * Tp / Gp), en = (int)((int64_t)(gw + 1) * Tp / Gp);
     left = en - st;
     const DProb* P = probs + ph * kDecMaxProbs;
     int q = 0;
-    while (P[q].u0 + P[q].n_slabs * P[q].kts <= st) ++q;
+    while (P[q].t0 + P[q].n_slabs * P[q].ktiles <= st) ++q;
     p = q;
-    load(probs, st - P[q].u0);
+    load(probs, st - P[q].t0);
   }
   __device__ __forceinline__ bool norm(const DProb* probs, int T0, int T1, int G, int gw) {
     while (left == 0) {
@@ -948,16 +1042,21 @@ struct Prod {
   }
   __device__ __forceinline__ void issue(const DProb* probs, int sl) {
     uint8_t* dst = ring + sl * CF::kSlotBytes;
-    const int t0 = ku * kDecKC;
-    const int kc = min(kDecKC, ktiles - t0);
-    const uint32_t bytes = (uint32_t)(kc * tb);
+    const int c = min(min(kc, ktiles - t), left);
+    const uint32_t bytes = (uint32_t)(c * tb);
     mbar_arrive_expect_tx(&fb[sl], bytes * (uint32_t)nm);
-    const int64_t off = ((int64_t)s * ktiles + t0) * tb;
-    bulk_g2s(dst, base0 + off, bytes, &fb[sl]);
-    if (nm == 2) bulk_g2s(dst + bytes, base1 + off, bytes, &fb[sl]);
-    --left;
-    if (++ku == kts) {
-      ku = 0;
+    const int64_t off = ((int64_t)s * ktiles + t) * tb;
+    if (MOE) {  // streamed once: L2 keeps code, tables and prefetched tiles instead
+      bulk_g2s_hint(dst, base0 + off, bytes, &fb[sl], pol);
+      if (nm == 2) bulk_g2s_hint(dst + bytes, base1 + off, bytes, &fb[sl], pol);
+    } else {
+      bulk_g2s(dst, base0 + off, bytes, &fb[sl]);
+      if (nm == 2) bulk_g2s(dst + bytes, base1 + off, bytes, &fb[sl]);
+    }
+    left -= c;
+    t += c;
+    if (t == ktiles) {
+      t = 0;
       if (++s == nslabs && left > 0) {
         const DProb* P = probs + ph * kDecMaxProbs;
         do ++p; while (P[p].n_slabs == 0);
@@ -970,7 +1069,7 @@ struct Prod {
 struct PhaseState {
   int slot;
   uint32_t parity;
-  long long t_wait, t_fin, t_issue, n_units;
+  long long t_wait, t_fin, t_issue, n_units, t_comp;
 };
 
 // Activation rows of block B for the phase: phase 1 -> x rows (binary16,
@@ -1003,29 +1102,42 @@ __device__ __forceinline__ void run_phase(const DecArgs& a, Prod<NT, NMAT1, MOE>
   constexpr int kS = CF::kSlots;
   const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
   const DProb* PP = probs + PH * kDecMaxProbs;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const DecExpert* bxs = reinterpret_cast<const DecExpert*>(smem + CF::kOffMats);
   const int Tp = PH == 0 ? T0 : T1;
-  const int Gp = min(G, Tp);
+  const int Gp = min(PH == 0 ? G - 1 : G, Tp);
   if (gw >= Gp) return;
   const int start = (int)((int64_t)gw * Tp / Gp), end = (int)((int64_t)(gw + 1) * Tp / Gp);
   int p = 0;
   int pos = start;
   DEC_DBG(PH == 0 ? 2 : 5);
   while (pos < end) {
-    while (PP[p].u0 + PP[p].n_slabs * PP[p].kts <= pos) ++p;
+    while (PP[p].t0 + PP[p].n_slabs * PP[p].ktiles <= pos) ++p;
     const DProb& P = PP[p];
-    const int s = (pos - P.u0) / P.kts;
-    int ku = pos - P.u0 - s * P.kts;
-    const int seg_end = min(end, P.u0 + (s + 1) * P.kts);
+    const int s = (pos - P.t0) / P.ktiles;
+    const int tt = pos - P.t0 - s * P.ktiles;
+    const int seg_end = min(end, P.t0 + (s + 1) * P.ktiles);
+    const int pkc = P.kc;
     const bool pseudo = P.kind == 0;
-    const DecMat& M = experts[blocks[P.b].e].m[P.mat];
+    const DecMat& M = bxs[P.b].m[P.mat];
     const DqConsts dq = make_dq_consts(M.mode);
     const bool preal = pseudo && M.real;
     const int ptb = P.tb;
     const int ktiles = P.ktiles;
-    if (PH == 1) {  // the block's h rows must be published
-      if (lane == 0) spin_until(a.ws.bflag + P.b, a.epoch);
-      __syncwarp();
+    if (!pseudo && lane == 0 && seg_end == P.t0 + (s + 1) * ktiles && !(a.dbg_flags & 16)) {
+      // this segment ends the slab: its finisher's V fragments / steps -> L2 now
+      const DecExpert& X = bxs[P.b];
+#pragma unroll
+      for (int mat = 0; mat < NM; ++mat) {
+        const DecMat& Mv = X.m[PH == 0 ? mat : 2];
+        if (Mv.rank <= 0) continue;
+        const int nks = Mv.r16 >> 4;
+        const uint32_t vb = (uint32_t)nks * (Mv.real ? kVftRealBytes : kVftInt3Bytes);
+        prefetch_l2(Mv.vft + (int64_t)s * vb, vb);
+        if (!Mv.real) prefetch_l2(Mv.vstep + (int64_t)s * 64 * Mv.gpr, (uint32_t)(256 * Mv.gpr));
+      }
     }
+    const int32_t* hfl = a.ws.hflag + P.b * (a.ws.f_max >> 6);
     const __half* rowp[NT];
     block_rows<NT>(rowp, blocks[P.b], PH, P.b, xact, ldxa, a.ws, g);
 
@@ -1041,12 +1153,18 @@ __device__ __forceinline__ void run_phase(const DecArgs& a, Prod<NT, NMAT1, MOE>
 
     // k-tile pipeline over the segment: B fragments of tile t + 1 load while tile t computes
     const int kend = ktiles * 32;
-    int k = ku * kDecKC * 32;
+    int k = tt * 32;
     BTile<NT> bc;
-    load_btile<NT>(bc, rowp, k, true, q);
-    for (int left = seg_end - pos; left > 0; --left, ++ku) {
+    // phase 2: the h slabs of this slot and of the next tile (its B fragments
+    // are loaded one tile ahead)
+    if (PH == 1) wait_h(hfl, k, min(kend, k + (min(pkc, seg_end - pos) + 1) * 32), a.epoch, lane);
+    const bool bload = !(a.dbg_flags & 32);  // experiment: bit 5 = no activation loads (wrong results)
+    load_btile<NT, PH == 1>(bc, rowp, k, bload, q);
+    for (int left = seg_end - pos; left > 0;) {
       const int slot = ps.slot;
-      const int kc = min(kDecKC, ktiles - ku * kDecKC);
+      const int kc = min(pkc, left);
+      left -= kc;
+      if (PH == 1 && k != tt * 32) wait_h(hfl, k, min(kend, k + (kc + 1) * 32), a.epoch, lane);
       if (DEC_TIMERS) {
         const long long tw0 = clock64();
         mbar_wait(&fb[slot], ps.parity);
@@ -1056,18 +1174,20 @@ __device__ __forceinline__ void run_phase(const DecArgs& a, Prod<NT, NMAT1, MOE>
         mbar_wait(&fb[slot], ps.parity);
       }
       const uint8_t* st = ring + slot * CF::kSlotBytes;
+      const long long tc0 = DEC_TIMERS ? clock64() : 0;
 #pragma unroll 1
       for (int kk = 0; kk < kc; ++kk, k += 32) {
         BTile<NT> bn;
-        load_btile<NT>(bn, rowp, k + 32, k + 32 < kend, q);
+        load_btile<NT, PH == 1>(bn, rowp, k + 32, bload && k + 32 < kend, q);
         if (pseudo)
           tile_pseudo<NT, NM>(st + kk * ptb, preal, bc, acc, lane);
         else
           tile_real<NT, NM, NM>(st + kk * kTileBytes, kc * kTileBytes, bc, acc, dq, lane);
         bc = bn;
       }
+      if (DEC_TIMERS) ps.t_comp += clock64() - tc0;
       __syncwarp();
-      if (left == 1) break;  // the segment's last slot is the finisher's scratch (issued below)
+      if (left == 0) break;  // the segment's last slot is the finisher's scratch (issued below)
       if (DEC_TIMERS) {
         const long long ti0 = clock64();
         if (lane == 0 && pr.norm(probs, T0, T1, G, gw)) pr.issue(probs, slot);
@@ -1096,7 +1216,7 @@ __device__ __forceinline__ void run_phase(const DecArgs& a, Prod<NT, NMAT1, MOE>
       pos = seg_end;
       if (pos == end) DEC_DBG(3 + 3 * PH);
       const long long tf0 = DEC_TIMERS ? clock64() : 0;
-      dec_finish<NT, NMAT1, MOE, NM>(a, accs, PH, p, s, start, end, Gp, Tp, gw, G);
+      dec_finish<NT, NMAT1, MOE, NM>(a, accs, PH, p, s, start, end, Gp, Tp, gw, G, false);
       if (DEC_TIMERS) ps.t_fin += clock64() - tf0;
       __syncwarp();
       fence_proxy_async();  // generic smem use of the slot before the next bulk copy into it
@@ -1163,13 +1283,33 @@ __global__ void __launch_bounds__(32 * DecCfg<NT, NMAT1>::kWarps, 1)
   pr.ring = ring;
   pr.fb = fb;
   pr.nphase = MOE ? 2 : 1;
+  pr.pol = policy_evict_first();
   if (lane == 0) {
     pr.seek(probs, 0, T0, T1, G, gw);
     for (int sl = 0; sl < kS && pr.norm(probs, T0, T1, G, gw); ++sl) pr.issue(probs, sl);
   }
   __syncwarp();
 
-  PhaseState st{0, 0u, 0, 0, 0, 0};
+  PhaseState st{0, 0u, 0, 0, 0, 0, 0};
+  if (NT == 1 && gw == G - 1) {  // (NT = 2: the extra call sites cost the finisher registers)
+    // Code warm-up while the memory system is still idle: run the finisher
+    // paths once with every side effect off, so that the real finishers at the
+    // end of each phase (one per slab, all at about the same time) find this
+    // code in L2 instead of queueing behind the weight stream for it.
+    const DProb* P0 = probs;
+    int q0 = 0;
+    while (q0 < kDecMaxProbs - 1 && !(P0[q0].kind == 1 && P0[q0].n_slabs > 0)) ++q0;
+    float* scratch = reinterpret_cast<float*>(ring);
+    dec_finish<NT, NMAT1, MOE, NMAT1>(a, scratch, 0, q0, 0, 0, 1, 1, 1, gw, G, true);
+    if (MOE) {
+      const DProb* P1 = probs + kDecMaxProbs;
+      int q1 = 0;
+      while (q1 < kDecMaxProbs - 1 && !(P1[q1].kind == 1 && P1[q1].n_slabs > 0)) ++q1;
+      dec_finish<NT, NMAT1, MOE, 1>(a, scratch, 1, q1, 0, 0, 1, 1, 1, gw, G, true);
+    }
+    __syncwarp();
+    fence_proxy_async();
+  }
   run_phase<NT, NMAT1, MOE, NMAT1, 0>(a, pr, st, probs, blocks, experts, ring, fb, xact, ldxa, T0, T1, G, gw);
   DEC_DBG(4);
   if (MOE)
@@ -1177,7 +1317,7 @@ __global__ void __launch_bounds__(32 * DecCfg<NT, NMAT1>::kWarps, 1)
   DEC_DBG(7);
   if (DEC_TIMERS && a.dbg != nullptr && lane == 0) {
     long long* o = a.dbg + ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * 16;
-    o[11] = st.t_wait; o[12] = st.t_fin; o[13] = st.t_issue; o[14] = st.n_units;
+    o[11] = st.t_wait; o[12] = st.t_fin; o[13] = st.t_issue; o[14] = st.n_units; o[10] = st.t_comp;
   }
   pdl_launch_dependents();
 }

@@ -80,6 +80,16 @@ template <typename K>
 cudaError_t set_smem(K kernel, int bytes) {
   return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
+// Same, and the smallest shared-memory carveout that holds it: the rest of the
+// SM's 256 KB unified L1 / shared storage stays L1 (the decode kernel's
+// activation rows are read through L1).
+template <typename K>
+cudaError_t set_smem_min_carveout(K kernel, int bytes) {
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return e;
+  const int pct = (int)(((int64_t)bytes + 2048) * 100 / (228 * 1024)) + 1;
+  return cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, pct > 100 ? 100 : pct);
+}
 
 // Launch with programmatic dependent launch allowed (the kernel itself calls
 // griddepcontrol.wait before touching the previous grid's outputs).
@@ -713,8 +723,9 @@ constexpr int kCntCap = 1 << 17;   // slab counters per phase
 constexpr int kCCntCap = 4096;     // d-slab (combine) counters
 // control block (int32, zeroed once; counters return to zero after every call,
 // flags hold the epoch of the call that set them)
+constexpr int kHflagCap = 1 << 17;  // per (block, 64-column slab of h) ready flags
 constexpr size_t kCtrlInts = 2 * (size_t)kCntCap + kDecMaxBlocks * 3 + kDecMaxBlocks + kCCntCap +
-                             kDecMaxBlocks * 3 + kDecMaxBlocks;
+                             kDecMaxBlocks * 3 + kDecMaxBlocks + kHflagCap;
 
 struct DecodeWs {
   int32_t* ctrl = nullptr;
@@ -759,15 +770,15 @@ milo_status launch_decode(DecArgs a, const void* x, int32_t x_dtype, int64_t ldx
   int dev = 0;
   cudaGetDevice(&dev);
   if (configured_dev != dev) {
-    CUDA_TRY(set_smem(decode_kernel<NT, NMAT1, MOE>, CF::kBytes));
+    CUDA_TRY(set_smem_min_carveout(decode_kernel<NT, NMAT1, MOE>, CF::kBytes));
     configured_dev = dev;
   }
   const int G = sms * CF::kCons;
   const int m_pad = CF::kMPad;
   Arena ar;
   const int64_t part_stride = CF::kPartMax;
-  const size_t o_part = ar.take((size_t)2 * G * 2 * part_stride * 4);
-  const size_t o_t = ar.take((size_t)nb_max * 3 * m_pad * std::max(r16_max, 16) * 4);
+  const size_t o_part = ar.take((size_t)2 * G * 2 * part_stride * 8);  // tagged (value, epoch) words
+  const size_t o_t = ar.take((size_t)nb_max * 3 * m_pad * std::max(r16_max, 16) * 8);
   const size_t o_h = ar.take(MOE ? (size_t)nb_max * m_pad * f_max * 2 : 0);
   const size_t o_y = ar.take(MOE ? (size_t)y_rows * a.d * 4 : 0);
   const bool replicate = a.m <= 16;  // CTA-private x copies (decode.cuh)
@@ -780,8 +791,8 @@ milo_status launch_decode(DecArgs a, const void* x, int32_t x_dtype, int64_t ldx
   uint8_t* base = static_cast<uint8_t*>(w->data);
   int32_t* c = w->ctrl;
   DecWs& W = a.ws;
-  W.part = reinterpret_cast<float*>(base + o_part);
-  W.t = reinterpret_cast<float*>(base + o_t);
+  W.part = reinterpret_cast<uint64_t*>(base + o_part);
+  W.t = reinterpret_cast<uint64_t*>(base + o_t);
   W.h = reinterpret_cast<__half*>(base + o_h);
   W.Y = reinterpret_cast<float*>(base + o_y);
   W.cnt1 = c;
@@ -791,6 +802,8 @@ milo_status launch_decode(DecArgs a, const void* x, int32_t x_dtype, int64_t ldx
   W.ccnt = W.bcnt + kDecMaxBlocks;
   W.tflag = W.ccnt + kCCntCap;
   W.bflag = W.tflag + kDecMaxBlocks * 3;
+  W.hflag = W.bflag + kDecMaxBlocks;
+  if (MOE && (int64_t)nb_max * (f_max / 64) > kHflagCap) return fail(MILO_ERR_CONFIG, "decode: h flag capacity");
   W.part_stride = part_stride;
   W.r16_max = std::max(r16_max, 16);
   W.f_max = f_max;

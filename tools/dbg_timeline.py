@@ -31,13 +31,18 @@ L.milo_debug_timeline(None)
 d = dbg.cpu().numpy().reshape(-1, 16).astype(np.float64)
 t0 = d[:, 0][d[:, 0] > 0].min()
 names = ["start", "stage0 done", "p1 start", "p1 units end", "p1 done", "p2 start", "p2 units end", "end",
-         "s0 after sync1", "s0 enter", "s0 topk done(w)", "-", "-", "-", "-", "xrep done"]
-for i in [0, 15, 9, 10, 8, 1, 2, 3, 4, 5, 6, 7]:
+         "F enter", "F atomic", "F summed", "F tflag", "F tv done", "F h stored", "F h st issued", "xrep done"]
+for i in [0, 15, 1, 2, 3, 8, 9, 10, 11, 12, 14, 13, 4, 5, 6, 7]:
     nm = names[i]
     v = d[:, i][d[:, i] > 0] - t0
     if len(v): print(f"{nm:14s} n={len(v):5d} min={v.min()/1e3:7.2f} med={np.median(v)/1e3:7.2f} p90={np.percentile(v,90)/1e3:7.2f} max={v.max()/1e3:7.2f} us")
 
-for i, nm in [(11, "wait cyc"), (12, "finish cyc"), (13, "issue cyc"), (14, "units")]:
+v = d[:, 14]
+for a_, b_ in [(3, 8), (8, 9), (9, 10), (10, 11), (11, 12), (12, 14), (14, 13), (13, 4), (3, 4)]:
+    ok = (d[:, a_] > 0) & (d[:, b_] > 0)
+    v = d[ok, b_] - d[ok, a_]
+    if len(v): print(f"  {names[a_]:>12s} -> {names[b_]:<12s} n={len(v):5d} med={np.median(v)/1e3:6.2f} p90={np.percentile(v,90)/1e3:6.2f} max={v.max()/1e3:6.2f} us")
+for i, nm in ([(11, "wait cyc"), (12, "finish cyc"), (13, "issue cyc"), (14, "units"), (10, "compute cyc")] if os.environ.get("TIMERS") else []):
     v = d[:, i]
     print(f"{nm:12s} min={v.min():10.0f} med={np.median(v):10.0f} p90={np.percentile(v,90):10.0f} max={v.max():10.0f}  (us at 1.965GHz: med {np.median(v)/1965:.2f})")
 ue = d[:, 3] - t0; dn = d[:, 4] - t0
