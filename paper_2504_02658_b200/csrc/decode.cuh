@@ -319,7 +319,7 @@ __device__ __forceinline__ void load_btile(BTile<NT>& b, const __half* const (&r
 }
 
 // One k-tile of a real unit: NMAT macro tiles (matrix mat's tile at tile + mat * mstride).
-template <int NT, int NMAT, int NA>
+template <int NT, int NMAT, int NA, int A0 = 0>
 __device__ __forceinline__ void tile_real(const uint8_t* tile0, int mstride, const BTile<NT>& b,
                                           float (&acc)[NA][4][NT][4], const DqConsts& dq, int lane) {
   const int q = lane & 3;
@@ -339,7 +339,7 @@ __device__ __forceinline__ void tile_real(const uint8_t* tile0, int mstride, con
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) mma_16816(acc[mat][i][nt], &wv[4 * i], b.v[j][nt][0], b.v[j][nt][1]);
+        for (int nt = 0; nt < NT; ++nt) mma_16816(acc[A0 + mat][i][nt], &wv[4 * i], b.v[j][nt][0], b.v[j][nt][1]);
     }
   }
 }
@@ -1069,7 +1069,7 @@ struct Prod {
 struct PhaseState {
   int slot;
   uint32_t parity;
-  long long t_wait, t_fin, t_issue, n_units, t_comp;
+  long long t_wait, t_fin, t_issue, n_units, t_comp, t_h, t_comp1;
 };
 
 // Activation rows of block B for the phase: phase 1 -> x rows (binary16,
@@ -1141,9 +1141,10 @@ __device__ __forceinline__ void run_phase(const DecArgs& a, Prod<NT, NMAT1, MOE>
     const __half* rowp[NT];
     block_rows<NT>(rowp, blocks[P.b], PH, P.b, xact, ldxa, a.ws, g);
 
-    float acc[NM][4][NT][4];
+    constexpr int NA = NM;
+    float acc[NA][4][NT][4];
 #pragma unroll
-    for (int x = 0; x < NM; ++x)
+    for (int x = 0; x < NA; ++x)
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -1151,20 +1152,30 @@ __device__ __forceinline__ void run_phase(const DecArgs& a, Prod<NT, NMAT1, MOE>
 #pragma unroll
           for (int e = 0; e < 4; ++e) acc[x][i][nt][e] = 0.0f;
 
-    // k-tile pipeline over the segment: B fragments of tile t + 1 load while tile t computes
+    // k-tile pipeline over the segment: B fragments load kLA tiles ahead of the
+    // tile being computed (phase 2 reads h at L2 latency: two tiles ahead)
+    constexpr int kLA = PH == 1 ? 2 : 1;
     const int kend = ktiles * 32;
     int k = tt * 32;
-    BTile<NT> bc;
-    // phase 2: the h slabs of this slot and of the next tile (its B fragments
-    // are loaded one tile ahead)
-    if (PH == 1) wait_h(hfl, k, min(kend, k + (min(pkc, seg_end - pos) + 1) * 32), a.epoch, lane);
+    BTile<NT> bc, bn1;
+    // phase 2: the h slabs of this slot and of the look-ahead tiles
+    if (PH == 1) {
+      const long long th0 = DEC_TIMERS ? clock64() : 0;
+      wait_h(hfl, k, min(kend, k + (min(pkc, seg_end - pos) + kLA) * 32), a.epoch, lane);
+      if (DEC_TIMERS) ps.t_h += clock64() - th0;
+    }
     const bool bload = !(a.dbg_flags & 32);  // experiment: bit 5 = no activation loads (wrong results)
     load_btile<NT, PH == 1>(bc, rowp, k, bload, q);
+    if (kLA == 2) load_btile<NT, PH == 1>(bn1, rowp, k + 32, bload && k + 32 < kend, q);
     for (int left = seg_end - pos; left > 0;) {
       const int slot = ps.slot;
       const int kc = min(pkc, left);
       left -= kc;
-      if (PH == 1 && k != tt * 32) wait_h(hfl, k, min(kend, k + (kc + 1) * 32), a.epoch, lane);
+      if (PH == 1 && k != tt * 32) {
+        const long long th0 = DEC_TIMERS ? clock64() : 0;
+        wait_h(hfl, k, min(kend, k + (kc + kLA) * 32), a.epoch, lane);
+        if (DEC_TIMERS) ps.t_h += clock64() - th0;
+      }
       if (DEC_TIMERS) {
         const long long tw0 = clock64();
         mbar_wait(&fb[slot], ps.parity);
@@ -1178,12 +1189,17 @@ __device__ __forceinline__ void run_phase(const DecArgs& a, Prod<NT, NMAT1, MOE>
 #pragma unroll 1
       for (int kk = 0; kk < kc; ++kk, k += 32) {
         BTile<NT> bn;
-        load_btile<NT, PH == 1>(bn, rowp, k + 32, bload && k + 32 < kend, q);
+        load_btile<NT, PH == 1>(bn, rowp, k + 32 * kLA, bload && k + 32 * kLA < kend, q);
         if (pseudo)
-          tile_pseudo<NT, NM>(st + kk * ptb, preal, bc, acc, lane);
+          tile_pseudo<NT, NA>(st + kk * ptb, preal, bc, acc, lane);
         else
-          tile_real<NT, NM, NM>(st + kk * kTileBytes, kc * kTileBytes, bc, acc, dq, lane);
-        bc = bn;
+          tile_real<NT, NM, NA>(st + kk * kTileBytes, kc * kTileBytes, bc, acc, dq, lane);
+        if (kLA == 2) {
+          bc = bn1;
+          bn1 = bn;
+        } else {
+          bc = bn;
+        }
       }
       if (DEC_TIMERS) ps.t_comp += clock64() - tc0;
       __syncwarp();
@@ -1290,7 +1306,7 @@ __global__ void __launch_bounds__(32 * DecCfg<NT, NMAT1>::kWarps, 1)
   }
   __syncwarp();
 
-  PhaseState st{0, 0u, 0, 0, 0, 0, 0};
+  PhaseState st{0, 0u, 0, 0, 0, 0, 0, 0, 0};
   if (NT == 1 && gw == G - 1) {  // (NT = 2: the extra call sites cost the finisher registers)
     // Code warm-up while the memory system is still idle: run the finisher
     // paths once with every side effect off, so that the real finishers at the
@@ -1312,12 +1328,13 @@ __global__ void __launch_bounds__(32 * DecCfg<NT, NMAT1>::kWarps, 1)
   }
   run_phase<NT, NMAT1, MOE, NMAT1, 0>(a, pr, st, probs, blocks, experts, ring, fb, xact, ldxa, T0, T1, G, gw);
   DEC_DBG(4);
+  st.t_comp1 = st.t_comp;
   if (MOE)
     run_phase<NT, NMAT1, MOE, 1, 1>(a, pr, st, probs, blocks, experts, ring, fb, xact, ldxa, T0, T1, G, gw);
   DEC_DBG(7);
   if (DEC_TIMERS && a.dbg != nullptr && lane == 0) {
     long long* o = a.dbg + ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * 16;
-    o[11] = st.t_wait; o[12] = st.t_fin; o[13] = st.t_issue; o[14] = st.n_units; o[10] = st.t_comp;
+    o[11] = st.t_wait; o[12] = st.t_fin; o[13] = st.t_issue; o[14] = st.n_units; o[10] = st.t_comp; o[9] = st.t_h; o[8] = st.t_comp1;
   }
   pdl_launch_dependents();
 }

@@ -42,7 +42,9 @@ for a_, b_ in [(3, 8), (8, 9), (9, 10), (10, 11), (11, 12), (12, 14), (14, 13), 
     ok = (d[:, a_] > 0) & (d[:, b_] > 0)
     v = d[ok, b_] - d[ok, a_]
     if len(v): print(f"  {names[a_]:>12s} -> {names[b_]:<12s} n={len(v):5d} med={np.median(v)/1e3:6.2f} p90={np.percentile(v,90)/1e3:6.2f} max={v.max()/1e3:6.2f} us")
-for i, nm in ([(11, "wait cyc"), (12, "finish cyc"), (13, "issue cyc"), (14, "units"), (10, "compute cyc")] if os.environ.get("TIMERS") else []):
+d_all = d
+d = d[d[:, 0] > 0]
+for i, nm in ([(11, "wait cyc"), (12, "finish cyc"), (13, "issue cyc"), (14, "units"), (10, "compute cyc"), (8, "compute p1 cyc"), (9, "wait_h cyc")] if os.environ.get("TIMERS") else []):
     v = d[:, i]
     print(f"{nm:12s} min={v.min():10.0f} med={np.median(v):10.0f} p90={np.percentile(v,90):10.0f} max={v.max():10.0f}  (us at 1.965GHz: med {np.median(v)/1965:.2f})")
 ue = d[:, 3] - t0; dn = d[:, 4] - t0
