@@ -330,9 +330,19 @@ def gemm_w3a16(A, W: Weight, comp: Optional[Comp] = None, cfg: Optional[GemmConf
     a_dt = F32 if A.dtype == torch.float32 else F16 if A.dtype == torch.float16 else None
     if a_dt is None:
         raise ArgumentError("A must be float32 or float16")
-    out_dtype = out_dtype or torch.float32
-    c_dt = F32 if out_dtype == torch.float32 else F16
     m = A.shape[0]
+    if out is not None:
+        # the output buffer defines the output type
+        if out_dtype is not None and out_dtype != out.dtype:
+            raise ArgumentError("out_dtype does not match out.dtype")
+        out_dtype = out.dtype
+        if (out.dtype not in (torch.float32, torch.float16) or tuple(out.shape) != (m, W.cols)
+                or not out.is_contiguous() or out.device != A.device):
+            raise ArgumentError("out must be a contiguous (m, n) float32/float16 tensor on A's device")
+    out_dtype = out_dtype or torch.float32
+    if out_dtype not in (torch.float32, torch.float16):
+        raise ArgumentError("out_dtype must be float32 or float16")
+    c_dt = F32 if out_dtype == torch.float32 else F16
     if out is None:
         out = torch.empty((m, W.cols), dtype=out_dtype, device=A.device)
     c = cfg._c()

@@ -862,15 +862,139 @@ int prefill_min_rows() {
   return v;
 }
 
-template <int NMAT>
-milo_status launch_prefill(const PfProblem* host_probs, int n_probs, cudaStream_t stream, int sms,
-                           uint8_t* scratch) {
-  using CF = PfCfg<NMAT>;
+// Grouped activation images + LoRC t partials (pf_img_t_kernel), then the
+// t hi / lo images (pf_t_images_kernel): one launch each per GEMM phase.
+struct ImgTPlan {
+  bool fuse_t = false;  // t partials in the image kernel (slower than pf_t_kernel for long k: off)
+  std::vector<ImgJob> jobs;
+  std::vector<TProb> tps;  // for pf_t_images_kernel (rows, rchunks, ks = k / 64, part, timg, ntok)
+  int blocks = 0;
+  void add(const void* x, int32_t x_dtype, int64_t ldx, const int32_t* row_ids, int64_t rows, int64_t k,
+           int ntok, uint8_t* img, const milo_comp* const* comps, uint8_t* const* timg, float* const* part, int nc) {
+    ImgJob J{};
+    J.x = x;
+    J.x_dtype = x_dtype;
+    J.ldx = ldx;
+    J.row_ids = row_ids;
+    J.rows = (int32_t)rows;
+    J.k = (int32_t)k;
+    J.ntok = ntok;
+    J.img = img;
+    J.blk0 = blocks;
+    for (int i = 0; i < nc; ++i) {
+      const milo_comp* c = comps[i];
+      if (!c || c->rank == 0 || !fuse_t) continue;
+      ImgT& T = J.t[J.n_t++];
+      T.ucodes = c->ucodes;
+      T.uscales = c->uscales;
+      T.ureal = c->ureal;
+      T.rank = (int32_t)c->rank;
+      T.gpr = c->gpr;
+      T.rchunks = c->rch;
+      T.part = part[i];
+      TProb tp{};
+      tp.rows = (int32_t)rows;
+      tp.rchunks = c->rch;
+      tp.ks = (int32_t)(k / kPfK);
+      tp.part = part[i];
+      tp.timg = timg[i];
+      tp.ntok = ntok;
+      tps.push_back(tp);
+    }
+    jobs.push_back(J);
+    blocks += (int)(((rows + ntok - 1) / ntok) * (k / kPfK));
+  }
+  static size_t part_bytes(int64_t rows, int64_t k, const milo_comp* c, int sms) {
+    if (!c || c->rank == 0) return 0;
+    return (size_t)std::max<int64_t>(k / kPfK, t_splits(rows, k, c, sms)) * rows * c->rch * 64 * 4;
+  }
+  // k splits of pf_t_kernel: about one wave of CTAs over all `nprob` problems
+  static int t_splits(int64_t rows, int64_t k, const milo_comp* c, int sms, int nprob = 1) {
+    const int row_tiles = (int)((rows + kTRows - 1) / kTRows);
+    return std::max(1, std::min<int>((int)(k / 256), (2 * sms) / std::max(1, row_tiles * c->rch * nprob)));
+  }
+  // table: device memory for jobs + tps (>= table_bytes())
+  size_t table_bytes() const { return ((jobs.size() * sizeof(ImgJob) + 255) & ~size_t(255)) + tps.size() * sizeof(TProb) + 256; }
+  cudaError_t launch_all(uint8_t* table, cudaStream_t stream) const {
+    if (jobs.empty()) return cudaSuccess;
+    static thread_local int configured_dev = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (configured_dev != dev) {
+      cudaError_t e = cudaFuncSetAttribute(pf_img_t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kImgTSmem);
+      if (e != cudaSuccess) return e;
+      configured_dev = dev;
+    }
+    const size_t jb = (jobs.size() * sizeof(ImgJob) + 255) & ~size_t(255);
+    cudaError_t e = cudaMemcpyAsync(table, jobs.data(), jobs.size() * sizeof(ImgJob), cudaMemcpyHostToDevice, stream);
+    if (e != cudaSuccess) return e;
+    if (!tps.empty()) {
+      e = cudaMemcpyAsync(table + jb, tps.data(), tps.size() * sizeof(TProb), cudaMemcpyHostToDevice, stream);
+      if (e != cudaSuccess) return e;
+    }
+    e = launch(pf_img_t_kernel, dim3((unsigned)blocks), dim3(256), kImgTSmem, stream, false,
+               (const ImgJob*)table, (int)jobs.size());
+    if (e != cudaSuccess || tps.empty()) return e;
+    return launch(pf_t_images_kernel, dim3(256, (unsigned)tps.size()), dim3(256), 0, stream, false,
+                  (const TProb*)(table + jb), (int)tps.size());
+  }
+};
+
+// t = half(x) U for the prefill LoRC stages: pf_t_kernel (k split, fixed-order
+// reduction) + pf_t_images_kernel; `table` holds the TProb array (device).
+cudaError_t launch_t_batch(const std::vector<TProb>& v, int units, uint8_t* table, cudaStream_t stream) {
+  if (v.empty()) return cudaSuccess;
+  cudaError_t e = cudaMemcpyAsync(table, v.data(), v.size() * sizeof(TProb), cudaMemcpyHostToDevice, stream);
+  if (e != cudaSuccess) return e;
+  e = launch(pf_t_kernel, dim3(units), dim3(256), 0, stream, false, (const TProb*)table, (int)v.size());
+  if (e != cudaSuccess) return e;
+  return launch(pf_t_images_kernel, dim3(256, (unsigned)v.size()), dim3(256), 0, stream, false, (const TProb*)table,
+                (int)v.size());
+}
+TProb make_tprob(const void* x, int32_t x_dtype, int64_t ldx, const int32_t* row_ids, int64_t rows, int64_t k,
+                 int ntok, const milo_comp* c, uint8_t* timg, float* part, int sms, int unit0, int* units,
+                 int nprob = 1) {
+  TProb tp{};
+  tp.x = x;
+  tp.x_dtype = x_dtype;
+  tp.ldx = ldx;
+  tp.row_ids = row_ids;
+  tp.rows = (int32_t)rows;
+  tp.k = (int32_t)k;
+  tp.rank = (int32_t)c->rank;
+  tp.gpr = c->gpr;
+  tp.rchunks = c->rch;
+  tp.ks = ImgTPlan::t_splits(rows, k, c, sms, nprob);
+  tp.ucodes = c->ucodes;
+  tp.uscales = c->uscales;
+  tp.ureal = c->ureal;
+  tp.timg = timg;
+  tp.part = part;
+  tp.ntok = ntok;
+  tp.unit0 = unit0;
+  const int row_tiles = (int)((rows + kTRows - 1) / kTRows);
+  *units = row_tiles * tp.rchunks * tp.ks;
+  return tp;
+}
+cudaError_t launch_t(const void* x, int32_t x_dtype, int64_t ldx, const int32_t* row_ids, int64_t rows, int64_t k,
+                     int ntok, const milo_comp* c, uint8_t* timg, float* part, uint8_t* table, int sms,
+                     cudaStream_t stream) {
+  int units = 0;
+  std::vector<TProb> v{make_tprob(x, x_dtype, ldx, row_ids, rows, k, ntok, c, timg, part, sms, 0, &units)};
+  return launch_t_batch(v, units, table, stream);
+}
+
+// NG = 2 n-tiles per item (activation images shared by two MMAs) when every
+// problem's n is a multiple of 256 and the accumulators fit TMEM (one matrix).
+template <int NMAT, int NG>
+milo_status launch_prefill_ng(const PfProblem* host_probs, int n_probs, cudaStream_t stream, int sms,
+                              uint8_t* scratch) {
+  using CF = PfCfg<NMAT, NG>;
   static thread_local int configured_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
   if (configured_dev != dev) {
-    CUDA_TRY(set_smem(pf_gemm_kernel<NMAT>, CF::kBytes));
+    CUDA_TRY(set_smem(pf_gemm_kernel<NMAT, NG>, CF::kBytes));
     configured_dev = dev;
   }
   std::vector<int32_t> starts(n_probs + 1, 0);
@@ -878,7 +1002,7 @@ milo_status launch_prefill(const PfProblem* host_probs, int n_probs, cudaStream_
   for (int i = 0; i < n_probs; ++i) {
     const PfProblem& P = host_probs[i];
     ntok_max = std::max(ntok_max, (int)P.ntok);
-    starts[i + 1] = starts[i] + (P.n / kPfM) * ((P.rows + P.ntok - 1) / P.ntok);
+    starts[i + 1] = starts[i] + (P.n / (kPfM * NG)) * ((P.rows + P.ntok - 1) / P.ntok);
   }
   // problem table + starts travel in the scratch buffer (stream-ordered upload)
   const size_t pb = (size_t)n_probs * sizeof(PfProblem);
@@ -895,8 +1019,32 @@ milo_status launch_prefill(const PfProblem* host_probs, int n_probs, cudaStream_
   a.n_items = starts[n_probs];
   if (a.n_items == 0) return MILO_OK;
   const int grid = std::min(a.n_items, sms);
-  CUDA_TRY(launch(pf_gemm_kernel<NMAT>, dim3(grid), dim3(PfRoles<NMAT>::kThreads), CF::kBytes, stream, false, a));
+  CUDA_TRY(launch(pf_gemm_kernel<NMAT, NG>, dim3(grid), dim3(PfRoles<NMAT, NG>::kThreads), CF::kBytes, stream, false, a));
   return MILO_OK;
+}
+
+int prefill_ng() {
+  static const int v = [] {
+    const char* e = getenv("MILO_PF_NG");
+    return e ? atoi(e) : 2;
+  }();
+  return v;
+}
+
+template <int NMAT>
+milo_status launch_prefill(const PfProblem* host_probs, int n_probs, cudaStream_t stream, int sms,
+                           uint8_t* scratch) {
+  // NG = 2 when it still fills the grid (it halves the item count)
+  bool ng2 = NMAT == 1 && prefill_ng() == 2;
+  int64_t items2 = 0;
+  for (int i = 0; i < n_probs && ng2; ++i) {
+    const PfProblem& P = host_probs[i];
+    ng2 = P.n % (2 * kPfM) == 0;
+    items2 += (P.n / (2 * kPfM)) * ((P.rows + P.ntok - 1) / P.ntok);
+  }
+  ng2 = ng2 && items2 >= sms;
+  if (ng2) return launch_prefill_ng<1, 2>(host_probs, n_probs, stream, sms, scratch);
+  return launch_prefill_ng<NMAT, 1>(host_probs, n_probs, stream, sms, scratch);
 }
 
 }  // namespace
@@ -933,42 +1081,18 @@ extern "C" milo_status milo_gemm_w3a16(const milo_weight* w, const milo_comp* co
     void* mem = nullptr;
     const size_t img_b = (size_t)tiles * ks * ntok * 128;
     const bool lorc = comp && comp->rank > 0;
-    TProb tp{};
-    size_t t_img_b = 0, t_part_b = 0;
-    int t_units = 0;
-    if (lorc) {
-      tp.x = A;
-      tp.x_dtype = a_dtype;
-      tp.ldx = a_cols;
-      tp.rows = (int32_t)m;
-      tp.k = (int32_t)k;
-      tp.rank = (int32_t)comp->rank;
-      tp.gpr = comp->gpr;
-      tp.rchunks = comp->rch;
-      const int row_tiles = (int)((m + kTRows - 1) / kTRows);
-      tp.ks = std::max(1, std::min<int>((int)(k / 256), (2 * props.sms) / std::max(1, row_tiles * tp.rchunks)));
-      tp.ucodes = comp->ucodes;
-      tp.uscales = comp->uscales;
-      tp.ureal = comp->ureal;
-      t_units = row_tiles * tp.rchunks * tp.ks;
-      tp.ntok = ntok;
-      t_img_b = (size_t)tiles * tp.rchunks * 2 * ntok * 128;
-      t_part_b = (size_t)tp.ks * m * tp.rchunks * 64 * 4;
-    }
-    CUDA_TRY(cudaMallocAsync(&mem, img_b + t_img_b + t_part_b + 8192, stream));
+    const size_t t_img_b = lorc ? (size_t)tiles * comp->rch * 2 * ntok * 128 : 0;
+    const size_t t_part_b = ImgTPlan::part_bytes(m, k, lorc ? comp : nullptr, props.sms);
+    CUDA_TRY(cudaMallocAsync(&mem, img_b + t_img_b + t_part_b + 16384, stream));
     uint8_t* img = static_cast<uint8_t*>(mem);
-    if (lorc) {
-      tp.timg = img + img_b;
-      tp.part = reinterpret_cast<float*>(img + img_b + t_img_b);
-      TProb* dtp = reinterpret_cast<TProb*>(img + img_b + t_img_b + t_part_b + 4096);
-      CUDA_TRY(cudaMemcpyAsync(dtp, &tp, sizeof(TProb), cudaMemcpyHostToDevice, stream));
-      CUDA_TRY(launch(pf_t_kernel, dim3(t_units), dim3(256), 0, stream, false, (const TProb*)dtp, 1));
-      CUDA_TRY(launch(pf_t_images_kernel, dim3((unsigned)std::min<int64_t>(1024, (tiles * ntok * tp.rchunks * 64 + 255) / 256), 1),
-                      dim3(256), 0, stream, false, (const TProb*)dtp, 1));
-    }
-    cudaError_t e = launch(pf_image_kernel, dim3((unsigned)(tiles * ks)), dim3(256), 0, stream, false, A,
-                           a_dtype, (int64_t)a_cols, (const int32_t*)nullptr, (int32_t)m, (int32_t)k,
-                           (int32_t)ntok, img);
+    uint8_t* timg = img + img_b;
+    float* tpart = reinterpret_cast<float*>(img + img_b + t_img_b);
+    ImgTPlan plan;
+    const milo_comp* cs[1] = {comp};
+    plan.add(A, a_dtype, a_cols, nullptr, m, k, ntok, img, cs, &timg, &tpart, 1);
+    cudaError_t e = plan.launch_all(img + img_b + t_img_b + t_part_b + 8192, stream);
+    if (e == cudaSuccess && lorc) e = launch_t(A, a_dtype, a_cols, nullptr, m, k, ntok, comp, timg, tpart,
+                                               img + img_b + t_img_b + t_part_b + 12288, props.sms, stream);
     if (e != cudaSuccess) {
       cudaFreeAsync(mem, stream);
       return fail(MILO_ERR_CUDA, "launch failed: %s", cudaGetErrorString(e));
@@ -987,7 +1111,7 @@ extern "C" milo_status milo_gemm_w3a16(const milo_weight* w, const milo_comp* co
     P.out = C;
     if (lorc) {
       P.vimg[0] = comp->vimg;
-      P.timg[0] = tp.timg;
+      P.timg[0] = timg;
       P.rchunks[0] = comp->rch;
     }
     st = launch_prefill<1>(&P, 1, stream, props.sms, img + img_b + t_img_b + t_part_b);
@@ -1435,10 +1559,8 @@ milo_status moe_prefill(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype
       const int nt = pf_ntok(rows);
       const int64_t tiles = (rows + nt - 1) / nt;
       const int64_t kk = moe->hw[groups[gi].e][j]->rows;
-      const int row_tiles = (int)((rows + kTRows - 1) / kTRows);
-      const int ks = std::max(1, std::min<int>((int)(kk / 256), (2 * sms) / std::max(1, row_tiles * c->rch)));
       o_timg[j][gi] = ar.take((size_t)tiles * c->rch * 2 * nt * 128);
-      o_part[j][gi] = ar.take((size_t)ks * rows * c->rch * 64 * 4);
+      o_part[j][gi] = ar.take(ImgTPlan::part_bytes(rows, kk, c, sms));
     }
   const size_t o_tab = ar.take(262144);
   void* mem = nullptr;
@@ -1462,52 +1584,50 @@ milo_status moe_prefill(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype
     if (bytes && src) guard(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream));
     return dst;
   };
-  auto run_t = [&](int phase, const void* src, int32_t sdt, int64_t ldx, bool gather) {
-    std::vector<TProb> v;
+  const int n_tprob[2] = {1, 1};  // k splits sized per problem (several CTAs per SM stay resident)
+  // one grouped launch per phase: images (+ gathered rows) and the LoRC t partials
+  auto img_t_phase = [&](int phase) {
+    ImgTPlan plan;
+    for (size_t gi = 0; gi < groups.size(); ++gi) {
+      const int e = groups[gi].e;
+      const int nt = pf_ntok(groups[gi].rows);
+      const int mats[2] = {phase == 0 ? 0 : 2, phase == 0 ? 1 : 2};
+      const milo_comp* cs[2] = {moe->hc[e][mats[0]], phase == 0 ? moe->hc[e][mats[1]] : nullptr};
+      uint8_t* timg[2] = {base + o_timg[mats[0]][gi], base + o_timg[mats[1]][gi]};
+      float* part[2] = {reinterpret_cast<float*>(base + o_part[mats[0]][gi]),
+                        reinterpret_cast<float*>(base + o_part[mats[1]][gi])};
+      if (phase == 0)
+        plan.add(x, x_dtype, d, dtok + groups[gi].off, groups[gi].rows, d, nt, base + o_img1[gi], cs, timg, part, 2);
+      else
+        plan.add(hbuf + groups[gi].off * f_max, 1, f_max, nullptr, groups[gi].rows, moe->hw[e][2]->rows, nt,
+                 base + o_img2[gi], cs, timg, part, 1);
+    }
+    guard(plan.launch_all(upload(nullptr, plan.table_bytes()), stream));
+    std::vector<TProb> tv;
     int units = 0;
-    const int mats[2] = {phase == 0 ? 0 : 2, phase == 0 ? 1 : -1};
-    for (size_t gi = 0; gi < groups.size(); ++gi)
-      for (int mi : mats) {
+    for (size_t gi = 0; gi < groups.size(); ++gi) {
+      const int e = groups[gi].e;
+      const int nt = pf_ntok(groups[gi].rows);
+      for (int mi : {phase == 0 ? 0 : 2, phase == 0 ? 1 : -1}) {
         if (mi < 0) continue;
-        const milo_comp* c = moe->hc[groups[gi].e][mi];
+        const milo_comp* c = moe->hc[e][mi];
         if (!c || c->rank == 0) continue;
-        TProb tp{};
-        const int64_t rows = groups[gi].rows;
-        tp.x = gather ? src : static_cast<const uint8_t*>(src) + groups[gi].off * ldx * 2;
-        tp.x_dtype = sdt;
-        tp.ldx = ldx;
-        tp.row_ids = gather ? dtok + groups[gi].off : nullptr;
-        tp.rows = (int32_t)rows;
-        tp.k = (int32_t)moe->hw[groups[gi].e][mi]->rows;
-        tp.rank = (int32_t)c->rank;
-        tp.gpr = c->gpr;
-        tp.rchunks = c->rch;
-        const int row_tiles = (int)((rows + kTRows - 1) / kTRows);
-        tp.ks = std::max(1, std::min<int>(tp.k / 256, (2 * sms) / std::max(1, row_tiles * c->rch)));
-        tp.ucodes = c->ucodes;
-        tp.uscales = c->uscales;
-        tp.ureal = c->ureal;
-        tp.timg = base + o_timg[mi][gi];
-        tp.part = reinterpret_cast<float*>(base + o_part[mi][gi]);
-        tp.ntok = pf_ntok(rows);
-        tp.unit0 = units;
-        units += row_tiles * tp.rchunks * tp.ks;
-        v.push_back(tp);
+        int u = 0;
+        if (phase == 0)
+          tv.push_back(make_tprob(x, x_dtype, d, dtok + groups[gi].off, groups[gi].rows, d, nt, c,
+                                  base + o_timg[mi][gi], reinterpret_cast<float*>(base + o_part[mi][gi]), sms, units, &u,
+                                  n_tprob[phase]));
+        else
+          tv.push_back(make_tprob(hbuf + groups[gi].off * f_max, 1, f_max, nullptr, groups[gi].rows,
+                                  moe->hw[e][2]->rows, nt, c, base + o_timg[mi][gi],
+                                  reinterpret_cast<float*>(base + o_part[mi][gi]), sms, units, &u, n_tprob[phase]));
+        units += u;
       }
-    if (v.empty()) return;
-    const TProb* dv = reinterpret_cast<const TProb*>(upload(v.data(), v.size() * sizeof(TProb)));
-    guard(launch(pf_t_kernel, dim3(units), dim3(256), 0, stream, false, dv, (int)v.size()));
-    guard(launch(pf_t_images_kernel, dim3(256, (unsigned)v.size()), dim3(256), 0, stream, false, dv, (int)v.size()));
+    }
+    guard(launch_t_batch(tv, units, upload(nullptr, tv.size() * sizeof(TProb)), stream));
   };
-  // ---- phase 1: x rows -> images; t1, t3; w1|w3 + LoRC + SwiGLU -> h
-  for (size_t gi = 0; gi < groups.size() && st == MILO_OK; ++gi) {
-    const int nt = pf_ntok(groups[gi].rows);
-    const int64_t tiles = (groups[gi].rows + nt - 1) / nt;
-    guard(launch(pf_image_kernel, dim3((unsigned)(tiles * (d / kPfK))), dim3(256), 0, stream, false, x, x_dtype,
-                 (int64_t)d, (const int32_t*)(dtok + groups[gi].off), (int32_t)groups[gi].rows, (int32_t)d,
-                 (int32_t)nt, base + o_img1[gi]));
-  }
-  run_t(0, x, x_dtype, d, true);
+  // ---- phase 1: x rows -> images, t1, t3; w1|w3 + LoRC + SwiGLU -> h
+  img_t_phase(0);
   {
     std::vector<PfProblem> pv;
     for (size_t gi = 0; gi < groups.size(); ++gi) {
@@ -1540,17 +1660,8 @@ milo_status moe_prefill(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype
                              upload(nullptr, pv.size() * sizeof(PfProblem) + 4096));
   }
   (void)tiles_tot;
-  // ---- phase 2: h rows -> images; t2; w2 + LoRC -> Y slots
-  for (size_t gi = 0; gi < groups.size() && st == MILO_OK; ++gi) {
-    const int e = groups[gi].e;
-    const int64_t f = moe->hw[e][2]->rows;
-    const int nt = pf_ntok(groups[gi].rows);
-    const int64_t tiles = (groups[gi].rows + nt - 1) / nt;
-    guard(launch(pf_image_kernel, dim3((unsigned)(tiles * (f / kPfK))), dim3(256), 0, stream, false,
-                 (const void*)(hbuf + groups[gi].off * f_max), 1, f_max, (const int32_t*)nullptr,
-                 (int32_t)groups[gi].rows, (int32_t)f, (int32_t)nt, base + o_img2[gi]));
-  }
-  run_t(1, hbuf, 1, f_max, false);
+  // ---- phase 2: h rows -> images, t2; w2 + LoRC -> Y slots
+  if (st == MILO_OK) img_t_phase(1);
   if (st == MILO_OK) {
     std::vector<PfProblem> pv;
     for (size_t gi = 0; gi < groups.size(); ++gi) {

@@ -40,21 +40,28 @@ constexpr int kPfProdWarp = 4;         // packed-weight producer
 constexpr int kPfMmaWarp = 5;
 constexpr int kPfBWarp = 6;            // activation / t image producer
 constexpr int kPfDeqWarp0 = 7;
-template <int NMAT>
+// NG = n-tiles (128 output columns each) per work item: the item's activation
+// image of a stage feeds NG MMAs (NG accumulators), so activation traffic per
+// FLOP drops by NG -- the activation ring, not the tensor core, bounds the
+// NG = 1 kernel (one 16 KB image per 128 x 128 x 64 MMA, ~2 us copy latency).
+// Groups <= A-ring slots: a group that starts stage st has only seen stage
+// st - groups consumed, and its parity wait on the slot is unambiguous only
+// if the slot's barrier is at most one phase behind (st - 2 AS consumed).
+template <int NMAT, int NG = 1>
 struct PfRoles {
-  static constexpr int kGroups = NMAT == 1 ? 4 : 3;  // stages de-quantized concurrently
+  static constexpr int kGroups = NG == 2 ? 3 : (NMAT == 1 ? 4 : 3);  // stages de-quantized concurrently
   static constexpr int kDeqWarps = kGroups * kPfGroupWarps;
   static constexpr int kThreads = 32 * (kPfDeqWarp0 + kDeqWarps);
 };
 
-template <int NMAT>
+template <int NMAT, int NG = 1>
 struct PfCfg {
-  static constexpr int kPS = NMAT == 1 ? 12 : 8;         // packed-weight ring (HBM latency)
-  static constexpr int kAS = NMAT == 1 ? 6 : 3;          // dequantized A ring (>= dequant groups)
-  static constexpr int kBRegion = NMAT == 1 ? 64 * 1024 : 32 * 1024;  // activation images ring
+  static constexpr int kPS = NG == 2 ? 6 : (NMAT == 1 ? 12 : 8);     // packed-weight ring (HBM latency)
+  static constexpr int kAS = NG == 2 ? 3 : (NMAT == 1 ? 6 : 3);      // dequantized A ring
+  static constexpr int kBRegion = NG == 2 ? 64 * 1024 : (NMAT == 1 ? 64 * 1024 : 32 * 1024);
   static constexpr int kBSMax = 16;                      // B slots = region / (ntok_max x 128), <= 16
-  static constexpr int kStageA = NMAT * kPfImg;
-  static constexpr int kStageP = NMAT * kPfPackedPerMat;
+  static constexpr int kStageA = NG * NMAT * kPfImg;
+  static constexpr int kStageP = NG * NMAT * kPfPackedPerMat;
   static constexpr int kOffA = 0;                        // 1024-aligned images first
   static constexpr int kOffB = kOffA + kAS * kStageA;
   static constexpr int kOffP = kOffB + kBRegion;
@@ -64,7 +71,7 @@ struct PfCfg {
   static constexpr int kOffTmem = kOffBar + kNumBars * 8;
   static constexpr int kOffStage = (kOffTmem + 16 + 127) & ~127;  // epilogue transpose [4 warps][32][33] f32
   static constexpr int kBytes = kOffStage + kPfEpiWarps * 32 * 33 * 4 + 1024;  // + alignment slack
-  static constexpr int kTmemCols = 2 * NMAT * kPfN;      // double-buffered accumulators
+  static constexpr int kTmemCols = 2 * NG * NMAT * kPfN;  // double-buffered accumulators
 };
 
 // One GEMM problem: a weight matrix (or w1|w3 pair) times a block of token rows.
@@ -154,6 +161,7 @@ __device__ __forceinline__ void pf_wait(uint64_t* bar, uint32_t parity) {
 
 // Work item -> (problem, n-tile, token tile).  Items of a problem are n-tile
 // major so consecutive items share the activation images (L2 reuse).
+template <int NG>
 __device__ __forceinline__ void pf_item(const PfArgs& a, int item, int& p, int& nt, int& tt) {
   int lo = 0, hi = a.n_problems - 1;
   while (lo < hi) {
@@ -173,10 +181,11 @@ __device__ __forceinline__ void pf_item(const PfArgs& a, int item, int& p, int& 
 // roles: packed weights (deep, HBM latency), dequantized A, activation images.
 // Every role walks the same stage sequence: per item, k / 64 main stages then
 // 3 LoRC stages per 64-rank chunk per matrix.
-template <int NMAT>
-__global__ void __launch_bounds__(PfRoles<NMAT>::kThreads, 1) pf_gemm_kernel(const __grid_constant__ PfArgs a) {
-  constexpr int kPfDeqGroups = PfRoles<NMAT>::kGroups;
-  using CF = PfCfg<NMAT>;
+template <int NMAT, int NG>
+__global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel(const __grid_constant__ PfArgs a) {
+  constexpr int kPfDeqGroups = PfRoles<NMAT, NG>::kGroups;
+  static_assert(kPfDeqGroups <= PfCfg<NMAT, NG>::kAS, "dequant groups must not outnumber A slots");
+  using CF = PfCfg<NMAT, NG>;
   constexpr int PS = CF::kPS, AS = CF::kAS;
   const int bslot = a.ntok_max * 128;
   const int BS = min(CF::kBSMax, CF::kBRegion / bslot);
@@ -265,7 +274,7 @@ __global__ void __launch_bounds__(PfRoles<NMAT>::kThreads, 1) pf_gemm_kernel(con
       uint32_t pph = 0;
       for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
         int p, nt, tt;
-        pf_item(a, item, p, nt, tt);
+        pf_item<NG>(a, item, p, nt, tt);
         const PfProblem P = a.problems[p];  // by value: fields live in registers
         const int ks = P.k / kPfK, kts = P.k / kTileK;
         for (int st = 0; st < ks; ++st) {
@@ -273,12 +282,13 @@ __global__ void __launch_bounds__(PfRoles<NMAT>::kThreads, 1) pf_gemm_kernel(con
 
           uint8_t* sP = smem + CF::kOffP + ps * CF::kStageP;
           mbar_arrive_expect_tx(&p_full[ps], (uint32_t)CF::kStageP);
-          for (int mat = 0; mat < NMAT; ++mat)
-            for (int sl = 0; sl < 2; ++sl) {
-              const int kst = (st + nt * 13) % ks;  // rotated k order per n-tile (spreads L2 hot spots)
-              const uint8_t* src = P.w[mat] + ((int64_t)(2 * nt + sl) * kts + 2 * kst) * kTileBytes;
-              bulk_g2s(sP + (mat * 2 + sl) * 2 * kTileBytes, src, 2 * kTileBytes, &p_full[ps]);
-            }
+          const int kst = (st + nt * 13) % ks;  // rotated k order per n-tile (spreads L2 hot spots)
+          for (int ng = 0; ng < NG; ++ng)
+            for (int mat = 0; mat < NMAT; ++mat)
+              for (int sl = 0; sl < 2; ++sl) {
+                const uint8_t* src = P.w[mat] + ((int64_t)(2 * (NG * nt + ng) + sl) * kts + 2 * kst) * kTileBytes;
+                bulk_g2s(sP + ((ng * NMAT + mat) * 2 + sl) * 2 * kTileBytes, src, 2 * kTileBytes, &p_full[ps]);
+              }
           if (item == (int)blockIdx.x) pf_trace(st, 0);
 
           if (++ps == PS) {
@@ -296,7 +306,7 @@ __global__ void __launch_bounds__(PfRoles<NMAT>::kThreads, 1) pf_gemm_kernel(con
       uint32_t bph = 0;
       for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
         int p, nt, tt;
-        pf_item(a, item, p, nt, tt);
+        pf_item<NG>(a, item, p, nt, tt);
         const PfProblem P = a.problems[p];  // by value: fields live in registers
         const int ks = P.k / kPfK, total = item_stages(P);
         for (int st = 0; st < total; ++st) {
@@ -333,7 +343,7 @@ __global__ void __launch_bounds__(PfRoles<NMAT>::kThreads, 1) pf_gemm_kernel(con
     uint32_t pph = 0, aph = 0;
     for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
       int p, nt, tt;
-      pf_item(a, item, p, nt, tt);
+      pf_item<NG>(a, item, p, nt, tt);
       const PfProblem P = a.problems[p];  // by value: fields live in registers
       const int ks = P.k / kPfK, total = item_stages(P);
       const DqConsts dq = make_dq_consts(P.mode);
@@ -341,16 +351,20 @@ __global__ void __launch_bounds__(PfRoles<NMAT>::kThreads, 1) pf_gemm_kernel(con
         const bool mine = (gs % kPfDeqGroups) == grp;
         uint8_t* sA = smem + CF::kOffA + as * CF::kStageA;
         if (mine) {
-          // the group's first warp waits for the A slot, then either fetches a V
-          // image into it (LoRC stage) or just releases the group (v_full)
+          // every warp of the group waits for the A slot (a parity wait on v_full
+          // alone would pass early when this group's first stage reuses a slot
+          // whose previous phase has not completed yet); the first warp then
+          // either fetches a V image into it (LoRC stage) or releases v_full
+          mbar_wait(&a_empty[as], aph ^ 1);
           if (gw == 0 && lane == 0) {
-            mbar_wait(&a_empty[as], aph ^ 1);
             if (st >= ks) {
               int mat, ch, vpart, tpart;
               lorc_stage(P, st - ks, mat, ch, vpart, tpart);
-              mbar_arrive_expect_tx(&v_full[as], (uint32_t)kPfImg);
-              bulk_g2s(sA + mat * kPfImg, P.vimg[mat] + (((int64_t)nt * P.rchunks[mat] + ch) * 2 + vpart) * kPfImg,
-                       kPfImg, &v_full[as]);
+              mbar_arrive_expect_tx(&v_full[as], (uint32_t)(NG * kPfImg));
+              for (int ng = 0; ng < NG; ++ng)
+                bulk_g2s(sA + (ng * NMAT + mat) * kPfImg,
+                         P.vimg[mat] + (((int64_t)(NG * nt + ng) * P.rchunks[mat] + ch) * 2 + vpart) * kPfImg, kPfImg,
+                         &v_full[as]);
             } else {
               mbar_arrive(&v_full[as]);
             }
@@ -360,20 +374,20 @@ __global__ void __launch_bounds__(PfRoles<NMAT>::kThreads, 1) pf_gemm_kernel(con
             mbar_wait(&p_full[ps], pph);
             if (gw == 0 && lane == 0 && item == (int)blockIdx.x) pf_trace(st, 1);
             const uint8_t* sP = smem + CF::kOffP + ps * CF::kStageP;
-            constexpr int kJobs = 8 * NMAT / kPfGroupWarps;
+            constexpr int kJobs = 8 * NMAT * NG / kPfGroupWarps;
 #pragma unroll
             for (int jb = 0; jb < ((a.flags & 1) ? 0 : kJobs); ++jb) {
               const int jid = gw + kPfGroupWarps * jb;
               const int j = jid & 1, t4 = jid >> 1;
-              const int kt = t4 & 1, sl = (t4 >> 1) & 1, mat = t4 >> 2;
-              const uint8_t* tile = sP + ((mat * 2 + sl) * 2 + kt) * kTileBytes;
+              const int kt = t4 & 1, sl = (t4 >> 1) & 1, nm = t4 >> 2;  // nm = ng * NMAT + mat
+              const uint8_t* tile = sP + ((nm * 2 + sl) * 2 + kt) * kTileBytes;
               const uint32_t* pa = reinterpret_cast<const uint32_t*>(tile + kPlaneAOff + lane * 16);
               const uint32_t* pb = reinterpret_cast<const uint32_t*>(tile + kPlaneBOff + lane * 8);
               const uint4 mm = *reinterpret_cast<const uint4*>(tile + kMetaOff + q * 32 + 16 * j);
               const uint32_t S2[2] = {mm.x, mm.z}, O2[2] = {mm.y, mm.w};
               uint32_t wv[16];
               unit_dequant(pa[2 * j], pa[2 * j + 1], pb[j], S2, O2, dq, wv);
-              uint8_t* A = sA + mat * kPfImg;
+              uint8_t* A = sA + nm * kPfImg;
 #pragma unroll
               for (int pp = 0; pp < 16; ++pp) {
                 const int i = pp >> 2, r = pp & 3;
@@ -411,13 +425,13 @@ __global__ void __launch_bounds__(PfRoles<NMAT>::kThreads, 1) pf_gemm_kernel(con
       uint32_t acc_phase = 0;
       for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
         int p, nt, tt;
-        pf_item(a, item, p, nt, tt);
+        pf_item<NG>(a, item, p, nt, tt);
         const PfProblem P = a.problems[p];  // by value: fields live in registers
         const int ks = P.k / kPfK, total = item_stages(P);
         const uint32_t idesc = pf_idesc(P.ntok);
         mbar_wait(&acc_empty[acc], acc_phase ^ 1);
         tc_fence_after();
-        const uint32_t d0 = tmem + (uint32_t)(acc * NMAT * kPfN);
+        const uint32_t d0 = tmem + (uint32_t)(acc * NG * NMAT * kPfN);
         for (int st = 0; st < total; ++st) {
           mbar_wait(&a_full[as], aph);
 
@@ -432,14 +446,16 @@ __global__ void __launch_bounds__(PfRoles<NMAT>::kThreads, 1) pf_gemm_kernel(con
             mat0 = mat;
             mat1 = mat + 1;
           }
-          for (int mat = mat0; mat < mat1; ++mat) {
+          for (int ng = 0; ng < NG; ++ng)
+            for (int mat = mat0; mat < mat1; ++mat) {
 #pragma unroll
-            for (int k16 = 0; k16 < kPfK / 16; ++k16) {
-              const uint64_t da = pf_desc_sw128(aA + mat * kPfImg + k16 * 32);
-              const uint64_t db = pf_desc_sw128(aB + k16 * 32);
-              if (!(a.flags & 2)) pf_mma(d0 + (uint32_t)(mat * kPfN), da, db, idesc, (st > 0 || k16 > 0) ? 1u : 0u);
+              for (int k16 = 0; k16 < kPfK / 16; ++k16) {
+                const uint64_t da = pf_desc_sw128(aA + (ng * NMAT + mat) * kPfImg + k16 * 32);
+                const uint64_t db = pf_desc_sw128(aB + k16 * 32);
+                if (!(a.flags & 2))
+                  pf_mma(d0 + (uint32_t)((ng * NMAT + mat) * kPfN), da, db, idesc, (st > 0 || k16 > 0) ? 1u : 0u);
+              }
             }
-          }
           pf_commit(&a_empty[as]);
           pf_commit(&b_empty[bs]);
           if ((a.flags & 32) && item == (int)blockIdx.x && st < 64) {  // debug: commit latency
@@ -472,21 +488,23 @@ __global__ void __launch_bounds__(PfRoles<NMAT>::kThreads, 1) pf_gemm_kernel(con
     uint32_t acc_phase = 0;
     for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
       int p, nt, tt;
-      pf_item(a, item, p, nt, tt);
+      pf_item<NG>(a, item, p, nt, tt);
       const PfProblem P = a.problems[p];  // by value: fields live in registers
       mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
       if (threadIdx.x == 0) pf_dbg(6);
       // TMEM -> registers (thread = output column, 32 tokens per load) -> SwiGLU /
       // identity -> smem transpose -> 16-byte row stores (8 token rows per instruction)
-      const uint32_t tbase = tmem + ((uint32_t)(32 * ew) << 16) + (uint32_t)(acc * NMAT * kPfN);
       const int rows = P.rows, kind = P.kind, odt = P.out_dtype;
       const int64_t ldo = P.ldo;
       const int32_t* rmap = P.row_map;
       float* stg = reinterpret_cast<float*>(smem + CF::kOffStage) + ew * 32 * 33;
-      const int col0 = nt * kPfM + 32 * ew + 8 * (lane & 3);  // this lane's 8 output columns
-#pragma unroll 1
       const int ntok = P.ntok;
+#pragma unroll 1
+      for (int ng = 0; ng < NG; ++ng) {
+      const uint32_t tbase = tmem + ((uint32_t)(32 * ew) << 16) + (uint32_t)((acc * NG + ng) * NMAT * kPfN);
+      const int col0 = (NG * nt + ng) * kPfM + 32 * ew + 8 * (lane & 3);  // this lane's 8 output columns
+#pragma unroll 1
       for (int c0 = 0; c0 < ntok; c0 += 32) {
         uint32_t v0[32], v1[32];
         tmem_ld32(tbase + (uint32_t)c0, v0);
@@ -525,6 +543,7 @@ __global__ void __launch_bounds__(PfRoles<NMAT>::kThreads, 1) pf_gemm_kernel(con
         }
         __syncwarp();
       }
+      }  // ng
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[acc]);
@@ -665,6 +684,118 @@ __global__ void __launch_bounds__(256) pf_t_kernel(const TProb* __restrict__ pro
     if (row < P.rows) P.part[((int64_t)ksi * P.rows + row) * r64 + rcol] = acc[i];
   }
   (void)rcol;
+}
+
+// ---------------------------------------------------------------------------
+// Grouped activation images + LoRC t partials, one launch per GEMM phase.
+// CTA = (job, token tile, 64-k stage): the tile's rows (gathered, binary16)
+// become the stage's SW128 image, and while they sit in shared memory the CTA
+// also computes t = half(x) U over its 64 k for up to two compensators (fp32,
+// the reference's Eigen product order-independent up to rounding), written as
+// partials [k/64][rows][r64] that pf_t_images_kernel sums in stage order.
+// ---------------------------------------------------------------------------
+struct ImgT {
+  const uint8_t* ucodes;  // k x rank symm-int3 codes (or null -> ureal)
+  const float* uscales;   // k x gpr
+  const float* ureal;     // k x rank
+  int32_t rank, gpr, rchunks;
+  float* part;            // [k/64][rows][rchunks * 64]
+};
+struct ImgJob {
+  const void* x;
+  int32_t x_dtype;
+  int64_t ldx;
+  const int32_t* row_ids;  // null: identity
+  int32_t rows, k, ntok;
+  uint8_t* img;            // [tok_tiles][k/64][ntok x 128 B]
+  int32_t n_t;             // LoRC targets (0..2)
+  ImgT t[2];
+  int32_t blk0;            // first CTA of this job
+};
+constexpr int kImgTSmem = (kPfN * 65 + 64 * 65) * 4;
+
+__global__ void __launch_bounds__(256) pf_img_t_kernel(const ImgJob* __restrict__ jobs, int n_jobs) {
+  extern __shared__ float imgt_sm[];
+  float* sx = imgt_sm;             // [ntok][65]
+  float* su = imgt_sm + kPfN * 65; // [64][65]
+  int lo = 0, hi = n_jobs - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (jobs[mid].blk0 <= (int)blockIdx.x) lo = mid; else hi = mid - 1;
+  }
+  const ImgJob& J = jobs[lo];
+  const int ks = J.k / kPfK;
+  const int rel = blockIdx.x - J.blk0;
+  const int tile = rel / ks, st = rel % ks;
+  const int ntok = J.ntok, tid = threadIdx.x;
+  uint8_t* dst = J.img + (int64_t)rel * ntok * 128;
+  for (int c = tid; c < ntok * 8; c += blockDim.x) {  // 16-B chunks
+    const int r = c >> 3, ch = c & 7;
+    const int row = tile * ntok + r;
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (row < J.rows) {
+      const int64_t src_row = J.row_ids ? J.row_ids[row] : row;
+      const int64_t col = (int64_t)st * kPfK + ch * 8;
+      if (J.x_dtype == 0) {
+        const float4* sp = reinterpret_cast<const float4*>(static_cast<const float*>(J.x) + src_row * J.ldx + col);
+        const float4 p0 = sp[0], p1 = sp[1];
+        v = make_uint4(h2_as_u32(__floats2half2_rn(p0.x, p0.y)), h2_as_u32(__floats2half2_rn(p0.z, p0.w)),
+                       h2_as_u32(__floats2half2_rn(p1.x, p1.y)), h2_as_u32(__floats2half2_rn(p1.z, p1.w)));
+      } else {
+        v = *reinterpret_cast<const uint4*>(static_cast<const __half*>(J.x) + src_row * J.ldx + col);
+      }
+    }
+    *reinterpret_cast<uint4*>(dst + r * 128 + ((ch ^ (r & 7)) << 4)) = v;
+    if (J.n_t > 0) {
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float2 f = __half22float2(u32_as_h2(w[u]));
+        sx[r * 65 + ch * 8 + 2 * u] = f.x;
+        sx[r * 65 + ch * 8 + 2 * u + 1] = f.y;
+      }
+    }
+  }
+  if (J.n_t == 0) return;
+  const int j = tid & 63, rg = tid >> 6;  // rank column, row group (rows rg, rg + 4, ...)
+  const int nr4 = ntok / 4;               // rows per thread (ntok is a multiple of 16)
+  for (int ti = 0; ti < J.n_t; ++ti) {
+    const ImgT& T = J.t[ti];
+    const int r64 = T.rchunks * 64;
+    for (int ch = 0; ch < T.rchunks; ++ch) {
+      __syncthreads();  // sx written / su free
+      for (int e = tid; e < 64 * 64; e += blockDim.x) {  // U tile [64 k][64 ranks] (lowrank.cpp:122-134)
+        const int kk = e >> 6, jj = e & 63;
+        const int kr = st * kPfK + kk, rc = ch * 64 + jj;
+        float v = 0.0f;
+        if (rc < T.rank) {
+          if (T.ucodes) {
+            const float sp = T.uscales[(int64_t)kr * T.gpr + rc / 64] * (2.0f / 7.0f);
+            v = sp * ((float)T.ucodes[(int64_t)kr * T.rank + rc] - 4.0f);
+          } else {
+            v = T.ureal[(int64_t)kr * T.rank + rc];
+          }
+        }
+        su[kk * 65 + jj] = v;
+      }
+      __syncthreads();
+      float acc[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) acc[i] = 0.0f;
+#pragma unroll 4
+      for (int kk = 0; kk < 64; ++kk) {
+        const float uv = su[kk * 65 + j];
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (i < nr4) acc[i] += sx[(rg + 4 * i) * 65 + kk] * uv;
+      }
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int row = tile * ntok + rg + 4 * i;
+        if (i < nr4 && row < J.rows) T.part[((int64_t)st * J.rows + row) * r64 + ch * 64 + j] = acc[i];
+      }
+    }
+  }
 }
 
 // Sums the k-split partials in split order and writes the hi / lo images.

@@ -239,3 +239,21 @@ def test_prefill_identity_reproduces_weights(gpu, oracle):
     want = np.array([oracle.half_to_float(int(h)) for h in oracle.dequant_half(P).ravel()],
                     np.float32).reshape(k, n)
     assert (C == want).all()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m", [4, 96])
+def test_out_buffer_defines_output_dtype(gpu, m):
+    """A caller-provided output buffer fixes the output type (decode and prefill paths)."""
+    import torch
+    rng = np.random.default_rng(m)
+    from paper_2504_02658_b200.synth import packed_random_words
+    W = gpu.Weight(packed_random_words(256, 512, rng))
+    A = torch.from_numpy(rng.normal(0, 1, (m, 256)).astype(np.float32)).cuda()
+    ref = gpu.gemm_w3a16(A, W)
+    out16 = torch.full((m, 512), float("nan"), dtype=torch.float16, device="cuda")
+    got = gpu.gemm_w3a16(A, W, out=out16)
+    assert got is out16 and torch.isfinite(out16).all()
+    assert torch.allclose(out16.float(), ref, rtol=2e-3, atol=2e-3)
+    with pytest.raises(gpu.ArgumentError):
+        gpu.gemm_w3a16(A, W, out=out16, out_dtype=torch.float32)
