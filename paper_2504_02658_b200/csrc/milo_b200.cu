@@ -1018,7 +1018,11 @@ milo_status launch_prefill_ng(const PfProblem* host_probs, int n_probs, cudaStre
   a.n_problems = n_probs;
   a.n_items = starts[n_probs];
   if (a.n_items == 0) return MILO_OK;
-  const int grid = std::min(a.n_items, sms);
+  static const int grid_cap = [] {  // experiments: MILO_PF_GRID caps the persistent grid
+    const char* e = getenv("MILO_PF_GRID");
+    return e ? atoi(e) : 0;
+  }();
+  const int grid = std::min(a.n_items, grid_cap > 0 ? std::min(grid_cap, sms) : sms);
   CUDA_TRY(launch(pf_gemm_kernel<NMAT, NG>, dim3(grid), dim3(PfRoles<NMAT, NG>::kThreads), CF::kBytes, stream, false, a));
   return MILO_OK;
 }

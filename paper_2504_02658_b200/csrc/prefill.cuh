@@ -29,6 +29,18 @@
 
 namespace milo_dev {
 
+#ifndef PF_NG2_AS
+#define PF_NG2_AS 3
+#endif
+#ifndef PF_NG2_GROUPS
+#define PF_NG2_GROUPS 3
+#endif
+#ifndef PF_NG2_PS
+#define PF_NG2_PS 6
+#endif
+#ifndef PF_NG2_B
+#define PF_NG2_B 64
+#endif
 constexpr int kPfM = 128;              // output columns per tile (UMMA M)
 constexpr int kPfN = 128;              // tokens per tile (UMMA N, TMEM columns)
 constexpr int kPfK = 64;               // k per stage (128 B of binary16 per operand row)
@@ -49,16 +61,18 @@ constexpr int kPfDeqWarp0 = 7;
 // if the slot's barrier is at most one phase behind (st - 2 AS consumed).
 template <int NMAT, int NG = 1>
 struct PfRoles {
-  static constexpr int kGroups = NG == 2 ? 3 : (NMAT == 1 ? 4 : 3);  // stages de-quantized concurrently
+  static constexpr int kGroups = NG == 2 ? PF_NG2_GROUPS : (NMAT == 1 ? 4 : 3);  // stages de-quantized concurrently
   static constexpr int kDeqWarps = kGroups * kPfGroupWarps;
   static constexpr int kThreads = 32 * (kPfDeqWarp0 + kDeqWarps);
 };
 
 template <int NMAT, int NG = 1>
 struct PfCfg {
-  static constexpr int kPS = NG == 2 ? 6 : (NMAT == 1 ? 12 : 8);     // packed-weight ring (HBM latency)
-  static constexpr int kAS = NG == 2 ? 3 : (NMAT == 1 ? 6 : 3);      // dequantized A ring
-  static constexpr int kBRegion = NG == 2 ? 64 * 1024 : (NMAT == 1 ? 64 * 1024 : 32 * 1024);
+  // NG = 2: the packed (HBM) and activation (L2) rings are latency x depth
+  // bound per SM, so they get the space and A keeps PF_NG2_AS slots
+  static constexpr int kPS = NG == 2 ? PF_NG2_PS : (NMAT == 1 ? 12 : 8);      // packed-weight ring (HBM latency)
+  static constexpr int kAS = NG == 2 ? PF_NG2_AS : (NMAT == 1 ? 6 : 3);       // dequantized A ring
+  static constexpr int kBRegion = NG == 2 ? PF_NG2_B * 1024 : (NMAT == 1 ? 64 * 1024 : 32 * 1024);
   static constexpr int kBSMax = 16;                      // B slots = region / (ntok_max x 128), <= 16
   static constexpr int kStageA = NG * NMAT * kPfImg;
   static constexpr int kStageP = NG * NMAT * kPfPackedPerMat;

@@ -17,4 +17,4 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:decode_kernel -s 6 -c 1 \
   -o $O/prof_decode python tools/timeline.py --batch 1 --iters 3 > $O/ncu_full.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:pf_gemm_kernel -s 3 -c 1 \
-  -o $O/prof_prefill python tools/time_prefill.py 256 >> $O/ncu_full.log 2>&1
+  -o $O/prof_prefill python tools/time_prefill.py 2048 >> $O/ncu_full.log 2>&1
