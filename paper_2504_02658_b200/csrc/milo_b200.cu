@@ -781,7 +781,13 @@ milo_status launch_decode(DecArgs a, const void* x, int32_t x_dtype, int64_t ldx
   const size_t o_t = ar.take((size_t)nb_max * 3 * m_pad * std::max(r16_max, 16) * 8);
   const size_t o_h = ar.take(MOE ? (size_t)nb_max * m_pad * f_max * 2 : 0);
   const size_t o_y = ar.take(MOE ? (size_t)y_rows * a.d * 4 : 0);
-  const bool replicate = a.m <= 16;  // CTA-private x copies (decode.cuh)
+  // CTA-private binary16 copies of x (decode.cuh) when x is f32 (it is rounded
+  // to binary16 on the way); binary16 x is read in place
+  static const int xrep_env = [] {
+    const char* e = getenv("MILO_XREP");
+    return e ? atoi(e) : -1;
+  }();
+  const bool replicate = a.m <= 16 && (xrep_env >= 0 ? xrep_env == 1 : x_dtype == 0);
   const size_t o_x = ar.take(replicate ? (size_t)sms * a.m * a.d * 2
                                        : (x_dtype == 0 ? (size_t)a.m * a.d * 2 : 0));
   DecodeWs* w = nullptr;
