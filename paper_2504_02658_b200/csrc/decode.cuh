@@ -54,7 +54,9 @@ namespace milo_dev {
 #endif
 
 constexpr int kDecMaxBlocks = 64;
-constexpr int kDecMaxTok = 16;                    // MoE decode path: m <= 16
+constexpr int kDecMaxTok = 16;                    // token rows per block (NT = 2)
+constexpr int kDecMaxM = 64;                      // MoE decode path: m <= 64 (experts' tokens split into blocks)
+constexpr int kDecMaxEntries = 256;               // m * K routed entries
 constexpr int kDecMaxProbs = 3 * kDecMaxBlocks;   // per phase
 constexpr int kDecKC = 8;                         // max k-tiles (32 k each) per ring slot
 constexpr int kDecSlotW = 8192;                   // weight / pseudo-tile bytes per slot
@@ -148,6 +150,7 @@ struct DProb {
 struct DBlock {
   int32_t e;
   int32_t rows;
+  int32_t chunk;             // this block = the expert's tokens [chunk * m_pad, ...)
   int16_t xrow[kDecMaxTok];  // x row of each block row (MoE: token; linear: row)
   int16_t slot[kDecMaxTok];  // output row (MoE: Y slot; linear: C row)
 };
@@ -170,9 +173,10 @@ struct DecCfg {
   static constexpr int kOffProbs = kOffBars + kCons * kSlots * 8;
   static constexpr int kOffBlocks = kOffProbs + 2 * kDecMaxProbs * (int)sizeof(DProb);
   static constexpr int kOffRoute = kOffBlocks + kDecMaxBlocks * (int)sizeof(DBlock);
-  static constexpr int kRouteBytes = kDecMaxTok * 16 * 4 * 2 + 256 * 4 + 64;
+  static constexpr int kRouteBytes = kDecMaxEntries * 4 * 2 + 256 * 8 + 64;
   static constexpr int kOffMats = kOffRoute + kRouteBytes;  // DecExpert per block (smem copy)
-  static constexpr int kBytes = kOffMats + kDecMaxBlocks * (int)sizeof(DecExpert);
+  static constexpr int kMats = NMAT1 == 2 ? kDecMaxBlocks : 16;  // single linear: <= 16 / 8 blocks
+  static constexpr int kBytes = kOffMats + kMats * (int)sizeof(DecExpert);
 };
 
 // ---------------------------------------------------------------- helpers
@@ -591,14 +595,14 @@ __device__ __noinline__ void dec_stage0(const DecArgs& a) {
   DProb* probs = reinterpret_cast<DProb*>(smem + CF::kOffProbs);
   DBlock* blocks = reinterpret_cast<DBlock*>(smem + CF::kOffBlocks);
   int32_t* r_ids = reinterpret_cast<int32_t*>(smem + CF::kOffRoute);
-  float* r_wts = reinterpret_cast<float*>(r_ids + kDecMaxTok * 16);
-  uint32_t* emask = reinterpret_cast<uint32_t*>(r_wts + kDecMaxTok * 16);
+  float* r_wts = reinterpret_cast<float*>(r_ids + kDecMaxEntries);
+  unsigned long long* emask = reinterpret_cast<unsigned long long*>(r_wts + kDecMaxEntries);  // token bits
   int32_t* sc = reinterpret_cast<int32_t*>(emask + 256);
   const DecExpert* experts = MOE ? a.experts : &a.lin;
   const int m = a.m;
   if (MOE) {
     const int K = a.K, E = a.E;
-    for (int e = tid; e < 256; e += blockDim.x) emask[e] = 0u;
+    for (int e = tid; e < 256; e += blockDim.x) emask[e] = 0ull;
     if (a.logits != nullptr) {
       for (int t = warp; t < m; t += blockDim.x >> 5)
         topk_regs(a.logits + (int64_t)t * E, E, K, a.score_mode, r_ids + t * K, r_wts + t * K, lane);
@@ -616,30 +620,45 @@ __device__ __noinline__ void dec_stage0(const DecArgs& a) {
       }
     for (int i = tid; i < m * K; i += blockDim.x) {
       const int e = r_ids[i];
-      if (e >= 0 && e < E) atomicOr(&emask[e], 1u << (i / K));
+      if (e >= 0 && e < E) atomicOr(&emask[e], 1ull << (i / K));
     }
     __syncthreads();
-    if (warp == 0) {  // touched experts ascending, then shared experts
+    if (warp == 0) {  // touched experts ascending (their tokens in chunks of m_pad), then shared experts
       int nb = 0;
-      for (int e0 = 0; e0 < E; e0 += 32) {
+      const int nse = E + a.S;
+      for (int e0 = 0; e0 < nse; e0 += 32) {
         const int e = e0 + lane;
-        const bool on = e < E && emask[e] != 0u;
-        const uint32_t bal = __ballot_sync(0xffffffffu, on);
-        if (on) blocks[nb + __popc(bal & ((1u << lane) - 1u))].e = e;
-        nb += __popc(bal);
+        const int cnt = e < E ? __popcll(emask[e]) : (e < nse ? m : 0);
+        const int nch = (cnt + kMPad - 1) / kMPad;
+        int incl = nch;  // inclusive scan of the chunk counts
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int v = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += v;
+        }
+        for (int c = 0; c < nch; ++c) {
+          if (nb + incl - nch + c < kDecMaxBlocks) {
+            blocks[nb + incl - nch + c].e = e;
+            blocks[nb + incl - nch + c].chunk = c;
+          }
+        }
+        nb += __shfl_sync(0xffffffffu, incl, 31);
       }
-      for (int s = lane; s < a.S; s += 32) blocks[nb + s].e = E + s;
-      if (lane == 0) sc[0] = nb + a.S;
+      if (lane == 0) sc[0] = min(nb, kDecMaxBlocks);
     }
     __syncthreads();
     const int nb = sc[0];
     for (int b = tid; b < nb; b += blockDim.x) {
       DBlock& B = blocks[b];
       const int e = B.e;
-      const uint32_t mask = e < E ? emask[e] : ((1u << m) - 1u);
-      int r = 0;
-      for (int t = 0; t < m; ++t) {
-        if (!(mask >> t & 1u)) continue;
+      const unsigned long long mask = e < E ? emask[e] : (m >= 64 ? ~0ull : ((1ull << m) - 1ull));
+      int r = 0, skip = B.chunk * kMPad;
+      for (int t = 0; t < m && r < kMPad; ++t) {
+        if (!(mask >> t & 1ull)) continue;
+        if (skip > 0) {
+          --skip;
+          continue;
+        }
         int slot;
         if (e < E) {
           int kk = 0;
@@ -662,6 +681,7 @@ __device__ __noinline__ void dec_stage0(const DecArgs& a) {
     for (int b = tid; b < nb; b += blockDim.x) {
       DBlock& B = blocks[b];
       B.e = 0;
+      B.chunk = 0;
       B.rows = min(kMPad, m - b * kMPad);
       for (int r = 0; r < kDecMaxTok; ++r) {
         const bool on = r < B.rows;
@@ -673,7 +693,7 @@ __device__ __noinline__ void dec_stage0(const DecArgs& a) {
   __syncthreads();
   const int nb = sc[0];
   DecExpert* bx = reinterpret_cast<DecExpert*>(smem + CF::kOffMats);
-  for (int i = tid; i < nb * 3; i += blockDim.x) bx[i / 3].m[i % 3] = experts[blocks[i / 3].e].m[i % 3];
+  for (int i = tid; i < min(nb, CF::kMats) * 3; i += blockDim.x) bx[i / 3].m[i % 3] = experts[blocks[i / 3].e].m[i % 3];
   __syncthreads();
   // problem entries, one thread each: phase 1 [pseudo (b, mat)][real b], phase 2
   // [pseudo b][real b]; rank-0 pseudo entries stay as empty (n_slabs = 0) entries.
@@ -774,8 +794,8 @@ __device__ __noinline__ void dec_finish(const DecArgs& a, float* accs, int ph, i
   const DProb& P = reinterpret_cast<const DProb*>(smem + CF::kOffProbs)[ph * kDecMaxProbs + p];
   const DBlock* blocks = reinterpret_cast<const DBlock*>(smem + CF::kOffBlocks);
   const int32_t* r_ids = reinterpret_cast<const int32_t*>(smem + CF::kOffRoute);
-  const float* r_wts = reinterpret_cast<const float*>(r_ids + kDecMaxTok * 16);
-  const int32_t* sc = reinterpret_cast<const int32_t*>(r_wts + kDecMaxTok * 16 + 256);
+  const float* r_wts = reinterpret_cast<const float*>(r_ids + kDecMaxEntries);
+  const int32_t* sc = reinterpret_cast<const int32_t*>(reinterpret_cast<const unsigned long long*>(r_wts + kDecMaxEntries) + 256);
   const DecExpert* experts = MOE ? a.experts : &a.lin;
   const DecWs& W = a.ws;
   const int epoch = a.epoch;
@@ -1250,13 +1270,14 @@ template <int NT, int NMAT1, bool MOE>
 __global__ void __launch_bounds__(32 * DecCfg<NT, NMAT1>::kWarps, 1)
     decode_kernel(const __grid_constant__ DecArgs a) {
   using CF = DecCfg<NT, NMAT1>;
+  static_assert(CF::kBytes <= 227 * 1024, "decode kernel shared memory");
   constexpr int kC = CF::kCons, kS = CF::kSlots;
   extern __shared__ __align__(128) uint8_t smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   uint64_t* full_bars = reinterpret_cast<uint64_t*>(smem + CF::kOffBars);  // [kC][kS]
   const DProb* probs = reinterpret_cast<const DProb*>(smem + CF::kOffProbs);
   const DBlock* blocks = reinterpret_cast<const DBlock*>(smem + CF::kOffBlocks);
-  const int32_t* sc = reinterpret_cast<const int32_t*>(smem + CF::kOffRoute) + kDecMaxTok * 32 + 256;
+  const int32_t* sc = reinterpret_cast<const int32_t*>(smem + CF::kOffRoute + kDecMaxEntries * 8 + 256 * 8);
   const DecWs& W = a.ws;
   const DecExpert* experts = MOE ? a.experts : &a.lin;
 

@@ -1724,9 +1724,12 @@ milo_status moe_forward_impl(milo_moe* moe, const void* x, int64_t m, int32_t x_
   DeviceProps props = device_props();
   if (!props.ok || props.major != 10) return fail(MILO_ERR_CUDA, "no sm_100 device");
   cudaStream_t stream = (cudaStream_t)stream_;
-  const int64_t nb_dec = std::min<int64_t>(moe->E, m * moe->K) + moe->n_shared;
-  if (!legacy_path() && m <= kDecMaxTok && nb_dec <= kDecMaxBlocks && moe->E <= 256 &&
-      moe->K <= 16 && moe->d / 64 <= 4096) {
+  // decode megakernel blocks: each touched expert's tokens in chunks of m_pad rows
+  const int dec_mpad = m <= 8 ? 8 : 16;
+  const int64_t nb_dec = std::min<int64_t>(moe->E, m * moe->K) + (m * moe->K) / dec_mpad +
+                         (int64_t)moe->n_shared * ((m + dec_mpad - 1) / dec_mpad);
+  if (!legacy_path() && m <= kDecMaxM && m * moe->K <= kDecMaxEntries && nb_dec <= kDecMaxBlocks &&
+      moe->E <= 256 && moe->K <= 16 && moe->d / 64 <= 4096) {
     DecArgs a{};
     a.moe = 1;
     a.m = (int32_t)m;

@@ -37,7 +37,7 @@ def _experts(oracle, gpu, E, d, f, ranks, seed, mode=1):
     return o_ex, g_ex
 
 
-@pytest.mark.parametrize("m", [1, 3, 8, 16, 33, 100, 300])
+@pytest.mark.parametrize("m", [1, 3, 8, 16, 33, 64, 100, 300])
 def test_mixtral_like_layer(gpu, oracle, m):
     import torch
     E, K, d, f = 8, 2, 256, 512
@@ -134,3 +134,26 @@ def test_expert_parallel_layer_world1_matches_layer(gpu, oracle):
             assert rel_err(a.cpu().numpy(), b.cpu().numpy()) <= 1e-5
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m", [20, 64])
+def test_hot_expert_token_chunks(gpu, oracle, m):
+    """Decode megakernel with m <= 64: an expert routed more than 16 tokens is split into
+    16-row blocks (chunks), combined in k order like the oracle."""
+    import torch
+    E, K, d, f = 8, 2, 256, 512
+    ranks = [[(8 * ((e + j) % 4)) for j in range(3)] for e in range(E)]
+    o_ex, g_ex = _experts(oracle, gpu, E, d, f, ranks, seed=1300)
+    rng = np.random.default_rng(7 + m)
+    x = rng.normal(0, 1, (m, d)).astype(np.float32)
+    logits = rng.normal(0, 1, (m, E)).astype(np.float32)
+    logits[:, 3] += 10.0  # every token routes to expert 3 (m rows: several chunks)
+    ids, w = oracle.router_topk(logits, K, 0)
+    assert (ids[:, 0] == 3).all()
+    want = oracle.moe_forward(o_ex, [], x, ids, w)
+    layer = gpu.MoELayer(g_ex, [], top_k=K, score_mode=0)
+    out, gids, _ = layer.forward(torch.from_numpy(x).cuda(), torch.from_numpy(logits).cuda(),
+                                 return_routing=True)
+    assert (gids.cpu().numpy() == ids).all()
+    assert rel_err(out.cpu().numpy(), want) <= TOL_MOE
