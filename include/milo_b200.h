@@ -201,12 +201,14 @@ milo_status milo_moe_forward_host(milo_moe* moe, const float* x, int64_t m,
 
 /* Expert-parallel exchange (paper_2504_02658_b200/ep.py): fixed-capacity
  * dispatch of the m x K routed entries to `world` ranks owning `per` experts
- * each.  send_x: (world * capacity) x d binary16 rows, send_meta: local expert
- * id per row (-1 = unused), slot: m * K row index of each entry (-1 = unused).
- * m * K <= 1024, world * capacity <= 8192. */
+ * each.  send_x: (world * capacity) rows of ld_send binary16 (the first d =
+ * x row), send_meta: local expert id per row (-1 = unused) -- or NULL to put
+ * the id in the row itself as an int32 at half-column d (ld_send >= d + 8, one
+ * all-to-all for rows and ids); slot: m * K row index of each entry (-1 =
+ * unused).  m * K <= 1024, world * capacity <= 8192. */
 milo_status milo_ep_dispatch(const int32_t* ids, int64_t m, int32_t K, int32_t world, int32_t per,
                              int32_t capacity, const void* x, int32_t x_dtype, int64_t d, void* send_x,
-                             int32_t* send_meta, int32_t* slot, void* stream);
+                             int64_t ld_send, int32_t* send_meta, int32_t* slot, void* stream);
 /* out[t] = sum_k w[t,k] y[slot[t K + k]] in k order (f32), the EP combine. */
 milo_status milo_ep_combine(const float* y, const int32_t* slot, const float* wts, int64_t m, int32_t K,
                             int64_t d, float* out, void* stream);

@@ -137,7 +137,7 @@ def lib() -> C.CDLL:
         "milo_moe_forward": [vp, vp, i64, i32, vp, vp, i32, vp, vp, vp],
         "milo_moe_forward_routed": [vp, vp, i64, i32, vp, vp, vp, i32, vp],
         "milo_moe_forward_host": [vp, f32p, i64, f32p, f32p],
-        "milo_ep_dispatch": [vp, i64, i32, i32, i32, i32, vp, i32, i64, vp, vp, vp, vp],
+        "milo_ep_dispatch": [vp, i64, i32, i32, i32, i32, vp, i32, i64, vp, i64, vp, vp, vp],
         "milo_ep_combine": [vp, vp, vp, i64, i32, i64, vp, vp],
     }
     for name, args in sig.items():
@@ -459,20 +459,23 @@ class MoELayer:
 
 
 # ---------------------------------------------------------------- expert-parallel helpers
-def ep_dispatch(ids, x, world: int, per: int, capacity: int, stream=None):
-    """Fixed-capacity EP dispatch on the device: returns (send_x f16 [world*C, d],
-    send_meta int32 [world*C], slot int32 [m*K])."""
+def ep_dispatch(ids, x, world: int, per: int, capacity: int, stream=None, packed: bool = False):
+    """Fixed-capacity EP dispatch on the device.  Returns (send_x f16 [world*C, d],
+    send_meta int32 [world*C], slot int32 [m*K]); packed=True: (send f16
+    [world*C, d + 8] with the local expert id as int32 at column d, None, slot)."""
     import torch
     m, K = ids.shape
     d = x.shape[1]
-    send_x = torch.empty((world * capacity, d), dtype=torch.float16, device=x.device)
-    send_m = torch.empty((world * capacity,), dtype=torch.int32, device=x.device)
+    ld = d + 8 if packed else d
+    send_x = torch.empty((world * capacity, ld), dtype=torch.float16, device=x.device)
+    send_m = None if packed else torch.empty((world * capacity,), dtype=torch.int32, device=x.device)
     slot = torch.empty((m * K,), dtype=torch.int32, device=x.device)
     ids = ids.contiguous().int()
     x = x.contiguous()
     _check(lib().milo_ep_dispatch(_dptr(ids), m, K, world, per, capacity, _dptr(x),
-                                  F32 if x.dtype == torch.float32 else F16, d, _dptr(send_x),
-                                  _dptr(send_m), _dptr(slot), _stream_ptr(stream)))
+                                  F32 if x.dtype == torch.float32 else F16, d, _dptr(send_x), ld,
+                                  _dptr(send_m) if send_m is not None else None, _dptr(slot),
+                                  _stream_ptr(stream)))
     return send_x, send_m, slot
 
 

@@ -1812,14 +1812,16 @@ extern "C" milo_status milo_moe_forward(milo_moe* moe, const void* x, int64_t m,
 // Expert-parallel exchange helpers (include/milo_b200.h).
 extern "C" milo_status milo_ep_dispatch(const int32_t* ids, int64_t m, int32_t K, int32_t world,
                                         int32_t per, int32_t capacity, const void* x, int32_t x_dtype,
-                                        int64_t d, void* send_x, int32_t* send_meta, int32_t* slot,
-                                        void* stream) {
+                                        int64_t d, void* send_x, int64_t ld_send, int32_t* send_meta,
+                                        int32_t* slot, void* stream) {
   if (m < 0 || K < 1 || world < 1 || per < 1 || capacity < m * K || m * K > 1024 ||
       (int64_t)world * capacity > 8192 || d % 8 != 0)
     return fail(MILO_ERR_CONFIG, "ep_dispatch: unsupported sizes (m K <= 1024, world x capacity <= 8192)");
+  if (ld_send % 8 != 0 || ld_send < (send_meta ? d : d + 8))
+    return fail(MILO_ERR_CONFIG, "ep_dispatch: row stride must be a multiple of 8 and hold the id columns");
   if (m == 0) return MILO_OK;
   CUDA_TRY(launch(ep_dispatch_kernel, dim3(1), dim3(1024), 0, (cudaStream_t)stream, false, ids,
-                  (int32_t)(m * K), K, world, per, capacity, x, x_dtype, d, static_cast<__half*>(send_x),
+                  (int32_t)(m * K), K, world, per, capacity, x, x_dtype, d, static_cast<__half*>(send_x), ld_send,
                   send_meta, slot));
   return MILO_OK;
 }

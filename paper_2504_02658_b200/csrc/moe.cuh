@@ -376,10 +376,13 @@ namespace milo_dev {
 // the send buffer carries binary16 x[t] and the local expert id (-1 = unused).
 // One CTA (entries <= 1024).  slot[e] = dest * C + pos (or -1) for the combine.
 // ---------------------------------------------------------------------------
+// ld_send: row stride of send_x (halves).  send_meta == null: the local expert id
+// travels in the row itself (int32 at half-column d; ld_send >= d + 8), so one
+// all-to-all moves rows and ids together.
 __global__ void ep_dispatch_kernel(const int32_t* __restrict__ ids, int32_t mK, int32_t K, int32_t W,
                                    int32_t per, int32_t C, const void* __restrict__ x, int32_t x_dtype,
-                                   int64_t d, __half* __restrict__ send_x, int32_t* __restrict__ send_meta,
-                                   int32_t* __restrict__ slot) {
+                                   int64_t d, __half* __restrict__ send_x, int64_t ld_send,
+                                   int32_t* __restrict__ send_meta, int32_t* __restrict__ slot) {
   __shared__ int32_t s_slot[1024];
   __shared__ int32_t s_src[1024 * 8];  // slot -> entry (W * C <= 8192)
   const int tid = threadIdx.x;
@@ -404,7 +407,14 @@ __global__ void ep_dispatch_kernel(const int32_t* __restrict__ ids, int32_t mK, 
   __syncthreads();
   for (int r = tid; r < W * C; r += blockDim.x) {
     const int e = s_src[r];
-    send_meta[r] = e >= 0 ? ids[e] - (ids[e] / per) * per : -1;
+    const int32_t lid = e >= 0 ? ids[e] - (ids[e] / per) * per : -1;
+    if (send_meta != nullptr) {
+      send_meta[r] = lid;
+    } else {
+      int32_t* tail = reinterpret_cast<int32_t*>(send_x + (int64_t)r * ld_send + d);
+      tail[0] = lid;
+      tail[1] = tail[2] = tail[3] = 0;
+    }
   }
   const int64_t d8 = d / 8;
   for (int64_t i = tid; i < (int64_t)W * C * d8; i += blockDim.x) {
@@ -422,7 +432,7 @@ __global__ void ep_dispatch_kernel(const int32_t* __restrict__ ids, int32_t mK, 
         v = *reinterpret_cast<const uint4*>(static_cast<const __half*>(x) + t * d + c);
       }
     }
-    *reinterpret_cast<uint4*>(send_x + (int64_t)r * d + c) = v;
+    *reinterpret_cast<uint4*>(send_x + (int64_t)r * ld_send + c) = v;
   }
   (void)s_slot;
 }

@@ -95,11 +95,12 @@ class ExpertParallelMoE:
         assert m * self.K <= C, "fixed-capacity exchange: m * top_k exceeds the capacity"
         if self.device_kernels:
             import paper_2504_02658_b200 as mb
-            send_x, send_m, slot = mb.ep_dispatch(ids, x, W, self.per, C)
-            recv_x = torch.empty_like(send_x)
-            recv_m = torch.empty_like(send_m)
-            dist.all_to_all_single(recv_x, send_x, group=self.group)
-            dist.all_to_all_single(recv_m, send_m, group=self.group)
+            # rows and local expert ids in one buffer: one all-to-all for both
+            send, _, slot = mb.ep_dispatch(ids, x, W, self.per, C, packed=True)
+            recv = torch.empty_like(send)
+            dist.all_to_all_single(recv, send, group=self.group)
+            recv_x = recv[:, :self.d].contiguous()
+            recv_m = recv[:, self.d:self.d + 2].contiguous().view(torch.int32).view(-1)
             y_recv = self.local_fn(recv_x, recv_m).to(torch.float32)
             y_back = torch.empty_like(y_recv)
             dist.all_to_all_single(y_back, y_recv, group=self.group)
