@@ -168,10 +168,14 @@ class ExpertParallelMoE:
 
 def milo_local_fn(layer):
     """Binds the owned experts (a MoELayer over them, top_k = 1) as local_fn."""
+    ones = {}  # rows -> cached unit routing weights (no fill kernel per call)
+
     def fn(x_rows: torch.Tensor, local_ids: torch.Tensor) -> torch.Tensor:
         ids = local_ids.view(-1, 1).to(torch.int32)
-        w = torch.ones((x_rows.shape[0], 1), dtype=torch.float32, device=x_rows.device)
-        return layer.forward_routed(x_rows, ids, w)
+        key = (x_rows.shape[0], x_rows.device)
+        if key not in ones:
+            ones[key] = torch.ones((x_rows.shape[0], 1), dtype=torch.float32, device=x_rows.device)
+        return layer.forward_routed(x_rows, ids, ones[key])
     return fn
 
 
