@@ -1271,6 +1271,10 @@ struct milo_moe {
   std::vector<std::array<const milo_weight*, 3>> hw;
   std::vector<std::array<const milo_comp*, 3>> hc;
   bool prefill_ok = true;
+  // host-buffer entry point: pinned staging (x | logits, then out) and device buffer, grown on demand
+  void* host_stage = nullptr;
+  void* dev_stage = nullptr;
+  size_t stage_bytes = 0;
 };
 
 extern "C" milo_status milo_moe_create(const milo_expert_desc* experts, int32_t n_experts,
@@ -1374,6 +1378,8 @@ extern "C" milo_status milo_moe_destroy(milo_moe* moe) {
   if (!moe) return MILO_OK;
   cudaFree(moe->dev_experts);
   cudaFree(moe->dec_experts);
+  if (moe->host_stage) cudaFreeHost(moe->host_stage);
+  if (moe->dev_stage) cudaFree(moe->dev_stage);
   delete moe;
   return MILO_OK;
 }
@@ -1840,24 +1846,37 @@ extern "C" milo_status milo_moe_forward_host(milo_moe* moe, const float* x, int6
                                              const float* logits, float* out) {
   if (!moe) return fail(MILO_ERR_ARGUMENT, "null moe");
   if (m <= 0) return m == 0 ? MILO_OK : fail(MILO_ERR_SHAPE, "negative token count");
+  if (!x || !out || (moe->E > 0 && !logits)) return fail(MILO_ERR_ARGUMENT, "null argument");
   cudaStream_t stream = nullptr;
-  const size_t xb = (size_t)m * moe->d * 4, lb = (size_t)m * std::max(moe->E, 1) * 4;
-  void* mem = nullptr;
-  CUDA_TRY(cudaMallocAsync(&mem, 2 * xb + lb, stream));
-  uint8_t* b = static_cast<uint8_t*>(mem);
-  cudaError_t e = cudaMemcpyAsync(b, x, xb, cudaMemcpyHostToDevice, stream);
-  if (e == cudaSuccess && moe->E > 0)
-    e = cudaMemcpyAsync(b + xb, logits, (size_t)m * moe->E * 4, cudaMemcpyHostToDevice, stream);
+  // x and logits go up in ONE copy from a pinned staging buffer (host memcpy is
+  // cheaper than a second DMA launch at decode sizes); out comes back in one.
+  const size_t xb = (size_t)m * moe->d * 4, lb = (size_t)m * std::max(moe->E, 0) * 4;
+  const size_t lb16 = (lb + 15) & ~size_t(15);
+  const size_t need = xb + lb16 + xb;
+  if (moe->stage_bytes < need) {
+    if (moe->host_stage) cudaFreeHost(moe->host_stage);
+    if (moe->dev_stage) cudaFree(moe->dev_stage);
+    moe->host_stage = moe->dev_stage = nullptr;
+    moe->stage_bytes = 0;
+    CUDA_TRY(cudaMallocHost(&moe->host_stage, need));
+    CUDA_TRY(cudaMalloc(&moe->dev_stage, need));
+    moe->stage_bytes = need;
+  }
+  uint8_t* hs = static_cast<uint8_t*>(moe->host_stage);
+  uint8_t* b = static_cast<uint8_t*>(moe->dev_stage);
+  std::memcpy(hs, x, xb);
+  if (lb) std::memcpy(hs + xb, logits, lb);
+  cudaError_t e = cudaMemcpyAsync(b, hs, xb + lb, cudaMemcpyHostToDevice, stream);
   milo_status st = e == cudaSuccess ? MILO_OK : fail(MILO_ERR_CUDA, "%s", cudaGetErrorString(e));
   if (st == MILO_OK)
-    st = milo_moe_forward(moe, b, m, MILO_F32, reinterpret_cast<float*>(b + xb), b + xb + lb,
-                          MILO_F32, nullptr, nullptr, stream);
+    st = milo_moe_forward(moe, b, m, MILO_F32, reinterpret_cast<float*>(b + xb), b + xb + lb16, MILO_F32, nullptr,
+                          nullptr, stream);
   if (st == MILO_OK) {
-    e = cudaMemcpyAsync(out, b + xb + lb, xb, cudaMemcpyDeviceToHost, stream);
+    e = cudaMemcpyAsync(hs + xb + lb16, b + xb + lb16, xb, cudaMemcpyDeviceToHost, stream);
     if (e != cudaSuccess) st = fail(MILO_ERR_CUDA, "%s", cudaGetErrorString(e));
   }
-  cudaFreeAsync(mem, stream);
   e = cudaStreamSynchronize(stream);
   if (st == MILO_OK && e != cudaSuccess) st = fail(MILO_ERR_CUDA, "%s", cudaGetErrorString(e));
+  if (st == MILO_OK) std::memcpy(out, hs + xb + lb16, xb);
   return st;
 }
