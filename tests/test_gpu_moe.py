@@ -157,3 +157,53 @@ def test_hot_expert_token_chunks(gpu, oracle, m):
                                  return_routing=True)
     assert (gids.cpu().numpy() == ids).all()
     assert rel_err(out.cpu().numpy(), want) <= TOL_MOE
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,m,K", [(4, 3, 2), (8, 5, 2), (2, 16, 6)])
+def test_ep_dispatch_combine_kernels_multi_rank_layout(gpu, world, m, K):
+    """The EP exchange kernels for world > 1 (the multi-GPU scaling path, which a
+    1-GPU box cannot run end to end): every routed entry lands in its owner's
+    capacity block in entry order with its local expert id, unused rows carry
+    id -1 and zeros, and the combine sums the returned rows in k order."""
+    import torch
+    E, d = 4 * world, 64
+    per = E // world
+    C = m * K
+    rng = np.random.default_rng(world * 100 + m)
+    ids = np.stack([rng.choice(E, K, replace=False) for _ in range(m)]).astype(np.int32)
+    ids[0, -1] = -1  # an unused routing slot
+    x = rng.normal(0, 1, (m, d)).astype(np.float32)
+    send, _, slot = gpu.ep_dispatch(torch.from_numpy(ids).cuda(), torch.from_numpy(x).cuda(), world, per, C,
+                                    packed=True)
+    send = send.cpu()
+    slot = slot.cpu().numpy()
+    rows = send[:, :d].float().numpy()
+    lid = send[:, d:d + 2].contiguous().view(torch.int32).view(-1).numpy()
+    used = np.zeros(world * C, bool)
+    for dest in range(world):
+        pos = 0
+        for t in range(m):
+            for k in range(K):
+                e = ids[t, k]
+                if e < 0 or e // per != dest:
+                    continue
+                r = dest * C + pos
+                assert slot[t * K + k] == r
+                assert lid[r] == e - dest * per
+                assert np.array_equal(rows[r], x[t].astype(np.float16).astype(np.float32))
+                used[r] = True
+                pos += 1
+    assert slot[0 * K + K - 1] == -1
+    assert (lid[~used] == -1).all() and (rows[~used] == 0).all()
+    # combine: y rows returned per slot, weighted in k order
+    y = rng.normal(0, 1, (world * C, d)).astype(np.float32)
+    w = rng.random((m, K)).astype(np.float32)
+    out = gpu.ep_combine(torch.from_numpy(y).cuda(), torch.from_numpy(slot).cuda(),
+                         torch.from_numpy(w).cuda()).cpu().numpy()
+    want = np.zeros((m, d), np.float32)
+    for t in range(m):
+        for k in range(K):
+            if slot[t * K + k] >= 0:
+                want[t] += w[t, k] * y[slot[t * K + k]]
+    assert np.allclose(out, want, rtol=1e-6, atol=1e-6)
