@@ -297,18 +297,31 @@ def main():
     p2_bytes = float(np.mean([t["phase2_bytes"] for t in tr_p]))
     hbm = float(peaks["hbm_gbs"])
     single = n2 == 0  # one-launch decode kernel: the whole layer is one kernel
+    prefill = m > 64  # tcgen05 path: pf_gemm_kernel<2> (w1|w3) then pf_gemm_kernel<1> (w2)
+    bound, unit, peak = "hbm", "GB/s", hbm
     if single:
         dom_bytes = p1_bytes + p2_bytes
         dom_ms = t1 / max(n1, 1)
         dom_name = ("decode_kernel<%d,2,MoE> (whole layer: routing, LoRC, w1|w3+SwiGLU, w2, combine)"
                     % (1 if m <= 8 else 2))
+    elif prefill:
+        dom_bytes = p1_bytes
+        dom_ms = t1 / max(n1, 1)
+        dom_name = "pf_gemm_kernel<2,1> (phase 1: w1|w3 + LoRC stages + SwiGLU, tcgen05)"
+        bound, unit, peak = "tensor", "TFLOP/s", float(peaks["bf16_tflops"])
     else:
         dom_bytes = p1_bytes
         dom_ms = t1 / max(n1, 1)
         dom_name = "gemv_w3a16_kernel<NT,2> (phase 1: w1|w3 + SwiGLU + LoRC)"
     p1_ms = dom_ms
     p2_ms = t2 / max(n2, 1)
-    achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
+    if dom_ms <= 0:
+        achieved = 0.0
+    elif bound == "tensor":  # phase-1 flops: 2 matrices of d x f per routed token + LoRC
+        p1_flops = float(np.mean([t.get("phase1_flops", 0.0) for t in tr_p]))
+        achieved = p1_flops / (dom_ms * 1e-3) / 1e12
+    else:
+        achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
     traffic_ncu = None
     ncu_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(ncu_path):
@@ -381,8 +394,8 @@ def main():
                    "l2": "flushed between steps (256 MiB write + 256 MiB read, outside the timed events)"},
         "achieved_GBps_layer": round(tot_bytes / (value_us * 1e-6) / 1e9, 1),
         "layer_bytes": int(tot_bytes), "layer_flops": int(tot_flops),
-        "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": round(achieved, 1), "peak": hbm,
-                     "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": traffic_ncu,
+        "roofline": {"bound": bound, "kernel": dom_name, "achieved": round(achieved, 1), "peak": peak,
+                     "unit": unit, "frac": round(achieved / peak, 4), "traffic": traffic_ncu if bound == "hbm" else None,
                      "algorithmic_bytes_per_launch": int(dom_bytes),
                      "launch_us": round(p1_ms * 1e3, 2), "peak_source": peaks_src,
                      "phase2": {"algorithmic_bytes_per_launch": int(p2_bytes),

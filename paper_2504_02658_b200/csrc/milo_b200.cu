@@ -1029,6 +1029,7 @@ milo_status launch_prefill_ng(const PfProblem* host_probs, int n_probs, cudaStre
     return e ? atoi(e) : 0;
   }();
   const int grid = std::min(a.n_items, grid_cap > 0 ? std::min(grid_cap, sms) : sms);
+  ProfScope ps(NMAT == 2 ? kProfGemv1 : kProfGemv2, stream);  // bench: w1|w3 (phase 1) / w2 or linear
   CUDA_TRY(launch(pf_gemm_kernel<NMAT, NG>, dim3(grid), dim3(PfRoles<NMAT, NG>::kThreads), CF::kBytes, stream, false, a));
   return MILO_OK;
 }

@@ -5,12 +5,12 @@ import paper_2504_02658_b200 as mb
 from paper_2504_02658_b200.synth import CONFIGS, build_host_layer
 m = int(sys.argv[1]) if len(sys.argv) > 1 else 1
 mode = sys.argv[2] if len(sys.argv) > 2 else "moe"
-if mode == "moe":
-    spec = CONFIGS["mixtral"]
+if mode == "moe" or mode in CONFIGS:
+    spec = CONFIGS["mixtral" if mode == "moe" else mode]
     routed, shared = build_host_layer(spec, 0)
-    ex = [mb.Expert(*(mb.Weight(P) for P in h.w), *((mb.Comp(c) if c is not None else None) for c in h.c)) for h in routed]
-    layer = mb.MoELayer(ex, [], top_k=2)
-    x = torch.randn(m, 4096, device="cuda").half(); lg = torch.randn(m, 8, device="cuda")
+    mk = lambda hs: [mb.Expert(*(mb.Weight(P) for P in h.w), *((mb.Comp(c) if c is not None else None) for c in h.c)) for h in hs]
+    layer = mb.MoELayer(mk(routed), mk(shared), top_k=spec.top_k, score_mode=spec.score_mode)
+    x = torch.randn(m, spec.d, device="cuda").half(); lg = torch.randn(m, spec.experts, device="cuda")
     run = lambda: layer.forward(x, lg)
 else:
     from paper_2504_02658_b200.synth import packed_random_words
@@ -51,6 +51,6 @@ ue = d[:, 3] - t0; dn = d[:, 4] - t0
 order = np.argsort(-dn)[:12]
 print("latest p1-done warps (gw, cta, warp, units_end us, done us):")
 for w in order:
-    print(f"  gw={w:5d} cta={w // 12 if mode != 'moe' else w // 8:4d} units_end={ue[w]/1e3:7.2f} done={dn[w]/1e3:7.2f}")
+    print(f"  gw={w:5d} cta={w // 12 if mode == 'linear' else w // 8:4d} units_end={ue[w]/1e3:7.2f} done={dn[w]/1e3:7.2f}")
 order = np.argsort(-ue)[:8]
 print("latest units-end warps:", [(int(w), round(ue[w]/1e3, 1)) for w in order])
