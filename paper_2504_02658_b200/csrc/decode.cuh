@@ -950,7 +950,9 @@ __device__ __noinline__ void dec_finish(const DecArgs& a, float* accs, int ph, i
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int row = 8 * nt + 2 * q + (e & 1);
-          float h = silu_f(acc[0][i][nt][e]) * acc[NM - 1][i][nt][e];
+          // fast SiLU (h is rounded to binary16 next; MoE outputs stay within the 1e-4 tolerance)
+          const float g1 = acc[0][i][nt][e];
+          float h = __fdividef(g1, 1.0f + __expf(-g1)) * acc[NM - 1][i][nt][e];
           if (row >= B.rows) h = 0.0f;
           const float h_next = __shfl_down_sync(0xffffffffu, h, 4);  // column n + 1
           if ((g & 1) == 0 && !dry) {

@@ -158,7 +158,8 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
       : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ float pf_silu(float a) { return a / (1.0f + expf(-a)); }
+// fast SiLU: the result is rounded to binary16 (h rows) right after
+__device__ __forceinline__ float pf_silu(float a) { return __fdividef(a, 1.0f + __expf(-a)); }
 // Latency-critical handoffs spin on the non-blocking test (no suspend window).
 __device__ __forceinline__ void pf_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
