@@ -292,6 +292,34 @@ __device__ __forceinline__ void wait_h(const int32_t* hflag, int k0, int k1, int
   }
 }
 
+// Same, with the readiness already seen kept in a warp-uniform 32-slab window
+// (base, mask): once a segment's flags have been seen, later slots need no
+// global round trip.  nflags bounds the block's flag array.
+struct HWin {
+  int base;
+  uint32_t mask;
+};
+__device__ __forceinline__ void wait_h_cached(const int32_t* hflag, int nflags, HWin& w, int k0, int k1, int epoch,
+                                              int lane) {
+  const int j0 = k0 >> 6, j1 = (k1 - 1) >> 6;
+  if (j0 < w.base || j1 >= w.base + 32) {
+    w.base = j0;
+    w.mask = 0u;
+  }
+  const int n = j1 - j0 + 1;
+  const uint32_t need = (n >= 32 ? 0xffffffffu : ((1u << n) - 1u)) << (j0 - w.base);
+  if ((w.mask & need) == need) return;
+  const long long t0 = clock64();
+  for (;;) {
+    const int j = w.base + lane;
+    const bool ok = ((w.mask >> lane) & 1u) || (j < nflags && ld_relaxed_gpu(hflag + j) == epoch);
+    w.mask = __ballot_sync(0xffffffffu, ok);
+    if ((w.mask & need) == need) return;
+    __nanosleep(64);
+    if (clock64() - t0 > 4000000000LL) __trap();
+  }
+}
+
 // B fragments of one 32-k tile, loaded straight from the activation rows
 // (binary16, row-major, L1/L2 resident): v[j][nt] = {x[row][k + 16 j + 2q .. +1],
 // x[row][k + 16 j + 2q + 8 .. +9]}, row = 8 nt + g.  rowp[nt] == nullptr -> padding
@@ -1181,9 +1209,11 @@ __device__ __forceinline__ void run_phase(const DecArgs& a, Prod<NT, NMAT1, MOE>
     int k = tt * 32;
     BTile<NT> bc, bn1;
     // phase 2: the h slabs of this slot and of the look-ahead tiles
+    HWin hwin{0, 0u};
+    const int nhf = a.ws.f_max >> 6;
     if (PH == 1) {
       const long long th0 = DEC_TIMERS ? clock64() : 0;
-      wait_h(hfl, k, min(kend, k + (min(pkc, seg_end - pos) + kLA) * 32), a.epoch, lane);
+      wait_h_cached(hfl, nhf, hwin, k, min(kend, k + (min(pkc, seg_end - pos) + kLA) * 32), a.epoch, lane);
       if (DEC_TIMERS) ps.t_h += clock64() - th0;
     }
     const bool bload = !(a.dbg_flags & 32);  // experiment: bit 5 = no activation loads (wrong results)
@@ -1195,7 +1225,7 @@ __device__ __forceinline__ void run_phase(const DecArgs& a, Prod<NT, NMAT1, MOE>
       left -= kc;
       if (PH == 1 && k != tt * 32) {
         const long long th0 = DEC_TIMERS ? clock64() : 0;
-        wait_h(hfl, k, min(kend, k + (kc + kLA) * 32), a.epoch, lane);
+        wait_h_cached(hfl, nhf, hwin, k, min(kend, k + (kc + kLA) * 32), a.epoch, lane);
         if (DEC_TIMERS) ps.t_h += clock64() - th0;
       }
       if (DEC_TIMERS) {
