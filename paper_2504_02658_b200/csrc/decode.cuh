@@ -320,6 +320,15 @@ __device__ __forceinline__ void wait_h_cached(const int32_t* hflag, int nflags, 
   }
 }
 
+// Stream-K range arithmetic in 32 bits (tiles per phase x warps < 2^32, checked
+// at launch): 64-bit divisions are software routines on the finisher's chain.
+__device__ __forceinline__ int rng_at(int w, int T, int G) {
+  return (int)(((uint32_t)w * (uint32_t)T) / (uint32_t)G);
+}
+__device__ __forceinline__ int rng_owner(int x, int T, int G) {
+  return (int)((((uint32_t)x + 1u) * (uint32_t)G - 1u) / (uint32_t)T);
+}
+
 // B fragments of one 32-k tile, loaded straight from the activation rows
 // (binary16, row-major, L1/L2 resident): v[j][nt] = {x[row][k + 16 j + 2q .. +1],
 // x[row][k + 16 j + 2q + 8 .. +9]}, row = 8 nt + g.  rowp[nt] == nullptr -> padding
@@ -842,8 +851,8 @@ __device__ __noinline__ void dec_finish(const DecArgs& a, float* accs, int ph, i
     // the slab (its piece is its last work of the phase, so it is the latest
     // to arrive; the contributor after it only holds the slab's first piece of
     // its own range).  The others publish tagged partials and move on.
-    int w0 = (int)owner_of(sb, Tp, Gp), w1 = (int)owner_of(se - 1, Tp, Gp);
-    const int w1end = (int)((int64_t)(w1 + 1) * Tp / Gp);
+    int w0 = rng_owner(sb, Tp, Gp), w1 = rng_owner(se - 1, Tp, Gp);
+    const int w1end = rng_at(w1 + 1, Tp, Gp);
     int fin = (w1end <= se || w1 == w0) ? w1 : w1 - 1;
     if (dry) {  // code warm-up: the finisher path with one (pretend-ready) other contributor
       w0 = gw - 1;
@@ -888,7 +897,7 @@ __device__ __noinline__ void dec_finish(const DecArgs& a, float* accs, int ph, i
                 if (i < ni) acc[mat][i][nt][e] += accs[(((mat * 4 + i) * NT + nt) * 4 + e) * 32 + lane];
           continue;
         }
-        const int rs = (int)((int64_t)w * Tp / Gp);
+        const int rs = rng_at(w, Tp, Gp);
         const uint64_t* src = part_base + ((int64_t)w * 2 + (rs > sb ? 0 : 1)) * W.part_stride;
         constexpr int kI = NT == 1 ? 4 : 2;  // 16-column groups polled together (registers)
 #pragma unroll
@@ -1075,7 +1084,7 @@ struct Prod {
     const int Tp = ph == 0 ? T0 : T1;
     const int Gp = min(ph == 0 ? G - 1 : G, Tp);  // phase 1: the grid's last warp is the code warmer
     if (gw >= Gp) return;
-    const int st = (int)((int64_t)gw * Tp / Gp), en = (int)((int64_t)(gw + 1) * Tp / Gp);
+    const int st = rng_at(gw, Tp, Gp), en = rng_at(gw + 1, Tp, Gp);
     left = en - st;
     const DProb* P = probs + ph * kDecMaxProbs;
     int q = 0;
@@ -1157,7 +1166,7 @@ __device__ __forceinline__ void run_phase(const DecArgs& a, Prod<NT, NMAT1, MOE>
   const int Tp = PH == 0 ? T0 : T1;
   const int Gp = min(PH == 0 ? G - 1 : G, Tp);
   if (gw >= Gp) return;
-  const int start = (int)((int64_t)gw * Tp / Gp), end = (int)((int64_t)(gw + 1) * Tp / Gp);
+  const int start = rng_at(gw, Tp, Gp), end = rng_at(gw + 1, Tp, Gp);
   int p = 0;
   int pos = start;
   DEC_DBG(PH == 0 ? 2 : 5);

@@ -810,6 +810,11 @@ milo_status launch_decode(DecArgs a, const void* x, int32_t x_dtype, int64_t ldx
   W.bflag = W.tflag + kDecMaxBlocks * 3;
   W.hflag = W.bflag + kDecMaxBlocks;
   if (MOE && (int64_t)nb_max * (f_max / 64) > kHflagCap) return fail(MILO_ERR_CONFIG, "decode: h flag capacity");
+  {  // 32-bit stream-K range arithmetic: tiles of a phase x warps < 2^32 (decode.cuh rng_at)
+    const int64_t kmax = std::max<int64_t>(a.d, f_max), nmax = std::max<int64_t>(a.d, f_max);
+    const int64_t tiles_bound = (int64_t)nb_max * ((kmax / 32) * (nmax / 64) + (int64_t)(std::max(r16_max, 16) / 16) * 3 * (kmax / 32));
+    if (tiles_bound * G >= (int64_t)1 << 32) return fail(MILO_ERR_CONFIG, "decode: too many tiles for one launch");
+  }
   W.part_stride = part_stride;
   W.r16_max = std::max(r16_max, 16);
   W.f_max = f_max;
