@@ -624,7 +624,7 @@ __device__ __forceinline__ void topk_regs(const float* __restrict__ l, int E, in
 // Every CTA, redundantly: routing (or the given routing), the block table and
 // the per-phase problem tables in shared memory.  Ends with __syncthreads().
 template <int NT, int NMAT1, bool MOE>
-__device__ __noinline__ void dec_stage0(const DecArgs& a) {
+__device__ __forceinline__ void dec_stage0(const DecArgs& a) {
   using CF = DecCfg<NT, NMAT1>;
   constexpr int kMPad = CF::kMPad;
   extern __shared__ __align__(128) uint8_t smem[];
