@@ -812,7 +812,7 @@ __device__ __forceinline__ void dec_stage0(const DecArgs& a) {
 // warp covered the whole slab); the slab's last contributor sums all partials in
 // warp order and finishes the slab.
 template <int NT, int NMAT1, bool MOE, int NM>
-__device__ __noinline__ void dec_finish(const DecArgs& a, float* accs, int ph, int p, int s, int start,
+__device__ __forceinline__ void dec_finish(const DecArgs& a, float* accs, int ph, int p, int s, int start,
                                         int end, int Gp, int Tp, int gw, int G, bool dry) {
   using CF = DecCfg<NT, NMAT1>;
   constexpr int kMPad = CF::kMPad;
