@@ -59,7 +59,10 @@ constexpr int kDecMaxM = 64;                      // MoE decode path: m <= 64 (e
 constexpr int kDecMaxEntries = 256;               // m * K routed entries
 constexpr int kDecMaxProbs = 3 * kDecMaxBlocks;   // per phase
 constexpr int kDecKC = 8;                         // max k-tiles (32 k each) per ring slot
-constexpr int kDecSlotW = 8192;                   // weight / pseudo-tile bytes per slot
+#ifndef DEC_SLOT_BYTES
+#define DEC_SLOT_BYTES 8192
+#endif
+constexpr int kDecSlotW = DEC_SLOT_BYTES;         // weight / pseudo-tile bytes per slot
 constexpr int kPseudoInt3Bytes = 640;             // 512 B codes + 32 f32 steps
 constexpr int kPseudoRealBytes = 2048;            // hi / lo binary16 fragments
 constexpr int kVftInt3Bytes = 1024;               // per (slab, 16-rank step)
@@ -1312,6 +1315,7 @@ __global__ void __launch_bounds__(32 * DecCfg<NT, NMAT1>::kWarps, 1)
     decode_kernel(const __grid_constant__ DecArgs a) {
   using CF = DecCfg<NT, NMAT1>;
   static_assert(CF::kBytes <= 227 * 1024, "decode kernel shared memory");
+  static_assert(NMAT1 * 4 * NT * 4 * 32 * 4 <= CF::kSlotBytes, "parked accumulators must fit a ring slot");
   constexpr int kC = CF::kCons, kS = CF::kSlots;
   extern __shared__ __align__(128) uint8_t smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
