@@ -201,6 +201,9 @@ __device__ __forceinline__ void split_h2(float a, float b, uint32_t& hi, uint32_
   lo = h2_as_u32(__floats2half2_rn(a - f.x, b - f.y));
 }
 
+#ifndef DEC_WARM
+#define DEC_WARM 1  // finisher code warm-up by the grid's last warp
+#endif
 #ifndef DEC_TIMERS
 #define DEC_TIMERS 0  // per-warp cycle counters in the debug timeline (tools/dbg_timeline.py)
 #endif
@@ -1373,7 +1376,7 @@ __global__ void __launch_bounds__(32 * DecCfg<NT, NMAT1>::kWarps, 1)
   __syncwarp();
 
   PhaseState st{0, 0u, 0, 0, 0, 0, 0, 0, 0};
-  if (NT == 1 && gw == G - 1) {  // (NT = 2: the extra call sites cost the finisher registers)
+  if (DEC_WARM && NT == 1 && gw == G - 1) {  // (NT = 2: the extra call sites cost the finisher registers)
     // Code warm-up while the memory system is still idle: run the finisher
     // paths once with every side effect off, so that the real finishers at the
     // end of each phase (one per slab, all at about the same time) find this
