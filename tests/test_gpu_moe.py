@@ -207,3 +207,24 @@ def test_ep_dispatch_combine_kernels_multi_rank_layout(gpu, world, m, K):
             if slot[t * K + k] >= 0:
                 want[t] += w[t, k] * y[slot[t * K + k]]
     assert np.allclose(out, want, rtol=1e-6, atol=1e-6)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m", [1, 40, 130])
+def test_arctic_like_layer_128_experts(gpu, oracle, m):
+    """Arctic-480B-shaped routing (128 experts, top-2; reduced hidden sizes): decode
+    megakernel (m <= 64) and tcgen05 prefill path (m = 130) against the oracle."""
+    import torch
+    E, K, d, f = 128, 2, 256, 256
+    ranks = [[(0, 8, 16, 32)[(e + j) % 4] for j in range(3)] for e in range(E)]
+    o_ex, g_ex = _experts(oracle, gpu, E, d, f, ranks, seed=2100)
+    rng = np.random.default_rng(300 + m)
+    x = rng.normal(0, 1, (m, d)).astype(np.float32)
+    logits = rng.normal(0, 1, (m, E)).astype(np.float32)
+    ids, w = oracle.router_topk(logits, K, 0)
+    want = oracle.moe_forward(o_ex, [], x, ids, w)
+    layer = gpu.MoELayer(g_ex, [], top_k=K, score_mode=0)
+    out, gids, _ = layer.forward(torch.from_numpy(x).cuda(), torch.from_numpy(logits).cuda(),
+                                 return_routing=True)
+    assert (gids.cpu().numpy() == ids).all()
+    assert rel_err(out.cpu().numpy(), want) <= TOL_MOE
