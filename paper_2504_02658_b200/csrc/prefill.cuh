@@ -196,8 +196,18 @@ __device__ __forceinline__ void pf_item(const PfArgs& a, int item, int& p, int& 
 // roles: packed weights (deep, HBM latency), dequantized A, activation images.
 // Every role walks the same stage sequence: per item, k / 64 main stages then
 // 3 LoRC stages per 64-rank chunk per matrix.
+#ifndef PF_SPIN_WAITS
+#define PF_SPIN_WAITS 0  // experiments: all ring waits spin on test_wait instead of try_wait
+#endif
+__device__ __forceinline__ void ring_wait(uint64_t* bar, uint32_t parity) {
+  if (PF_SPIN_WAITS)
+    pf_wait(bar, parity);
+  else
+    mbar_wait(bar, parity);
+}
 template <int NMAT, int NG>
 __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel(const __grid_constant__ PfArgs a) {
+
   constexpr int kPfDeqGroups = PfRoles<NMAT, NG>::kGroups;
   static_assert(kPfDeqGroups <= PfCfg<NMAT, NG>::kAS, "dequant groups must not outnumber A slots");
   using CF = PfCfg<NMAT, NG>;
@@ -293,7 +303,7 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
         const PfProblem P = a.problems[p];  // by value: fields live in registers
         const int ks = P.k / kPfK, kts = P.k / kTileK;
         for (int st = 0; st < ks; ++st) {
-          mbar_wait(&p_empty[ps], pph ^ 1);
+          ring_wait(&p_empty[ps], pph ^ 1);
 
           uint8_t* sP = smem + CF::kOffP + ps * CF::kStageP;
           mbar_arrive_expect_tx(&p_full[ps], (uint32_t)CF::kStageP);
@@ -325,7 +335,7 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
         const PfProblem P = a.problems[p];  // by value: fields live in registers
         const int ks = P.k / kPfK, total = item_stages(P);
         for (int st = 0; st < total; ++st) {
-          mbar_wait(&b_empty[bs], bph ^ 1);
+          ring_wait(&b_empty[bs], bph ^ 1);
           uint8_t* sB = smem + CF::kOffB + bs * bslot;
           const uint8_t* src;
           const uint32_t ib = (uint32_t)P.ntok * 128u;  // one token-tile image
@@ -370,7 +380,7 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
           // alone would pass early when this group's first stage reuses a slot
           // whose previous phase has not completed yet); the first warp then
           // either fetches a V image into it (LoRC stage) or releases v_full
-          mbar_wait(&a_empty[as], aph ^ 1);
+          ring_wait(&a_empty[as], aph ^ 1);
           if (gw == 0 && lane == 0) {
             if (st >= ks) {
               int mat, ch, vpart, tpart;
@@ -384,9 +394,9 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
               mbar_arrive(&v_full[as]);
             }
           }
-          mbar_wait(&v_full[as], aph);
+          ring_wait(&v_full[as], aph);
           if (st < ks) {
-            mbar_wait(&p_full[ps], pph);
+            ring_wait(&p_full[ps], pph);
             if (gw == 0 && lane == 0 && item == (int)blockIdx.x) pf_trace(st, 1);
             const uint8_t* sP = smem + CF::kOffP + ps * CF::kStageP;
             constexpr int kJobs = 8 * NMAT * NG / kPfGroupWarps;
@@ -444,13 +454,13 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
         const PfProblem P = a.problems[p];  // by value: fields live in registers
         const int ks = P.k / kPfK, total = item_stages(P);
         const uint32_t idesc = pf_idesc(P.ntok);
-        mbar_wait(&acc_empty[acc], acc_phase ^ 1);
+        ring_wait(&acc_empty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d0 = tmem + (uint32_t)(acc * NG * NMAT * kPfN);
         for (int st = 0; st < total; ++st) {
-          mbar_wait(&a_full[as], aph);
+          ring_wait(&a_full[as], aph);
 
-          mbar_wait(&b_full[bs], bph);
+          ring_wait(&b_full[bs], bph);
           tc_fence_after();
           const uint32_t aA = smem_u32(smem + CF::kOffA + as * CF::kStageA);
           const uint32_t aB = smem_u32(smem + CF::kOffB + bs * bslot);
@@ -475,7 +485,7 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
           pf_commit(&b_empty[bs]);
           if ((a.flags & 32) && item == (int)blockIdx.x && st < 64) {  // debug: commit latency
             pf_trace(st, 1);
-            mbar_wait(&a_empty[as], aph);
+            ring_wait(&a_empty[as], aph);
             pf_trace(st, 3);
           }
           if (item == (int)blockIdx.x) pf_trace(st, 2);
@@ -505,7 +515,7 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
       int p, nt, tt;
       pf_item<NG>(a, item, p, nt, tt);
       const PfProblem P = a.problems[p];  // by value: fields live in registers
-      mbar_wait(&acc_full[acc], acc_phase);
+      ring_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
       if (threadIdx.x == 0) pf_dbg(6);
       // TMEM -> registers (thread = output column, 32 tokens per load) -> SwiGLU /
