@@ -199,6 +199,23 @@ milo_status milo_moe_forward_routed(milo_moe* moe, const void* x, int64_t m, int
 milo_status milo_moe_forward_host(milo_moe* moe, const float* x, int64_t m,
                                   const float* router_logits, float* out);
 
+/* ---------------------------------------------- MILO1 container loaders
+ * The reference's tensor-store container (tensor_store.cpp:96-131): "MILO1",
+ * u32 LE header length, JSON header, little-endian payload.
+ * milo_packed_load_host: a packed-i3 container (pack.cpp:306-400, validated
+ * like milo::load_packed) into a host desc; the returned handle owns the
+ * arrays the desc points to (milo_packed_host_free).  No device needed.
+ * milo_weight_load: the same, uploaded and repacked (milo_weight_create).
+ * milo_comp_load: the compensator factor pair the reference's quantize writes
+ * (<name>.u.milo / <name>.v.milo, pipeline.cpp:233-283; the reference has no
+ * reader): symm-i3 codes + binary16 scales (the writer's rounding of the
+ * float scales is kept), or f32 real factors.  Errors: MILO_ERR_IO (open),
+ * MILO_ERR_FORMAT (magic, header, dtype, payload size), MILO_ERR_SHAPE. */
+milo_status milo_packed_load_host(const char* path, milo_packed_desc* desc, void** handle);
+void milo_packed_host_free(void* handle);
+milo_status milo_weight_load(const char* path, milo_weight** out);
+milo_status milo_comp_load(const char* u_path, const char* v_path, milo_comp** out);
+
 /* Expert-parallel exchange (paper_2504_02658_b200/ep.py): fixed-capacity
  * dispatch of the m x K routed entries to `world` ranks owning `per` experts
  * each.  send_x: (world * capacity) rows of ld_send binary16 (the first d =

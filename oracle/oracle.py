@@ -208,6 +208,10 @@ class Oracle:
             self._fnv = self._f("fnv1a64", u64, [C.c_char_p])
             self._cq = self._f("comp_quantize", i, [u64, u64, u64, f32p, f32p, u64, u8p, f32p,
                                                     u8p, f32p])
+            self._save_packed = self._f("save_packed", i, [u64, u64, i, i, i, u64, u32p, u32p, u32p, u16p,
+                                                           u16p, C.c_char_p, C.c_char_p])
+            self._load_info = self._f("load_packed_info", i, [C.c_char_p, C.POINTER(u64)])
+            self._load_packed = self._f("load_packed", i, [C.c_char_p, u32p, u32p, u32p, u16p, u16p])
             self.lib.ref_last_error.restype = C.c_char_p
             self.lib.ref_moe_create.restype = C.c_void_p
             self.lib.ref_moe_create.argtypes = [i]
@@ -379,6 +383,30 @@ class Oracle:
         zh = np.zeros(k * n // 64, np.uint16) if mode == 1 else None
         self._check(self._rp(k, n, mode, seed, _p(words, u32p), _p(sh, u16p), _p(zh, u16p)))
         return Packed(k, n, 0, False, mode, 64, words, None, None, sh, zh)
+
+    def save_packed(self, P: Packed, name: str, path: str):
+        """milo::save_packed (pack.cpp:306-343): the reference's packed-i3 MILO1 writer."""
+        assert self.which == "ref"
+        self._check(self._save_packed(P.rows, P.cols, P.layout, int(P.split), P.mode, P.group_size,
+                                      _p(P.words, u32p), _p(P.plane_a, u32p), _p(P.plane_b, u32p),
+                                      _p(P.scales, u16p), _p(P.zeros, u16p), name.encode(), str(path).encode()))
+
+    def load_packed(self, path: str) -> Packed:
+        """milo::load_packed (pack.cpp:345-400)."""
+        assert self.which == "ref"
+        info = (C.c_uint64 * 6)()
+        self._check(self._load_info(str(path).encode(), info))
+        rows, cols, layout, split, mode, gs = (int(v) for v in info)
+        groups = rows * cols // 32
+        qg = rows * cols // gs
+        words = None if split else np.zeros(groups * 3, np.uint32)
+        pa = np.zeros(groups * 2, np.uint32) if split else None
+        pb = np.zeros(groups, np.uint32) if split else None
+        sh = np.zeros(qg, np.uint16)
+        zh = np.zeros(qg, np.uint16) if mode == 1 else None
+        self._check(self._load_packed(str(path).encode(), _p(words, u32p), _p(pa, u32p), _p(pb, u32p),
+                                      _p(sh, u16p), _p(zh, u16p)))
+        return Packed(rows, cols, layout, bool(split), mode, gs, words, pa, pb, sh, zh)
 
     def fill_normal(self, seed, count, mean=0.0, sigma=1.0) -> np.ndarray:
         assert self.which == "ref"

@@ -219,6 +219,44 @@ int ref_unpack_codes(std::uint64_t rows, std::uint64_t cols, int layout, int spl
   });
 }
 
+// The reference's own packed-i3 container writer / reader (pack.cpp:306-400):
+// test fixtures for milo_weight_load come from save_packed, and load_packed is
+// the parity reference for the B200 library's reader.
+int ref_save_packed(std::uint64_t rows, std::uint64_t cols, int layout, int split, int mode,
+                    std::uint64_t group_size, const std::uint32_t* words,
+                    const std::uint32_t* plane_a, const std::uint32_t* plane_b,
+                    const std::uint16_t* scales, const std::uint16_t* zeros, const char* name,
+                    const char* path) {
+  return guarded([&] {
+    PackedInt3Matrix p = make_packed(rows, cols, layout, split, mode, group_size, words, plane_a,
+                                     plane_b, scales, zeros);
+    save_packed(p, name, path);
+  });
+}
+
+// Header fields of a packed-i3 container (load_packed); out6 = rows, cols, layout,
+// split, mode, group_size.
+int ref_load_packed_info(const char* path, std::uint64_t* out6) {
+  return guarded([&] {
+    PackedInt3Matrix p = load_packed(path);
+    out6[0] = p.rows;
+    out6[1] = p.cols;
+    out6[2] = p.layout == PackLayout::Linear ? 0 : 1;
+    out6[3] = p.split ? 1 : 0;
+    out6[4] = p.mode == DequantMode::Symmetric ? 0 : 1;
+    out6[5] = p.group_size;
+  });
+}
+
+// Payload of a packed-i3 container (load_packed) into caller buffers sized from the info.
+int ref_load_packed(const char* path, std::uint32_t* words, std::uint32_t* plane_a,
+                    std::uint32_t* plane_b, std::uint16_t* scales, std::uint16_t* zeros) {
+  return guarded([&] {
+    PackedInt3Matrix p = load_packed(path);
+    export_packed(p, words, plane_a, plane_b, scales, zeros);
+  });
+}
+
 int ref_dequant_packed_half(std::uint64_t rows, std::uint64_t cols, int layout, int split,
                             int mode, std::uint64_t group_size, const std::uint32_t* words,
                             const std::uint32_t* plane_a, const std::uint32_t* plane_b,

@@ -137,6 +137,9 @@ def lib() -> C.CDLL:
         "milo_moe_forward": [vp, vp, i64, i32, vp, vp, i32, vp, vp, vp],
         "milo_moe_forward_routed": [vp, vp, i64, i32, vp, vp, vp, i32, vp],
         "milo_moe_forward_host": [vp, f32p, i64, f32p, f32p],
+        "milo_packed_load_host": [C.c_char_p, C.POINTER(_PackedDesc), C.POINTER(vp)],
+        "milo_weight_load": [C.c_char_p, C.POINTER(vp)],
+        "milo_comp_load": [C.c_char_p, C.c_char_p, C.POINTER(vp)],
         "milo_ep_dispatch": [vp, i64, i32, i32, i32, i32, vp, i32, i64, vp, i64, vp, vp, vp],
         "milo_ep_combine": [vp, vp, vp, i64, i32, i64, vp, vp],
     }
@@ -239,8 +242,38 @@ def _c32(a, dt):
     return None if a is None else np.ascontiguousarray(a, dtype=dt).ravel()
 
 
+def load_packed_host(path: str) -> PackedInt3Matrix:
+    """Reads a packed-i3 MILO1 container (milo::load_packed, pack.cpp:345-400) on
+    the host: the library's C++ reader, no device needed."""
+    d = _PackedDesc()
+    h = vp()
+    _check(lib().milo_packed_load_host(str(path).encode(), C.byref(d), C.byref(h)))
+    try:
+        def arr(ptr, n, dt):
+            return None if not ptr or n == 0 else np.ctypeslib.as_array(ptr, shape=(n,)).astype(dt, copy=True)
+        return PackedInt3Matrix(int(d.rows), int(d.cols), int(d.layout), bool(d.split), int(d.mode),
+                                int(d.group_size), arr(d.words, d.n_words, np.uint32),
+                                arr(d.plane_a, d.n_plane_a, np.uint32), arr(d.plane_b, d.n_plane_b, np.uint32),
+                                arr(d.scales, d.n_scales, np.uint16), arr(d.zeros, d.n_zeros, np.uint16))
+    finally:
+        lib().milo_packed_host_free(h)
+
+
 class Weight:
     """Device-resident packed INT3 weight (milo_weight handle), repacked once."""
+
+    @classmethod
+    def load(cls, path: str) -> "Weight":
+        """From a packed-i3 MILO1 container written by the reference's save_packed."""
+        self = cls.__new__(cls)
+        h = vp()
+        _check(lib().milo_weight_load(str(path).encode(), C.byref(h)))
+        self._h = h
+        self._keep = None
+        rows, cols, mode = C.c_uint64(), C.c_uint64(), C.c_int32()
+        _check(lib().milo_weight_info(h, C.byref(rows), C.byref(cols), C.byref(mode), None))
+        self.rows, self.cols, self.mode = rows.value, cols.value, mode.value
+        return self
 
     def __init__(self, p):
         self._keep = [_c32(p.words, np.uint32), _c32(p.plane_a, np.uint32),
@@ -291,6 +324,16 @@ class Weight:
 
 class Comp:
     """Device-resident compensator (milo_comp handle)."""
+
+    @classmethod
+    def load(cls, u_path: str, v_path: str) -> "Comp":
+        """From the factor pair the reference's quantize writes (<name>.u.milo / .v.milo)."""
+        self = cls.__new__(cls)
+        h = vp()
+        _check(lib().milo_comp_load(str(u_path).encode(), str(v_path).encode(), C.byref(h)))
+        self._h = h
+        self.rows = self.cols = self.rank = None
+        return self
 
     def __init__(self, c):
         keep = dict(U=_c32(c.U, np.float32), V=_c32(c.V, np.float32),

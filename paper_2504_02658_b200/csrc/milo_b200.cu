@@ -8,6 +8,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <array>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <string>
@@ -1886,3 +1887,357 @@ extern "C" milo_status milo_moe_forward_host(milo_moe* moe, const float* x, int6
   if (st == MILO_OK) std::memcpy(out, hs + xb + lb16, xb);
   return st;
 }
+
+// ===========================================================================
+// MILO1 container loaders.  Format of the
+// reference's tensor store (tensor_store.cpp:96-131): 5 magic bytes "MILO1",
+// u32 LE header length, a JSON header, a little-endian payload.
+//  * packed-i3 (pack.cpp:306-400): words (or plane A then plane B) as u32,
+//    binary16 scales, binary16 zeros (asymmetric only); validated like
+//    load_packed (dtype, names, exact payload size).
+//  * compensator factors written by quantize (pipeline.cpp:233-283; the
+//    reference has no reader): symm-i3 = u8 codes + binary16 scales per
+//    (row, 64-group), U (k x r) and V^T (n x r, "transposed"); real = f32 U
+//    (k x r) and V (r x n).
+// ===========================================================================
+namespace {
+
+// Flat JSON object (strings, integers, booleans); nested values are skipped.
+struct JsonFlat {
+  std::map<std::string, std::string> str;
+  std::map<std::string, long long> num;
+  std::map<std::string, bool> boolean;
+};
+
+bool json_flat_parse(const std::string& t, JsonFlat& out) {
+  size_t i = 0;
+  auto ws = [&] {
+    while (i < t.size() && (t[i] == ' ' || t[i] == '\n' || t[i] == '\t' || t[i] == '\r')) ++i;
+  };
+  auto str = [&](std::string& s) -> bool {
+    if (i >= t.size() || t[i] != '"') return false;
+    ++i;
+    s.clear();
+    while (i < t.size() && t[i] != '"') {
+      if (t[i] == '\\' && i + 1 < t.size()) {
+        ++i;
+        s.push_back(t[i] == 'n' ? '\n' : t[i] == 't' ? '\t' : t[i]);
+      } else {
+        s.push_back(t[i]);
+      }
+      ++i;
+    }
+    if (i >= t.size()) return false;
+    ++i;
+    return true;
+  };
+  std::function<bool()> skip_value = [&]() -> bool {  // nested objects / arrays
+    ws();
+    if (i >= t.size()) return false;
+    if (t[i] == '"') {
+      std::string s;
+      return str(s);
+    }
+    if (t[i] == '{' || t[i] == '[') {
+      const char close = t[i] == '{' ? '}' : ']';
+      ++i;
+      ws();
+      if (i < t.size() && t[i] == close) {
+        ++i;
+        return true;
+      }
+      for (;;) {
+        if (close == '}') {
+          ws();
+          std::string k;
+          if (!str(k)) return false;
+          ws();
+          if (i >= t.size() || t[i] != ':') return false;
+          ++i;
+        }
+        if (!skip_value()) return false;
+        ws();
+        if (i < t.size() && t[i] == ',') {
+          ++i;
+          continue;
+        }
+        if (i < t.size() && t[i] == close) {
+          ++i;
+          return true;
+        }
+        return false;
+      }
+    }
+    while (i < t.size() && t[i] != ',' && t[i] != '}' && t[i] != ']') ++i;
+    return true;
+  };
+  ws();
+  if (i >= t.size() || t[i] != '{') return false;
+  ++i;
+  ws();
+  if (i < t.size() && t[i] == '}') return true;
+  for (;;) {
+    ws();
+    std::string key;
+    if (!str(key)) return false;
+    ws();
+    if (i >= t.size() || t[i] != ':') return false;
+    ++i;
+    ws();
+    if (i >= t.size()) return false;
+    if (t[i] == '"') {
+      std::string v;
+      if (!str(v)) return false;
+      out.str[key] = v;
+    } else if (t.compare(i, 4, "true") == 0) {
+      out.boolean[key] = true;
+      i += 4;
+    } else if (t.compare(i, 5, "false") == 0) {
+      out.boolean[key] = false;
+      i += 5;
+    } else if (t[i] == '-' || (t[i] >= '0' && t[i] <= '9')) {
+      size_t j = i;
+      while (j < t.size() && (t[j] == '-' || t[j] == '+' || t[j] == '.' || t[j] == 'e' || t[j] == 'E' ||
+                              (t[j] >= '0' && t[j] <= '9')))
+        ++j;
+      out.num[key] = std::atoll(t.substr(i, j - i).c_str());
+      i = j;
+    } else if (!skip_value()) {
+      return false;
+    }
+    ws();
+    if (i < t.size() && t[i] == ',') {
+      ++i;
+      continue;
+    }
+    if (i < t.size() && t[i] == '}') return true;
+    return false;
+  }
+}
+
+milo_status read_container(const char* path, JsonFlat& h, std::vector<uint8_t>& payload) {
+  FILE* f = path ? std::fopen(path, "rb") : nullptr;
+  if (!f) return fail(MILO_ERR_IO, "cannot open '%s' for reading", path ? path : "(null)");
+  std::vector<uint8_t> all;
+  uint8_t buf[1 << 16];
+  size_t n;
+  while ((n = std::fread(buf, 1, sizeof(buf), f)) > 0) all.insert(all.end(), buf, buf + n);
+  std::fclose(f);
+  if (all.size() < 5 || std::memcmp(all.data(), "MILO1", 5) != 0)
+    return fail(MILO_ERR_FORMAT, "'%s': bad magic, not a MILO1 container", path);
+  if (all.size() < 9) return fail(MILO_ERR_FORMAT, "container truncated while reading header length");
+  const uint32_t hlen = (uint32_t)all[5] | ((uint32_t)all[6] << 8) | ((uint32_t)all[7] << 16) | ((uint32_t)all[8] << 24);
+  if (all.size() < 9 + (size_t)hlen) return fail(MILO_ERR_FORMAT, "'%s': truncated header", path);
+  const std::string header(reinterpret_cast<const char*>(all.data() + 9), hlen);
+  if (!json_flat_parse(header, h)) return fail(MILO_ERR_FORMAT, "'%s': bad container header", path);
+  payload.assign(all.begin() + 9 + hlen, all.end());
+  return MILO_OK;
+}
+
+bool json_get(const JsonFlat& h, const char* k, long long& v) {
+  auto it = h.num.find(k);
+  if (it == h.num.end()) return false;
+  v = it->second;
+  return true;
+}
+
+float host_half_to_float(uint16_t h) {
+  const uint32_t s = (uint32_t)(h >> 15) << 31, e = (h >> 10) & 31, m = h & 1023;
+  uint32_t bits;
+  if (e == 0) {
+    if (m == 0) {
+      bits = s;
+    } else {  // subnormal
+      int ee = -1;
+      uint32_t mm = m;
+      do {
+        ++ee;
+        mm <<= 1;
+      } while (!(mm & 1024));
+      bits = s | ((uint32_t)(127 - 15 - ee) << 23) | ((mm & 1023) << 13);
+    }
+  } else if (e == 31) {
+    bits = s | 0x7F800000u | (m << 13);
+  } else {
+    bits = s | ((e + 127 - 15) << 23) | (m << 13);
+  }
+  float f;
+  std::memcpy(&f, &bits, 4);
+  return f;
+}
+
+// Owned host copy of a loaded packed-i3 container behind a milo_packed_desc.
+struct PackedHost {
+  milo_packed_desc d{};
+  std::vector<uint32_t> words, pa, pb;
+  std::vector<uint16_t> scales, zeros;
+};
+
+milo_status load_packed_host(const char* path, PackedHost& P) {
+  JsonFlat h;
+  std::vector<uint8_t> pl;
+  milo_status st = read_container(path, h, pl);
+  if (st != MILO_OK) return st;
+  auto dt = h.str.find("dtype");
+  if (dt == h.str.end() || dt->second != "packed-i3") return fail(MILO_ERR_FORMAT, "'%s': dtype is not packed-i3", path);
+  long long rows, cols, gs;
+  auto lay = h.str.find("layout");
+  auto mode = h.str.find("mode");
+  auto split = h.boolean.find("split");
+  if (!json_get(h, "rows", rows) || !json_get(h, "cols", cols) || !json_get(h, "group_size", gs) ||
+      lay == h.str.end() || mode == h.str.end() || split == h.boolean.end())
+    return fail(MILO_ERR_FORMAT, "'%s': bad container header", path);
+  int layout;
+  if (lay->second == "linear") layout = MILO_LAYOUT_LINEAR;
+  else if (lay->second == "tiled16x64") layout = MILO_LAYOUT_TILED16X64;
+  else return fail(MILO_ERR_FORMAT, "unknown pack layout '%s'", lay->second.c_str());
+  int md;
+  if (mode->second == "symmetric") md = MILO_MODE_SYMMETRIC;
+  else if (mode->second == "asymmetric") md = MILO_MODE_ASYMMETRIC;
+  else return fail(MILO_ERR_FORMAT, "unknown dequant mode '%s'", mode->second.c_str());
+  if (rows <= 0 || cols <= 0 || gs <= 0 || (rows * cols) % 32 != 0 || (rows * cols) % gs != 0)
+    return fail(MILO_ERR_FORMAT, "'%s': inconsistent shape in header", path);
+  const size_t groups = (size_t)(rows * cols / 32), nw = groups * 3, qg = (size_t)(rows * cols / gs);
+  const size_t expect = nw * 4 + qg * 2 + (md == MILO_MODE_ASYMMETRIC ? qg * 2 : 0);
+  if (pl.size() != expect)
+    return fail(MILO_ERR_FORMAT, "'%s': payload is %zu bytes, expected %zu", path, pl.size(), expect);
+  const uint8_t* p = pl.data();
+  const bool sp = split->second;
+  if (sp) {
+    P.pa.resize(groups * 2);
+    P.pb.resize(groups);
+    std::memcpy(P.pa.data(), p, groups * 8);
+    std::memcpy(P.pb.data(), p + groups * 8, groups * 4);
+  } else {
+    P.words.resize(nw);
+    std::memcpy(P.words.data(), p, nw * 4);
+  }
+  p += nw * 4;
+  P.scales.resize(qg);
+  std::memcpy(P.scales.data(), p, qg * 2);
+  p += qg * 2;
+  if (md == MILO_MODE_ASYMMETRIC) {
+    P.zeros.resize(qg);
+    std::memcpy(P.zeros.data(), p, qg * 2);
+  }
+  milo_packed_desc& d = P.d;
+  d.rows = (uint64_t)rows;
+  d.cols = (uint64_t)cols;
+  d.layout = layout;
+  d.split = sp ? 1 : 0;
+  d.mode = md;
+  d.group_size = (uint64_t)gs;
+  d.words = P.words.empty() ? nullptr : P.words.data();
+  d.n_words = P.words.size();
+  d.plane_a = P.pa.empty() ? nullptr : P.pa.data();
+  d.n_plane_a = P.pa.size();
+  d.plane_b = P.pb.empty() ? nullptr : P.pb.data();
+  d.n_plane_b = P.pb.size();
+  d.scales = P.scales.data();
+  d.n_scales = P.scales.size();
+  d.zeros = P.zeros.empty() ? nullptr : P.zeros.data();
+  d.n_zeros = P.zeros.size();
+  return MILO_OK;
+}
+
+struct FactorHost {
+  long long rows = 0, cols = 0, rank = 0, gs = 64;
+  bool transposed = false, real = false;
+  std::vector<uint8_t> codes;
+  std::vector<float> scales, values;
+};
+
+milo_status load_factor(const char* path, FactorHost& F) {
+  JsonFlat h;
+  std::vector<uint8_t> pl;
+  milo_status st = read_container(path, h, pl);
+  if (st != MILO_OK) return st;
+  auto dt = h.str.find("dtype");
+  if (dt == h.str.end() || !json_get(h, "rows", F.rows) || !json_get(h, "cols", F.cols) ||
+      !json_get(h, "rank", F.rank) || F.rows <= 0 || F.cols <= 0 || F.rank < 0)
+    return fail(MILO_ERR_FORMAT, "'%s': bad compensator header", path);
+  if (dt->second == "symm-i3") {
+    if (!json_get(h, "group_size", F.gs) || F.gs <= 0) return fail(MILO_ERR_FORMAT, "'%s': bad group_size", path);
+    auto tr = h.boolean.find("transposed");
+    F.transposed = tr != h.boolean.end() && tr->second;
+    const size_t n = (size_t)(F.rows * F.cols), gpr = (size_t)((F.cols + F.gs - 1) / F.gs);
+    if (pl.size() != n + (size_t)F.rows * gpr * 2)
+      return fail(MILO_ERR_FORMAT, "'%s': payload is %zu bytes, expected %zu", path, pl.size(), n + (size_t)F.rows * gpr * 2);
+    F.codes.assign(pl.begin(), pl.begin() + n);
+    F.scales.resize((size_t)F.rows * gpr);
+    for (size_t i = 0; i < F.scales.size(); ++i)
+      F.scales[i] = host_half_to_float((uint16_t)(pl[n + 2 * i] | (pl[n + 2 * i + 1] << 8)));
+  } else if (dt->second == "f32") {
+    F.real = true;
+    const size_t n = (size_t)(F.rows * F.cols);
+    if (pl.size() != n * 4) return fail(MILO_ERR_FORMAT, "'%s': payload is %zu bytes, expected %zu", path, pl.size(), n * 4);
+    F.values.resize(n);
+    std::memcpy(F.values.data(), pl.data(), n * 4);
+  } else {
+    return fail(MILO_ERR_FORMAT, "'%s': dtype '%s' is not a compensator factor", path, dt->second.c_str());
+  }
+  return MILO_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+milo_status milo_packed_load_host(const char* path, milo_packed_desc* desc, void** handle) {
+  if (!desc || !handle) return fail(MILO_ERR_ARGUMENT, "null argument");
+  *handle = nullptr;
+  PackedHost* P = new PackedHost();
+  milo_status st = load_packed_host(path, *P);
+  if (st != MILO_OK) {
+    delete P;
+    return st;
+  }
+  *desc = P->d;
+  *handle = P;
+  return MILO_OK;
+}
+
+void milo_packed_host_free(void* handle) { delete static_cast<PackedHost*>(handle); }
+
+milo_status milo_weight_load(const char* path, milo_weight** out) {
+  if (!out) return fail(MILO_ERR_ARGUMENT, "null argument");
+  *out = nullptr;
+  PackedHost P;
+  milo_status st = load_packed_host(path, P);
+  if (st != MILO_OK) return st;
+  return milo_weight_create(&P.d, out);
+}
+
+milo_status milo_comp_load(const char* u_path, const char* v_path, milo_comp** out) {
+  if (!out) return fail(MILO_ERR_ARGUMENT, "null argument");
+  *out = nullptr;
+  FactorHost U, V;
+  milo_status st = load_factor(u_path, U);
+  if (st == MILO_OK) st = load_factor(v_path, V);
+  if (st != MILO_OK) return st;
+  if (U.real != V.real || U.rank != V.rank) return fail(MILO_ERR_FORMAT, "compensator factors disagree (storage / rank)");
+  milo_comp_desc d{};
+  d.rank = (uint64_t)U.rank;
+  if (U.real) {  // U: k x r, V: r x n
+    if (U.cols != U.rank || V.rows != V.rank) return fail(MILO_ERR_SHAPE, "compensator factor shapes do not match the rank");
+    d.rows = (uint64_t)U.rows;
+    d.cols = (uint64_t)V.cols;
+    d.storage = MILO_COMP_REAL;
+    d.U = U.values.data();
+    d.V = V.values.data();
+  } else {  // qU: k x r, qVt: n x r (transposed)
+    if (U.cols != U.rank || V.cols != V.rank || !V.transposed || U.gs != V.gs)
+      return fail(MILO_ERR_SHAPE, "symm-i3 compensator factor shapes do not match the rank");
+    d.rows = (uint64_t)U.rows;
+    d.cols = (uint64_t)V.rows;
+    d.storage = MILO_COMP_SYMM_INT3;
+    d.qu_codes = U.codes.data();
+    d.qu_scales = U.scales.data();
+    d.qvt_codes = V.codes.data();
+    d.qvt_scales = V.scales.data();
+    d.group_size = (uint64_t)U.gs;
+  }
+  return milo_comp_create(&d, out);
+}
+
+}  // extern "C"
