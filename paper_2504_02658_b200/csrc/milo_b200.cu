@@ -8,6 +8,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <array>
+#include <chrono>
 #include <functional>
 #include <map>
 #include <mutex>
@@ -90,6 +91,52 @@ cudaError_t set_smem_min_carveout(K kernel, int bytes) {
   if (e != cudaSuccess) return e;
   const int pct = (int)(((int64_t)bytes + 2048) * 100 / (228 * 1024)) + 1;
   return cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, pct > 100 ? 100 : pct);
+}
+
+// Host -> device uploads of per-call tables go through a per-thread pinned
+// staging buffer: a cudaMemcpyAsync from pageable memory is a synchronous staged
+// copy (~5-10 us each; a MoE prefill call issues ~10 of them while the GPU idles).
+// pin_begin() at the start of a launch sequence waits for the previous sequence's
+// copies (event), pin_end() records that event.
+struct PinStage {
+  uint8_t* base = nullptr;
+  size_t cap = 0, off = 0;
+  cudaEvent_t ev = nullptr;
+  bool pending = false;
+};
+thread_local PinStage g_pin;
+void pin_begin() {
+  if (g_pin.pending) {
+    cudaEventSynchronize(g_pin.ev);
+    g_pin.pending = false;
+  }
+  g_pin.off = 0;
+}
+void pin_end(cudaStream_t s) {
+  if (!g_pin.ev) cudaEventCreateWithFlags(&g_pin.ev, cudaEventDisableTiming);
+  cudaEventRecord(g_pin.ev, s);
+  g_pin.pending = true;
+}
+cudaError_t h2d_async(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  if (!bytes || !src) return cudaSuccess;
+  const size_t need = g_pin.off + ((bytes + 255) & ~size_t(255));
+  if (need > g_pin.cap) {  // grow (rare): nothing of this sequence may still read the old buffer
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return e;
+    if (g_pin.base) cudaFreeHost(g_pin.base);
+    g_pin.cap = std::max<size_t>({need, 2 * g_pin.cap, (size_t)1 << 20});
+    e = cudaMallocHost(&g_pin.base, g_pin.cap);
+    if (e != cudaSuccess) {
+      g_pin.base = nullptr;
+      g_pin.cap = 0;
+      return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s);
+    }
+    g_pin.off = 0;
+  }
+  uint8_t* p = g_pin.base + g_pin.off;
+  std::memcpy(p, src, bytes);
+  g_pin.off += (bytes + 255) & ~size_t(255);
+  return cudaMemcpyAsync(dst, p, bytes, cudaMemcpyHostToDevice, s);
 }
 
 // Launch with programmatic dependent launch allowed (the kernel itself calls
@@ -938,10 +985,10 @@ struct ImgTPlan {
       configured_dev = dev;
     }
     const size_t jb = (jobs.size() * sizeof(ImgJob) + 255) & ~size_t(255);
-    cudaError_t e = cudaMemcpyAsync(table, jobs.data(), jobs.size() * sizeof(ImgJob), cudaMemcpyHostToDevice, stream);
+    cudaError_t e = h2d_async(table, jobs.data(), jobs.size() * sizeof(ImgJob), stream);
     if (e != cudaSuccess) return e;
     if (!tps.empty()) {
-      e = cudaMemcpyAsync(table + jb, tps.data(), tps.size() * sizeof(TProb), cudaMemcpyHostToDevice, stream);
+      e = h2d_async(table + jb, tps.data(), tps.size() * sizeof(TProb), stream);
       if (e != cudaSuccess) return e;
     }
     e = launch(pf_img_t_kernel, dim3((unsigned)blocks), dim3(256), kImgTSmem, stream, false,
@@ -956,7 +1003,7 @@ struct ImgTPlan {
 // reduction) + pf_t_images_kernel; `table` holds the TProb array (device).
 cudaError_t launch_t_batch(const std::vector<TProb>& v, int units, uint8_t* table, cudaStream_t stream) {
   if (v.empty()) return cudaSuccess;
-  cudaError_t e = cudaMemcpyAsync(table, v.data(), v.size() * sizeof(TProb), cudaMemcpyHostToDevice, stream);
+  cudaError_t e = h2d_async(table, v.data(), v.size() * sizeof(TProb), stream);
   if (e != cudaSuccess) return e;
   e = launch(pf_t_kernel, dim3(units), dim3(256), 0, stream, false, (const TProb*)table, (int)v.size());
   if (e != cudaSuccess) return e;
@@ -1018,9 +1065,8 @@ milo_status launch_prefill_ng(const PfProblem* host_probs, int n_probs, cudaStre
   }
   // problem table + starts travel in the scratch buffer (stream-ordered upload)
   const size_t pb = (size_t)n_probs * sizeof(PfProblem);
-  CUDA_TRY(cudaMemcpyAsync(scratch, host_probs, pb, cudaMemcpyHostToDevice, stream));
-  CUDA_TRY(cudaMemcpyAsync(scratch + ((pb + 255) & ~size_t(255)), starts.data(), starts.size() * 4,
-                           cudaMemcpyHostToDevice, stream));
+  CUDA_TRY(h2d_async(scratch, host_probs, pb, stream));
+  CUDA_TRY(h2d_async(scratch + ((pb + 255) & ~size_t(255)), starts.data(), starts.size() * 4, stream));
   PfArgs a{};
   a.ntok_max = ntok_max;
   a.dbg = g_dbg;
@@ -1106,11 +1152,13 @@ extern "C" milo_status milo_gemm_w3a16(const milo_weight* w, const milo_comp* co
     float* tpart = reinterpret_cast<float*>(img + img_b + t_img_b);
     ImgTPlan plan;
     const milo_comp* cs[1] = {comp};
+    pin_begin();
     plan.add(A, a_dtype, a_cols, nullptr, m, k, ntok, img, cs, &timg, &tpart, 1);
     cudaError_t e = plan.launch_all(img + img_b + t_img_b + t_part_b + 8192, stream);
     if (e == cudaSuccess && lorc) e = launch_t(A, a_dtype, a_cols, nullptr, m, k, ntok, comp, timg, tpart,
                                                img + img_b + t_img_b + t_part_b + 12288, props.sms, stream);
     if (e != cudaSuccess) {
+      pin_end(stream);
       cudaFreeAsync(mem, stream);
       return fail(MILO_ERR_CUDA, "launch failed: %s", cudaGetErrorString(e));
     }
@@ -1132,6 +1180,7 @@ extern "C" milo_status milo_gemm_w3a16(const milo_weight* w, const milo_comp* co
       P.rchunks[0] = comp->rch;
     }
     st = launch_prefill<1>(&P, 1, stream, props.sms, img + img_b + t_img_b + t_part_b);
+    pin_end(stream);
     cudaFreeAsync(mem, stream);
     return st;
   }
@@ -1521,16 +1570,35 @@ milo_status moe_prefill(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype
                         int32_t* ids, float* wts, void* out, int32_t out_dtype, cudaStream_t stream, int sms) {
   const int E = moe->E, K = moe->K, S = moe->n_shared;
   const int64_t d = moe->d;
+  static const bool host_prof = getenv("MILO_HOST_PROF") != nullptr;  // experiments: host phase times
+  auto hnow = [] { return std::chrono::steady_clock::now(); };
+  const auto h0 = hnow();
+  auto hmark = [&](const char* what) {
+    if (host_prof)
+      std::fprintf(stderr, "moe_prefill host %-12s %8.1f us\n", what,
+                   std::chrono::duration<double, std::micro>(hnow() - h0).count());
+  };
   if (K > 0 && logits) {
     CUDA_TRY(launch(router_topk_kernel, dim3((unsigned)((m + 7) / 8)), dim3(256), 0, stream, false, logits, m, E,
                     K, moe->score_mode, ids, wts));
   }
   // ---- plan on the host (the reference composition order)
   std::vector<int32_t> hids((size_t)m * std::max(K, 1));
-  if (K > 0) {
-    CUDA_TRY(cudaMemcpyAsync(hids.data(), ids, hids.size() * 4, cudaMemcpyDeviceToHost, stream));
+  if (K > 0) {  // routing ids to the host through a pinned buffer (a pageable D2H is a staged copy)
+    static thread_local int32_t* pin_ids = nullptr;
+    static thread_local size_t pin_ids_n = 0;
+    if (pin_ids_n < hids.size()) {
+      if (pin_ids) cudaFreeHost(pin_ids);
+      pin_ids = nullptr;
+      pin_ids_n = 0;
+      CUDA_TRY(cudaMallocHost(&pin_ids, std::max<size_t>(hids.size(), 4096) * 4));
+      pin_ids_n = std::max<size_t>(hids.size(), 4096);
+    }
+    CUDA_TRY(cudaMemcpyAsync(pin_ids, ids, hids.size() * 4, cudaMemcpyDeviceToHost, stream));
     CUDA_TRY(cudaStreamSynchronize(stream));
+    std::memcpy(hids.data(), pin_ids, hids.size() * 4);
   }
+  hmark("ids synced");
   struct Grp { int e; int64_t off, rows; };
   std::vector<Grp> groups;
   std::vector<int32_t> tok, slot;  // per grouped row: x row, Y slot
@@ -1598,13 +1666,15 @@ milo_status moe_prefill(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype
   auto guard = [&](cudaError_t e) {
     if (e != cudaSuccess && st == MILO_OK) st = fail(MILO_ERR_CUDA, "prefill: %s", cudaGetErrorString(e));
   };
-  guard(cudaMemcpyAsync(dtok, tok.data(), (size_t)R * 4, cudaMemcpyHostToDevice, stream));
-  guard(cudaMemcpyAsync(dslot, slot.data(), (size_t)R * 4, cudaMemcpyHostToDevice, stream));
+  hmark("planned+alloc");
+  pin_begin();
+  guard(h2d_async(dtok, tok.data(), (size_t)R * 4, stream));
+  guard(h2d_async(dslot, slot.data(), (size_t)R * 4, stream));
   size_t tab_off = 0;
   auto upload = [&](const void* src, size_t bytes) -> uint8_t* {
     uint8_t* dst = tab + tab_off;
     tab_off = (tab_off + bytes + 255) & ~size_t(255);
-    if (bytes && src) guard(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream));
+    if (bytes && src) guard(h2d_async(dst, src, bytes, stream));
     return dst;
   };
   const int n_tprob[2] = {1, 1};  // k splits sized per problem (several CTAs per SM stay resident)
@@ -1651,6 +1721,7 @@ milo_status moe_prefill(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype
   };
   // ---- phase 1: x rows -> images, t1, t3; w1|w3 + LoRC + SwiGLU -> h
   img_t_phase(0);
+  hmark("phase1 imgs");
   {
     std::vector<PfProblem> pv;
     for (size_t gi = 0; gi < groups.size(); ++gi) {
@@ -1719,6 +1790,7 @@ milo_status moe_prefill(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype
     guard(launch(moe_combine_kernel, dim3(grid), dim3(256), 0, stream, false, (const float*)Y,
                  (const int32_t*)ids, (const float*)wts, m, K, S, d, out, out_dtype));
   }
+  pin_end(stream);
   cudaFreeAsync(mem, stream);
   return st;
 }
