@@ -204,6 +204,9 @@ __device__ __forceinline__ void split_h2(float a, float b, uint32_t& hi, uint32_
 #ifndef DEC_WARM
 #define DEC_WARM 1  // finisher code warm-up by the grid's last warp
 #endif
+#ifndef DEC_FIN_LOW
+#define DEC_FIN_LOW 1  // slab finisher: 1 = lowest contributor (its piece ends its range, 2 segments)
+#endif
 #ifndef DEC_TIMERS
 #define DEC_TIMERS 0  // per-warp cycle counters in the debug timeline (tools/dbg_timeline.py)
 #endif
@@ -853,13 +856,14 @@ __device__ __forceinline__ void dec_finish(const DecArgs& a, float* accs, int ph
   const int sb = P.t0 + s * P.ktiles, se = sb + P.ktiles;
   uint64_t* part_base = W.part + (int64_t)ph * G * 2 * W.part_stride;
   if (dry || !(start <= sb && end >= se)) {  // not the sole contributor
-    // The slab's finisher is fixed: the highest contributor whose range ENDS in
-    // the slab (its piece is its last work of the phase, so it is the latest
-    // to arrive; the contributor after it only holds the slab's first piece of
-    // its own range).  The others publish tagged partials and move on.
+    // The slab's finisher is fixed: the lowest contributor (its piece of the
+    // slab ends its range and it usually has two segments, so it arrives last;
+    // the others' pieces are their whole range or the first segment of theirs,
+    // which never wait on anything -- no cycles).  The others publish tagged
+    // partials and move on.
     int w0 = rng_owner(sb, Tp, Gp), w1 = rng_owner(se - 1, Tp, Gp);
     const int w1end = rng_at(w1 + 1, Tp, Gp);
-    int fin = (w1end <= se || w1 == w0) ? w1 : w1 - 1;
+    int fin = DEC_FIN_LOW ? w0 : ((w1end <= se || w1 == w0) ? w1 : w1 - 1);
     if (dry) {  // code warm-up: the finisher path with one (pretend-ready) other contributor
       w0 = gw - 1;
       w1 = fin = gw;
