@@ -967,10 +967,10 @@ struct ImgTPlan {
     if (!c || c->rank == 0) return 0;
     return (size_t)std::max<int64_t>(k / kPfK, t_splits(rows, k, c, sms)) * rows * c->rch * 64 * 4;
   }
-  // k splits of pf_t_kernel: about one wave of CTAs over all `nprob` problems
+  // k splits of pf_t_kernel: about kTCtasPerSm CTAs per SM over all `nprob` problems
   static int t_splits(int64_t rows, int64_t k, const milo_comp* c, int sms, int nprob = 1) {
     const int row_tiles = (int)((rows + kTRows - 1) / kTRows);
-    return std::max(1, std::min<int>((int)(k / 256), (2 * sms) / std::max(1, row_tiles * c->rch * nprob)));
+    return std::max(1, std::min<int>((int)(k / 256), (kTCtasPerSm * sms) / std::max(1, row_tiles * c->rch * nprob)));
   }
   // table: device memory for jobs + tps (>= table_bytes())
   size_t table_bytes() const { return ((jobs.size() * sizeof(ImgJob) + 255) & ~size_t(255)) + tps.size() * sizeof(TProb) + 256; }
@@ -1331,6 +1331,7 @@ struct milo_moe {
   void* host_stage = nullptr;
   void* dev_stage = nullptr;
   size_t stage_bytes = 0;
+  std::mutex stage_mu;  // the staging is per handle; handles may be shared across threads
 };
 
 extern "C" milo_status milo_moe_create(const milo_expert_desc* experts, int32_t n_experts,
@@ -1927,6 +1928,7 @@ extern "C" milo_status milo_moe_forward_host(milo_moe* moe, const float* x, int6
   if (m <= 0) return m == 0 ? MILO_OK : fail(MILO_ERR_SHAPE, "negative token count");
   if (!x || !out || (moe->E > 0 && !logits)) return fail(MILO_ERR_ARGUMENT, "null argument");
   cudaStream_t stream = nullptr;
+  std::lock_guard<std::mutex> lock(moe->stage_mu);
   // x and logits go up in ONE copy from a pinned staging buffer (host memcpy is
   // cheaper than a second DMA launch at decode sizes); out comes back in one.
   const size_t xb = (size_t)m * moe->d * 4, lb = (size_t)m * std::max(moe->E, 0) * 4;

@@ -641,10 +641,14 @@ struct TProb {
   int32_t unit0;            // first work unit of this problem (prefix)
 };
 
+#ifndef PF_T_CTAS
+#define PF_T_CTAS 2
+#endif
 constexpr int kTRows = 32;  // rows per t-kernel CTA
+constexpr int kTCtasPerSm = PF_T_CTAS;
 
 __global__ void __launch_bounds__(256) pf_t_kernel(const TProb* __restrict__ probs, int n_probs) {
-  __shared__ float sx[kTRows][65];
+  __shared__ __align__(16) float sx[kTRows][68];  // rows 16 B aligned: float4 reads of 4 k
   __shared__ float su[64][65];
   int lo = 0, hi = n_probs - 1;
   while (lo < hi) {
@@ -665,40 +669,67 @@ __global__ void __launch_bounds__(256) pf_t_kernel(const TProb* __restrict__ pro
 #pragma unroll
   for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
   const int rcol = ch * 64 + j;
+  // All 24 loads of a k block are issued before any is consumed (one global
+  // round trip per block): thread = column lc of x rows lr + 4 i and of U
+  // k-rows lr + 4 i; the x row bases are resolved once, outside the k loop.
+  const int lc = tid & 63, lr = tid >> 6;
+  int64_t xrow[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int row = tile * kTRows + lr + 4 * i;
+    xrow[i] = row < P.rows ? (P.row_ids ? (int64_t)P.row_ids[row] : (int64_t)row) * P.ldx : int64_t(-1);
+  }
+  const int urc = ch * 64 + lc;
+  const bool uok = urc < P.rank;
   for (int kb = k0; kb < k1; kb += 64) {
-    // x tile [32 rows][64 k] -> binary16-rounded fp32
-    for (int e = tid; e < kTRows * 64; e += 256) {
-      const int r = e >> 6, kk = e & 63;
-      const int row = tile * kTRows + r;
-      float v = 0.0f;
-      if (row < P.rows) {
-        const int64_t xr = P.row_ids ? P.row_ids[row] : row;
-        v = P.x_dtype == 0 ? __half2float(__float2half_rn(static_cast<const float*>(P.x)[xr * P.ldx + kb + kk]))
-                           : __half2float(static_cast<const __half*>(P.x)[xr * P.ldx + kb + kk]);
-      }
-      sx[r][kk] = v;
+    float xv[8], uv[16];
+    if (P.x_dtype == 0) {
+      const float* xp = static_cast<const float*>(P.x) + kb + lc;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) xv[i] = xrow[i] >= 0 ? __half2float(__float2half_rn(xp[xrow[i]])) : 0.0f;
+    } else {
+      const __half* xp = static_cast<const __half*>(P.x) + kb + lc;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) xv[i] = xrow[i] >= 0 ? __half2float(xp[xrow[i]]) : 0.0f;
     }
-    // u tile [64 k][64 ranks] = step * (c - 4) (lowrank.cpp:122-134) or real U
-    for (int e = tid; e < 64 * 64; e += 256) {
-      const int kk = e >> 6, jj = e & 63;
-      const int kr = kb + kk, rc = ch * 64 + jj;
-      float v = 0.0f;
-      if (rc < P.rank) {
-        if (P.ucodes) {
-          const float st = P.uscales[(int64_t)kr * P.gpr + rc / 64] * (2.0f / 7.0f);
-          v = st * ((float)P.ucodes[(int64_t)kr * P.rank + rc] - 4.0f);
-        } else {
-          v = P.ureal[(int64_t)kr * P.rank + rc];
+    if (P.ucodes) {
+      const uint8_t* cp = P.ucodes + (int64_t)(kb + lr) * P.rank + urc;
+      const float* sp = P.uscales + (int64_t)(kb + lr) * P.gpr + ch;
+      uint32_t c[16];
+      float st[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        c[i] = uok ? cp[(int64_t)4 * i * P.rank] : 4u;
+        st[i] = uok ? sp[(int64_t)4 * i * P.gpr] : 0.0f;
+      }
+#pragma unroll
+      for (int i = 0; i < 16; ++i) uv[i] = (st[i] * (2.0f / 7.0f)) * ((float)c[i] - 4.0f);
+    } else {
+      const float* rp = P.ureal + (int64_t)(kb + lr) * P.rank + urc;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) uv[i] = uok ? rp[(int64_t)4 * i * P.rank] : 0.0f;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) sx[lr + 4 * i][lc] = xv[i];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) su[lr + 4 * i][lc] = uv[i];
+    __syncthreads();
+    // Shared-load bound: x read as float4 (4 k per read; per-k summation order
+    // unchanged), and warps whose 32 rank columns all lie past the rank skip the
+    // product (every rank <= 32 leaves half the CTA idle otherwise).
+    if (ch * 64 + (j & ~31) < P.rank) {
+#pragma unroll 2
+      for (int kk = 0; kk < 64; kk += 4) {
+        const float u0 = su[kk][j], u1 = su[kk + 1][j], u2 = su[kk + 2][j], u3 = su[kk + 3][j];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float4 xv = *reinterpret_cast<const float4*>(&sx[rg * 8 + i][kk]);
+          acc[i] += xv.x * u0;
+          acc[i] += xv.y * u1;
+          acc[i] += xv.z * u2;
+          acc[i] += xv.w * u3;
         }
       }
-      su[kk][jj] = v;
-    }
-    __syncthreads();
-#pragma unroll 4
-    for (int kk = 0; kk < 64; ++kk) {
-      const float uv = su[kk][j];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) acc[i] += sx[rg * 8 + i][kk] * uv;
     }
     __syncthreads();
   }
