@@ -642,10 +642,43 @@ struct TProb {
 };
 
 #ifndef PF_T_CTAS
-#define PF_T_CTAS 2
+#define PF_T_CTAS 1
 #endif
 constexpr int kTRows = 32;  // rows per t-kernel CTA
 constexpr int kTCtasPerSm = PF_T_CTAS;
+
+// One k block of pf_t_kernel's operands into registers: x (binary16-rounded)
+// at column lc of rows lr + 4 i, U = step (c - 4) (lowrank.cpp:122-134) or the
+// real factor at k-rows lr + 4 i.  Every load is issued before any is consumed.
+__device__ __forceinline__ void t_load_block(const TProb& P, int kb, int lc, int lr, int ch, int urc, bool uok,
+                                             const int64_t (&xrow)[8], float (&xv)[8], float (&uv)[16]) {
+  if (P.x_dtype == 0) {
+    const float* xp = static_cast<const float*>(P.x) + kb + lc;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) xv[i] = xrow[i] >= 0 ? __half2float(__float2half_rn(xp[xrow[i]])) : 0.0f;
+  } else {
+    const __half* xp = static_cast<const __half*>(P.x) + kb + lc;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) xv[i] = xrow[i] >= 0 ? __half2float(xp[xrow[i]]) : 0.0f;
+  }
+  if (P.ucodes) {
+    const uint8_t* cp = P.ucodes + (int64_t)(kb + lr) * P.rank + urc;
+    const float* sp = P.uscales + (int64_t)(kb + lr) * P.gpr + ch;
+    uint32_t c[16];
+    float st[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      c[i] = uok ? cp[(int64_t)4 * i * P.rank] : 4u;
+      st[i] = uok ? sp[(int64_t)4 * i * P.gpr] : 0.0f;
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) uv[i] = (st[i] * (2.0f / 7.0f)) * ((float)c[i] - 4.0f);
+  } else {
+    const float* rp = P.ureal + (int64_t)(kb + lr) * P.rank + urc;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) uv[i] = uok ? rp[(int64_t)4 * i * P.rank] : 0.0f;
+  }
+}
 
 __global__ void __launch_bounds__(256) pf_t_kernel(const TProb* __restrict__ probs, int n_probs) {
   __shared__ __align__(16) float sx[kTRows][68];  // rows 16 B aligned: float4 reads of 4 k
@@ -669,9 +702,9 @@ __global__ void __launch_bounds__(256) pf_t_kernel(const TProb* __restrict__ pro
 #pragma unroll
   for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
   const int rcol = ch * 64 + j;
-  // All 24 loads of a k block are issued before any is consumed (one global
-  // round trip per block): thread = column lc of x rows lr + 4 i and of U
-  // k-rows lr + 4 i; the x row bases are resolved once, outside the k loop.
+  // Loader role: column lc of x rows lr + 4 i and of U k-rows lr + 4 i (the x
+  // row bases resolved once).  (Prefetching block kb + 64 into registers during
+  // the product measured slower: 112 registers, one CTA per SM either way.)
   const int lc = tid & 63, lr = tid >> 6;
   int64_t xrow[8];
 #pragma unroll
@@ -681,34 +714,9 @@ __global__ void __launch_bounds__(256) pf_t_kernel(const TProb* __restrict__ pro
   }
   const int urc = ch * 64 + lc;
   const bool uok = urc < P.rank;
+  float xv[8], uv[16];
+  if (k0 < k1) t_load_block(P, k0, lc, lr, ch, urc, uok, xrow, xv, uv);
   for (int kb = k0; kb < k1; kb += 64) {
-    float xv[8], uv[16];
-    if (P.x_dtype == 0) {
-      const float* xp = static_cast<const float*>(P.x) + kb + lc;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) xv[i] = xrow[i] >= 0 ? __half2float(__float2half_rn(xp[xrow[i]])) : 0.0f;
-    } else {
-      const __half* xp = static_cast<const __half*>(P.x) + kb + lc;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) xv[i] = xrow[i] >= 0 ? __half2float(xp[xrow[i]]) : 0.0f;
-    }
-    if (P.ucodes) {
-      const uint8_t* cp = P.ucodes + (int64_t)(kb + lr) * P.rank + urc;
-      const float* sp = P.uscales + (int64_t)(kb + lr) * P.gpr + ch;
-      uint32_t c[16];
-      float st[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        c[i] = uok ? cp[(int64_t)4 * i * P.rank] : 4u;
-        st[i] = uok ? sp[(int64_t)4 * i * P.gpr] : 0.0f;
-      }
-#pragma unroll
-      for (int i = 0; i < 16; ++i) uv[i] = (st[i] * (2.0f / 7.0f)) * ((float)c[i] - 4.0f);
-    } else {
-      const float* rp = P.ureal + (int64_t)(kb + lr) * P.rank + urc;
-#pragma unroll
-      for (int i = 0; i < 16; ++i) uv[i] = uok ? rp[(int64_t)4 * i * P.rank] : 0.0f;
-    }
 #pragma unroll
     for (int i = 0; i < 8; ++i) sx[lr + 4 * i][lc] = xv[i];
 #pragma unroll
@@ -723,15 +731,16 @@ __global__ void __launch_bounds__(256) pf_t_kernel(const TProb* __restrict__ pro
         const float u0 = su[kk][j], u1 = su[kk + 1][j], u2 = su[kk + 2][j], u3 = su[kk + 3][j];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          const float4 xv = *reinterpret_cast<const float4*>(&sx[rg * 8 + i][kk]);
-          acc[i] += xv.x * u0;
-          acc[i] += xv.y * u1;
-          acc[i] += xv.z * u2;
-          acc[i] += xv.w * u3;
+          const float4 xq = *reinterpret_cast<const float4*>(&sx[rg * 8 + i][kk]);
+          acc[i] += xq.x * u0;
+          acc[i] += xq.y * u1;
+          acc[i] += xq.z * u2;
+          acc[i] += xq.w * u3;
         }
       }
     }
     __syncthreads();
+    if (kb + 64 < k1) t_load_block(P, kb + 64, lc, lr, ch, urc, uok, xrow, xv, uv);
   }
   const int r64 = P.rchunks * 64;
 #pragma unroll
