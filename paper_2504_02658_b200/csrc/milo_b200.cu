@@ -1922,6 +1922,8 @@ extern "C" milo_status milo_ep_combine(const float* y, const int32_t* slot, cons
   return MILO_OK;
 }
 
+constexpr size_t kHostZeroCopyMax = 256 * 1024;  // output bytes written over the host link directly
+
 extern "C" milo_status milo_moe_forward_host(milo_moe* moe, const float* x, int64_t m,
                                              const float* logits, float* out) {
   if (!moe) return fail(MILO_ERR_ARGUMENT, "null moe");
@@ -1949,10 +1951,20 @@ extern "C" milo_status milo_moe_forward_host(milo_moe* moe, const float* x, int6
   if (lb) std::memcpy(hs + xb, logits, lb);
   cudaError_t e = cudaMemcpyAsync(b, hs, xb + lb, cudaMemcpyHostToDevice, stream);
   milo_status st = e == cudaSuccess ? MILO_OK : fail(MILO_ERR_CUDA, "%s", cudaGetErrorString(e));
+  // Decode-sized outputs are written by the kernel straight into the mapped
+  // pinned stage (posted writes over the host link, visible once the stream
+  // has synchronised): no device-to-host copy on the critical path.
+  void* out_dev = b + xb + lb16;
+  const bool zero_copy = xb <= kHostZeroCopyMax &&
+                         cudaHostGetDevicePointer(&out_dev, hs + xb + lb16, 0) == cudaSuccess;
+  if (!zero_copy) {
+    cudaGetLastError();
+    out_dev = b + xb + lb16;
+  }
   if (st == MILO_OK)
-    st = milo_moe_forward(moe, b, m, MILO_F32, reinterpret_cast<float*>(b + xb), b + xb + lb16, MILO_F32, nullptr,
+    st = milo_moe_forward(moe, b, m, MILO_F32, reinterpret_cast<float*>(b + xb), out_dev, MILO_F32, nullptr,
                           nullptr, stream);
-  if (st == MILO_OK) {
+  if (st == MILO_OK && !zero_copy) {
     e = cudaMemcpyAsync(hs + xb + lb16, b + xb + lb16, xb, cudaMemcpyDeviceToHost, stream);
     if (e != cudaSuccess) st = fail(MILO_ERR_CUDA, "%s", cudaGetErrorString(e));
   }

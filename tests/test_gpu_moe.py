@@ -97,6 +97,26 @@ def test_skewed_routing_and_host_entry(gpu, oracle):
     assert torch.equal(a, b)
 
 
+@pytest.mark.parametrize("m", [1, 16, 600])
+def test_host_entry_matches_device_call(gpu, oracle, m):
+    """milo_moe_forward_host: small outputs are written by the kernel into the
+    mapped pinned stage (no D2H copy), large ones (600 x 128 f32 > 256 KB) come
+    back by copy; both must equal the device-buffer call bit for bit."""
+    import torch
+    E, K, d, f = 4, 2, 128, 256
+    o_ex, g_ex = _experts(oracle, gpu, E, d, f, [[16, 8, 0]] * E, seed=510)
+    rng = np.random.default_rng(20 + m)
+    x = rng.normal(0, 1, (m, d)).astype(np.float32)
+    logits = rng.normal(0, 1, (m, E)).astype(np.float32)
+    layer = gpu.MoELayer(g_ex, [], top_k=K)
+    host = layer.forward_host(x, logits)
+    host2 = layer.forward_host(x, logits)  # the stage is reused across calls
+    dev = layer.forward(torch.from_numpy(x).cuda(), torch.from_numpy(logits).cuda()).cpu().numpy()
+    assert np.array_equal(host, dev) and np.array_equal(host2, dev)
+    ids, w = oracle.router_topk(logits, K, 0)
+    assert rel_err(host, oracle.moe_forward(o_ex, [], x, ids, w)) <= TOL_MOE
+
+
 def test_router_ties_prefer_lower_expert(gpu):
     import torch
     logits = torch.tensor([[1.0, 3.0, 3.0, 0.5], [2.0, 2.0, 2.0, 2.0]], device="cuda")
