@@ -257,3 +257,18 @@ def test_out_buffer_defines_output_dtype(gpu, m):
     assert torch.allclose(out16.float(), ref, rtol=2e-3, atol=2e-3)
     with pytest.raises(gpu.ArgumentError):
         gpu.gemm_w3a16(A, W, out=out16, out_dtype=torch.float32)
+
+
+@pytest.mark.gpu
+def test_empty_batch(gpu, oracle):
+    """m = 0: pad_batch keeps 0 rows (gemm.cpp:49-60), so C is 0 x n; shape errors
+    still come first (gemm.cpp:131-139)."""
+    import torch
+    k, n = 128, 256
+    P, _ = random_quantized(oracle, k, n, seed=71)
+    W = gpu.Weight(P)
+    got = gpu.gemm_w3a16(torch.empty((0, k), device="cuda"), W, cfg=_cfg(gpu, 1))
+    assert tuple(got.shape) == (0, n)
+    assert gpu.gemm_w3a16_host(np.empty((0, k), np.float32), W, cfg=_cfg(gpu, 1)).shape == (0, n)
+    with pytest.raises(gpu.ShapeError):
+        gpu.gemm_w3a16_host(np.empty((0, k + 64), np.float32), W, cfg=_cfg(gpu, 1))

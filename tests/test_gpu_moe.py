@@ -248,3 +248,13 @@ def test_arctic_like_layer_128_experts(gpu, oracle, m):
                                  return_routing=True)
     assert (gids.cpu().numpy() == ids).all()
     assert rel_err(out.cpu().numpy(), want) <= TOL_MOE
+
+
+def test_empty_token_batch(gpu, oracle):
+    import torch
+    E, K, d, f = 4, 2, 128, 256
+    _, g_ex = _experts(oracle, gpu, E, d, f, [[16, 0, 8]] * E, seed=520)
+    layer = gpu.MoELayer(g_ex, [], top_k=K)
+    out = layer.forward(torch.empty((0, d), device="cuda"), torch.empty((0, E), device="cuda"))
+    assert tuple(out.shape) == (0, d)
+    assert layer.forward_host(np.empty((0, d), np.float32), np.empty((0, E), np.float32)).shape == (0, d)
