@@ -103,8 +103,17 @@ struct PinStage {
   size_t cap = 0, off = 0;
   cudaEvent_t ev = nullptr;
   bool pending = false;
+  // Two-pass sequences (moe_prefill): mode 1 records the uploads of a dry run
+  // (no launches) at stage offsets mirroring their device offsets, pin_flush()
+  // issues them as few coalesced copies, mode 2 replays the sequence with the
+  // uploads already in flight, so no copy sits between two kernels.
+  int mode = 0;
+  struct Rec { uint8_t* dst; size_t off, bytes; };
+  std::vector<Rec> rec;
+  uint8_t *lo = nullptr, *hi = nullptr;  // device range in which recorded copies may be merged
 };
 thread_local PinStage g_pin;
+thread_local bool g_dry = false;  // dry run: launch() and ProfScope do nothing
 void pin_begin() {
   if (g_pin.pending) {
     cudaEventSynchronize(g_pin.ev);
@@ -117,26 +126,63 @@ void pin_end(cudaStream_t s) {
   cudaEventRecord(g_pin.ev, s);
   g_pin.pending = true;
 }
-cudaError_t h2d_async(void* dst, const void* src, size_t bytes, cudaStream_t s) {
-  if (!bytes || !src) return cudaSuccess;
-  const size_t need = g_pin.off + ((bytes + 255) & ~size_t(255));
-  if (need > g_pin.cap) {  // grow (rare): nothing of this sequence may still read the old buffer
-    cudaError_t e = cudaStreamSynchronize(s);
-    if (e != cudaSuccess) return e;
-    if (g_pin.base) cudaFreeHost(g_pin.base);
-    g_pin.cap = std::max<size_t>({need, 2 * g_pin.cap, (size_t)1 << 20});
-    e = cudaMallocHost(&g_pin.base, g_pin.cap);
-    if (e != cudaSuccess) {
-      g_pin.base = nullptr;
-      g_pin.cap = 0;
-      return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s);
-    }
-    g_pin.off = 0;
+cudaError_t pin_reserve(size_t need, cudaStream_t s) {  // grow, keeping this sequence's staged bytes
+  if (need <= g_pin.cap) return cudaSuccess;
+  cudaError_t e = cudaStreamSynchronize(s);  // nothing of this sequence may still read the old buffer
+  if (e != cudaSuccess) return e;
+  const size_t cap = std::max<size_t>({need, 2 * g_pin.cap, (size_t)1 << 20});
+  uint8_t* nb = nullptr;
+  e = cudaMallocHost(&nb, cap);
+  if (e != cudaSuccess) return e;
+  if (g_pin.base) {
+    std::memcpy(nb, g_pin.base, g_pin.off);
+    cudaFreeHost(g_pin.base);
   }
-  uint8_t* p = g_pin.base + g_pin.off;
-  std::memcpy(p, src, bytes);
-  g_pin.off += (bytes + 255) & ~size_t(255);
-  return cudaMemcpyAsync(dst, p, bytes, cudaMemcpyHostToDevice, s);
+  g_pin.base = nb;
+  g_pin.cap = cap;
+  return cudaSuccess;
+}
+cudaError_t h2d_async(void* dst_, const void* src, size_t bytes, cudaStream_t s) {
+  if (!bytes || !src || g_pin.mode == 2) return cudaSuccess;
+  uint8_t* dst = static_cast<uint8_t*>(dst_);
+  size_t off = g_pin.off;
+  if (g_pin.mode == 1 && !g_pin.rec.empty()) {  // mirror the device layout inside the merge range
+    const PinStage::Rec& l = g_pin.rec.back();
+    if (dst >= l.dst + l.bytes && dst >= g_pin.lo && dst + bytes <= g_pin.hi && l.dst >= g_pin.lo &&
+        dst - l.dst < (1 << 16))
+      off = std::max(off, l.off + (size_t)(dst - l.dst));
+  }
+  cudaError_t e = pin_reserve(off + bytes, s);
+  if (e != cudaSuccess) return g_pin.mode == 1 ? e : cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s);
+  std::memcpy(g_pin.base + off, src, bytes);
+  g_pin.off = (off + bytes + 255) & ~size_t(255);
+  if (g_pin.mode == 1) {
+    g_pin.rec.push_back({dst, off, bytes});
+    return cudaSuccess;
+  }
+  return cudaMemcpyAsync(dst, g_pin.base + off, bytes, cudaMemcpyHostToDevice, s);
+}
+// Issues the recorded uploads: runs whose device and stage offsets advance
+// together inside the merge range become one copy (the gaps are unused table
+// padding).
+cudaError_t pin_flush(cudaStream_t s) {
+  cudaError_t e = cudaSuccess;
+  size_t i = 0;
+  while (i < g_pin.rec.size() && e == cudaSuccess) {
+    const PinStage::Rec& a = g_pin.rec[i];
+    size_t end = a.bytes, j = i + 1;
+    for (; j < g_pin.rec.size(); ++j) {
+      const PinStage::Rec& b = g_pin.rec[j];
+      if (!(a.dst >= g_pin.lo && b.dst + b.bytes <= g_pin.hi && b.dst >= a.dst + end &&
+            (size_t)(b.dst - a.dst) == b.off - a.off))
+        break;
+      end = (size_t)(b.dst - a.dst) + b.bytes;
+    }
+    e = cudaMemcpyAsync(a.dst, g_pin.base + a.off, end, cudaMemcpyHostToDevice, s);
+    i = j;
+  }
+  g_pin.rec.clear();
+  return e;
 }
 
 // Launch with programmatic dependent launch allowed (the kernel itself calls
@@ -154,6 +200,7 @@ cudaError_t launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
+  if (g_dry) return cudaSuccess;
   ++g_launches;
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
@@ -172,7 +219,7 @@ struct ProfScope {
   cudaStream_t s;
   int kind;
   ProfScope(int k, cudaStream_t st) : s(st), kind(k) {
-    if (!g_prof.on) return;
+    if (!g_prof.on || g_dry) return;
     cudaEventCreate(&b);
     cudaEventCreate(&e);
     cudaEventRecord(b, s);
@@ -1624,7 +1671,6 @@ milo_status moe_prefill(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype
   const int64_t f_max = moe->f_max;
   // ---- workspace
   Arena ar;
-  const size_t o_tok = ar.take((size_t)R * 4), o_slot = ar.take((size_t)R * 4);
   std::vector<size_t> o_img1(groups.size()), o_img2(groups.size());
   int64_t tiles_tot = 0;
   for (size_t gi = 0; gi < groups.size(); ++gi) {
@@ -1654,12 +1700,13 @@ milo_status moe_prefill(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype
       o_timg[j][gi] = ar.take((size_t)tiles * c->rch * 2 * nt * 128);
       o_part[j][gi] = ar.take(ImgTPlan::part_bytes(rows, kk, c, sms));
     }
-  const size_t o_tab = ar.take(262144);
+  // every per-call table (token / slot lists, image, t and GEMM problem tables)
+  // lives in one region, uploaded by one copy before the first kernel
+  const size_t tab_bytes = 262144 + 2 * (((size_t)R * 4 + 255) & ~size_t(255));
+  const size_t o_tab = ar.take(tab_bytes);
   void* mem = nullptr;
   CUDA_TRY(cudaMallocAsync(&mem, ar.size, stream));
   uint8_t* base = static_cast<uint8_t*>(mem);
-  int32_t* dtok = reinterpret_cast<int32_t*>(base + o_tok);
-  int32_t* dslot = reinterpret_cast<int32_t*>(base + o_slot);
   __half* hbuf = reinterpret_cast<__half*>(base + o_h);
   float* Y = reinterpret_cast<float*>(base + o_y);
   uint8_t* tab = base + o_tab;
@@ -1668,16 +1715,19 @@ milo_status moe_prefill(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype
     if (e != cudaSuccess && st == MILO_OK) st = fail(MILO_ERR_CUDA, "prefill: %s", cudaGetErrorString(e));
   };
   hmark("planned+alloc");
-  pin_begin();
-  guard(h2d_async(dtok, tok.data(), (size_t)R * 4, stream));
-  guard(h2d_async(dslot, slot.data(), (size_t)R * 4, stream));
   size_t tab_off = 0;
   auto upload = [&](const void* src, size_t bytes) -> uint8_t* {
     uint8_t* dst = tab + tab_off;
     tab_off = (tab_off + bytes + 255) & ~size_t(255);
+    if (tab_off > tab_bytes) {
+      if (st == MILO_OK) st = fail(MILO_ERR_CUDA, "prefill: table region overflow");
+      return tab;
+    }
     if (bytes && src) guard(h2d_async(dst, src, bytes, stream));
     return dst;
   };
+  int32_t* dtok = nullptr;
+  int32_t* dslot = nullptr;
   const int n_tprob[2] = {1, 1};  // k splits sized per problem (several CTAs per SM stay resident)
   // one grouped launch per phase: images (+ gathered rows) and the LoRC t partials
   auto img_t_phase = [&](int phase) {
@@ -1720,76 +1770,105 @@ milo_status moe_prefill(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype
     }
     guard(launch_t_batch(tv, units, upload(nullptr, tv.size() * sizeof(TProb)), stream));
   };
-  // ---- phase 1: x rows -> images, t1, t3; w1|w3 + LoRC + SwiGLU -> h
-  img_t_phase(0);
-  hmark("phase1 imgs");
-  {
-    std::vector<PfProblem> pv;
-    for (size_t gi = 0; gi < groups.size(); ++gi) {
-      const int e = groups[gi].e;
-      PfProblem P{};
-      P.w[0] = moe->hw[e][0]->tiles;
-      P.w[1] = moe->hw[e][1]->tiles;
-      P.act = base + o_img1[gi];
-      for (int mi = 0; mi < 2; ++mi) {
-        const milo_comp* c = moe->hc[e][mi];
-        if (c && c->rank > 0) {
-          P.vimg[mi] = c->vimg;
-          P.timg[mi] = base + o_timg[mi][gi];
-          P.rchunks[mi] = c->rch;
+  auto sequence = [&] {
+    tab_off = 0;
+    dtok = reinterpret_cast<int32_t*>(upload(tok.data(), (size_t)R * 4));
+    dslot = reinterpret_cast<int32_t*>(upload(slot.data(), (size_t)R * 4));
+    // ---- phase 1: x rows -> images, t1, t3; w1|w3 + LoRC + SwiGLU -> h
+    img_t_phase(0);
+    hmark("phase1 imgs");
+    {
+      std::vector<PfProblem> pv;
+      for (size_t gi = 0; gi < groups.size(); ++gi) {
+        const int e = groups[gi].e;
+        PfProblem P{};
+        P.w[0] = moe->hw[e][0]->tiles;
+        P.w[1] = moe->hw[e][1]->tiles;
+        P.act = base + o_img1[gi];
+        for (int mi = 0; mi < 2; ++mi) {
+          const milo_comp* c = moe->hc[e][mi];
+          if (c && c->rank > 0) {
+            P.vimg[mi] = c->vimg;
+            P.timg[mi] = base + o_timg[mi][gi];
+            P.rchunks[mi] = c->rch;
+          }
         }
+        P.k = (int32_t)d;
+        P.n = (int32_t)moe->hw[e][0]->cols;
+        P.rows = (int32_t)groups[gi].rows;
+        P.ntok = pf_ntok(groups[gi].rows);
+        P.mode = moe->hw[e][0]->mode;
+        P.kind = 1;
+        P.out_dtype = 1;
+        P.ldo = f_max;
+        P.out = hbuf + groups[gi].off * f_max;
+        pv.push_back(P);
       }
-      P.k = (int32_t)d;
-      P.n = (int32_t)moe->hw[e][0]->cols;
-      P.rows = (int32_t)groups[gi].rows;
-      P.ntok = pf_ntok(groups[gi].rows);
-      P.mode = moe->hw[e][0]->mode;
-      P.kind = 1;
-      P.out_dtype = 1;
-      P.ldo = f_max;
-      P.out = hbuf + groups[gi].off * f_max;
-      pv.push_back(P);
+      if (st == MILO_OK)
+        st = launch_prefill<2>(pv.data(), (int)pv.size(), stream, sms,
+                               upload(nullptr, pv.size() * sizeof(PfProblem) + 4096));
     }
-    if (st == MILO_OK)
-      st = launch_prefill<2>(pv.data(), (int)pv.size(), stream, sms,
+    (void)tiles_tot;
+    // ---- phase 2: h rows -> images, t2; w2 + LoRC -> Y slots
+    if (st == MILO_OK) img_t_phase(1);
+    if (st == MILO_OK) {
+      std::vector<PfProblem> pv;
+      for (size_t gi = 0; gi < groups.size(); ++gi) {
+        const int e = groups[gi].e;
+        PfProblem P{};
+        P.w[0] = moe->hw[e][2]->tiles;
+        P.act = base + o_img2[gi];
+        const milo_comp* c = moe->hc[e][2];
+        if (c && c->rank > 0) {
+          P.vimg[0] = c->vimg;
+          P.timg[0] = base + o_timg[2][gi];
+          P.rchunks[0] = c->rch;
+        }
+        P.k = (int32_t)moe->hw[e][2]->rows;
+        P.n = (int32_t)d;
+        P.rows = (int32_t)groups[gi].rows;
+        P.ntok = pf_ntok(groups[gi].rows);
+        P.mode = moe->hw[e][2]->mode;
+        P.kind = 0;
+        P.out_dtype = 0;
+        P.ldo = d;
+        P.out = Y;
+        P.row_map = dslot + groups[gi].off;
+        pv.push_back(P);
+      }
+      st = launch_prefill<1>(pv.data(), (int)pv.size(), stream, sms,
                              upload(nullptr, pv.size() * sizeof(PfProblem) + 4096));
-  }
-  (void)tiles_tot;
-  // ---- phase 2: h rows -> images, t2; w2 + LoRC -> Y slots
-  if (st == MILO_OK) img_t_phase(1);
-  if (st == MILO_OK) {
-    std::vector<PfProblem> pv;
-    for (size_t gi = 0; gi < groups.size(); ++gi) {
-      const int e = groups[gi].e;
-      PfProblem P{};
-      P.w[0] = moe->hw[e][2]->tiles;
-      P.act = base + o_img2[gi];
-      const milo_comp* c = moe->hc[e][2];
-      if (c && c->rank > 0) {
-        P.vimg[0] = c->vimg;
-        P.timg[0] = base + o_timg[2][gi];
-        P.rchunks[0] = c->rch;
-      }
-      P.k = (int32_t)moe->hw[e][2]->rows;
-      P.n = (int32_t)d;
-      P.rows = (int32_t)groups[gi].rows;
-      P.ntok = pf_ntok(groups[gi].rows);
-      P.mode = moe->hw[e][2]->mode;
-      P.kind = 0;
-      P.out_dtype = 0;
-      P.ldo = d;
-      P.out = Y;
-      P.row_map = dslot + groups[gi].off;
-      pv.push_back(P);
     }
-    st = launch_prefill<1>(pv.data(), (int)pv.size(), stream, sms,
-                           upload(nullptr, pv.size() * sizeof(PfProblem) + 4096));
-  }
+    if (st == MILO_OK) {
+      const int64_t total = m * (d / 4);
+      const int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)sms * 8);
+      guard(launch(moe_combine_kernel, dim3(grid), dim3(256), 0, stream, false, (const float*)Y,
+                   (const int32_t*)ids, (const float*)wts, m, K, S, d, out, out_dtype));
+    }
+  };
+  // pass 1 records the uploads (no launches), one coalesced copy, pass 2 launches
+  struct PassReset {  // leave the thread's staging state clean on every exit
+    ~PassReset() {
+      g_dry = false;
+      g_pin.mode = 0;
+      g_pin.rec.clear();
+      g_pin.lo = g_pin.hi = nullptr;
+    }
+  } pass_reset;
+  pin_begin();
+  g_pin.lo = tab;
+  g_pin.hi = tab + tab_bytes;
+  g_pin.mode = 1;
+  g_dry = true;
+  sequence();
+  g_dry = false;
+  g_pin.mode = 0;
+  if (st == MILO_OK) guard(pin_flush(stream));
+  hmark("uploads issued");
   if (st == MILO_OK) {
-    const int64_t total = m * (d / 4);
-    const int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)sms * 8);
-    guard(launch(moe_combine_kernel, dim3(grid), dim3(256), 0, stream, false, (const float*)Y,
-                 (const int32_t*)ids, (const float*)wts, m, K, S, d, out, out_dtype));
+    g_pin.mode = 2;
+    sequence();
+    g_pin.mode = 0;
   }
   pin_end(stream);
   cudaFreeAsync(mem, stream);
