@@ -1197,18 +1197,7 @@ extern "C" milo_status milo_gemm_w3a16(const milo_weight* w, const milo_comp* co
     uint8_t* img = static_cast<uint8_t*>(mem);
     uint8_t* timg = img + img_b;
     float* tpart = reinterpret_cast<float*>(img + img_b + t_img_b);
-    ImgTPlan plan;
-    const milo_comp* cs[1] = {comp};
-    pin_begin();
-    plan.add(A, a_dtype, a_cols, nullptr, m, k, ntok, img, cs, &timg, &tpart, 1);
-    cudaError_t e = plan.launch_all(img + img_b + t_img_b + t_part_b + 8192, stream);
-    if (e == cudaSuccess && lorc) e = launch_t(A, a_dtype, a_cols, nullptr, m, k, ntok, comp, timg, tpart,
-                                               img + img_b + t_img_b + t_part_b + 12288, props.sms, stream);
-    if (e != cudaSuccess) {
-      pin_end(stream);
-      cudaFreeAsync(mem, stream);
-      return fail(MILO_ERR_CUDA, "launch failed: %s", cudaGetErrorString(e));
-    }
+    uint8_t* tabs = img + img_b + t_img_b + t_part_b;  // [GEMM problems | image plan @8K | t table @12K]
     PfProblem P{};
     P.w[0] = w->tiles;
     P.act = img;
@@ -1226,7 +1215,43 @@ extern "C" milo_status milo_gemm_w3a16(const milo_weight* w, const milo_comp* co
       P.timg[0] = timg;
       P.rchunks[0] = comp->rch;
     }
-    st = launch_prefill<1>(&P, 1, stream, props.sms, img + img_b + t_img_b + t_part_b);
+    // two passes like moe_prefill: the tables go up before the first kernel
+    auto sequence = [&]() -> milo_status {
+      ImgTPlan plan;
+      const milo_comp* cs[1] = {comp};
+      plan.add(A, a_dtype, a_cols, nullptr, m, k, ntok, img, cs, &timg, &tpart, 1);
+      cudaError_t e = plan.launch_all(tabs + 8192, stream);
+      if (e == cudaSuccess && lorc)
+        e = launch_t(A, a_dtype, a_cols, nullptr, m, k, ntok, comp, timg, tpart, tabs + 12288, props.sms, stream);
+      if (e != cudaSuccess) return fail(MILO_ERR_CUDA, "launch failed: %s", cudaGetErrorString(e));
+      return launch_prefill<1>(&P, 1, stream, props.sms, tabs);
+    };
+    {
+      struct PassReset {
+        ~PassReset() {
+          g_dry = false;
+          g_pin.mode = 0;
+          g_pin.rec.clear();
+          g_pin.lo = g_pin.hi = nullptr;
+        }
+      } pass_reset;
+      pin_begin();
+      g_pin.lo = tabs;
+      g_pin.hi = tabs + 16384;
+      g_pin.mode = 1;
+      g_dry = true;
+      st = sequence();
+      g_dry = false;
+      g_pin.mode = 0;
+      if (st == MILO_OK) {
+        cudaError_t e = pin_flush(stream);
+        if (e != cudaSuccess) st = fail(MILO_ERR_CUDA, "upload failed: %s", cudaGetErrorString(e));
+      }
+      if (st == MILO_OK) {
+        g_pin.mode = 2;
+        st = sequence();
+      }
+    }
     pin_end(stream);
     cudaFreeAsync(mem, stream);
     return st;
