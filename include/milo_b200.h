@@ -143,6 +143,9 @@ milo_status milo_dequant_half(const milo_weight* w, int32_t mode, uint16_t* out,
 /* ---------------------------------------------- compensator (lowrank.hpp) */
 milo_status milo_comp_create(const milo_comp_desc* desc, milo_comp** out);
 milo_status milo_comp_destroy(milo_comp* c);
+/* The Compensator's rows (k), cols (n), rank and storage (lowrank.hpp:31-50). */
+milo_status milo_comp_info(const milo_comp* c, uint64_t* rows, uint64_t* cols, uint64_t* rank,
+                           int32_t* storage);
 
 /* --------------------------------------------------- the W3A16 GEMM (K2) */
 /* C[m x n] = A_f16[m x k] * (dequant(W) + U V), fp32 accumulation.

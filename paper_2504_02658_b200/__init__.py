@@ -124,6 +124,7 @@ def lib() -> C.CDLL:
         "milo_weight_create": [C.POINTER(_PackedDesc), C.POINTER(vp)],
         "milo_weight_destroy": [vp],
         "milo_weight_info": [vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(i32), C.POINTER(u64)],
+        "milo_comp_info": [vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(u64), C.POINTER(i32)],
         "milo_unpack_codes": [vp, vp, vp],
         "milo_dequant_half": [vp, i32, vp, vp],
         "milo_comp_create": [C.POINTER(_CompDesc), C.POINTER(vp)],
@@ -332,7 +333,9 @@ class Comp:
         h = vp()
         _check(lib().milo_comp_load(str(u_path).encode(), str(v_path).encode(), C.byref(h)))
         self._h = h
-        self.rows = self.cols = self.rank = None
+        rows, cols, rank, storage = C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_int32()
+        _check(lib().milo_comp_info(h, C.byref(rows), C.byref(cols), C.byref(rank), C.byref(storage)))
+        self.rows, self.cols, self.rank, self.storage = rows.value, cols.value, rank.value, storage.value
         return self
 
     def __init__(self, c):

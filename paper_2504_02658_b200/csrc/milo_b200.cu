@@ -576,6 +576,16 @@ milo_status milo_weight_info(const milo_weight* w, uint64_t* rows, uint64_t* col
   return MILO_OK;
 }
 
+milo_status milo_comp_info(const milo_comp* c, uint64_t* rows, uint64_t* cols, uint64_t* rank,
+                           int32_t* storage) {
+  if (!c) return fail(MILO_ERR_ARGUMENT, "null compensator");
+  if (rows) *rows = c->rows;
+  if (cols) *cols = c->cols;
+  if (rank) *rank = c->rank;
+  if (storage) *storage = c->storage;
+  return MILO_OK;
+}
+
 static milo_status unpack_common(const milo_weight* w, int what, int mode, void* out, void* stream) {
   if (!w || !out) return fail(MILO_ERR_ARGUMENT, "null argument");
   if (what == 1 && mode == 1 && !w->has_zeros)
