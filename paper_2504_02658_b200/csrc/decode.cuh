@@ -53,11 +53,13 @@ namespace milo_dev {
 #define DEC_SLOTS 2  // ring slots per warp (MoE decode)
 #endif
 
-constexpr int kDecMaxBlocks = 64;
+#ifndef DEC_MAX_BLOCKS
+#define DEC_MAX_BLOCKS 96
+#endif
+constexpr int kDecMaxBlocks = DEC_MAX_BLOCKS;  // (expert, 16-token chunk) blocks per launch
 constexpr int kDecMaxTok = 16;                    // token rows per block (NT = 2)
 constexpr int kDecMaxM = 64;                      // MoE decode path: m <= 64 (experts' tokens split into blocks)
 constexpr int kDecMaxEntries = 256;               // m * K routed entries
-constexpr int kDecMaxProbs = 3 * kDecMaxBlocks;   // per phase
 constexpr int kDecKC = 8;                         // max k-tiles (32 k each) per ring slot
 #ifndef DEC_SLOT_BYTES
 #define DEC_SLOT_BYTES 8192
@@ -174,11 +176,15 @@ struct DecCfg {
   // smem carve-up
   static constexpr int kOffBars = kRing;  // full [kCons][kSlots]
   static constexpr int kOffProbs = kOffBars + kCons * kSlots * 8;
-  static constexpr int kOffBlocks = kOffProbs + 2 * kDecMaxProbs * (int)sizeof(DProb);
-  static constexpr int kOffRoute = kOffBlocks + kDecMaxBlocks * (int)sizeof(DBlock);
+  // (expert, chunk) blocks: the single linear needs <= 16 (its 12-warp ring
+  // leaves no room for more tables)
+  static constexpr int kMaxBlocks = NMAT1 == 2 ? kDecMaxBlocks : 16;
+  static constexpr int kMaxProbs = 3 * kMaxBlocks;  // per phase
+  static constexpr int kOffBlocks = kOffProbs + 2 * kMaxProbs * (int)sizeof(DProb);
+  static constexpr int kOffRoute = kOffBlocks + kMaxBlocks * (int)sizeof(DBlock);
   static constexpr int kRouteBytes = kDecMaxEntries * 4 * 2 + 256 * 8 + 64;
   static constexpr int kOffMats = kOffRoute + kRouteBytes;  // DecExpert per block (smem copy)
-  static constexpr int kMats = NMAT1 == 2 ? kDecMaxBlocks : 16;  // single linear: <= 16 / 8 blocks
+  static constexpr int kMats = kMaxBlocks;
   static constexpr int kBytes = kOffMats + kMats * (int)sizeof(DecExpert);
 };
 
@@ -683,14 +689,14 @@ __device__ __forceinline__ void dec_stage0(const DecArgs& a) {
           if (lane >= o) incl += v;
         }
         for (int c = 0; c < nch; ++c) {
-          if (nb + incl - nch + c < kDecMaxBlocks) {
+          if (nb + incl - nch + c < CF::kMaxBlocks) {
             blocks[nb + incl - nch + c].e = e;
             blocks[nb + incl - nch + c].chunk = c;
           }
         }
         nb += __shfl_sync(0xffffffffu, incl, 31);
       }
-      if (lane == 0) sc[0] = min(nb, kDecMaxBlocks);
+      if (lane == 0) sc[0] = min(nb, CF::kMaxBlocks);
     }
     __syncthreads();
     const int nb = sc[0];
@@ -749,7 +755,7 @@ __device__ __forceinline__ void dec_stage0(const DecArgs& a) {
   for (int i = tid; i < np1 + np2; i += blockDim.x) {
     const int ph = i < np1 ? 0 : 1;
     const int j = ph == 0 ? i : i - np1;
-    DProb& P = probs[ph * kDecMaxProbs + j];
+    DProb& P = probs[ph * CF::kMaxProbs + j];
     int b, mat, kind;
     if (ph == 0) {
       kind = j < nb * nm1 ? 0 : 1;
@@ -784,7 +790,7 @@ __device__ __forceinline__ void dec_stage0(const DecArgs& a) {
   if (warp < 2) {  // exclusive prefix of units / slabs per phase (warp ph)
     const int ph = warp;
     const int n = ph == 0 ? np1 : np2;
-    DProb* PP = probs + ph * kDecMaxProbs;
+    DProb* PP = probs + ph * CF::kMaxProbs;
     int cu = 0, cs = 0;
     for (int base = 0; base < n; base += 32) {
       const int i = base + lane;
@@ -837,7 +843,7 @@ __device__ __forceinline__ void dec_finish(const DecArgs& a, float* accs, int ph
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
         for (int e = 0; e < 4; ++e) acc[x][i][nt][e] = accs[(((x * 4 + i) * NT + nt) * 4 + e) * 32 + lane];
-  const DProb& P = reinterpret_cast<const DProb*>(smem + CF::kOffProbs)[ph * kDecMaxProbs + p];
+  const DProb& P = reinterpret_cast<const DProb*>(smem + CF::kOffProbs)[ph * CF::kMaxProbs + p];
   const DBlock* blocks = reinterpret_cast<const DBlock*>(smem + CF::kOffBlocks);
   const int32_t* r_ids = reinterpret_cast<const int32_t*>(smem + CF::kOffRoute);
   const float* r_wts = reinterpret_cast<const float*>(r_ids + kDecMaxEntries);
@@ -1077,7 +1083,7 @@ struct Prod {
   uint64_t pol;  // L2 evict_first
 
   __device__ __forceinline__ void load(const DProb* probs, int rel) {  // tile rel of problem p
-    const DProb& P = probs[ph * kDecMaxProbs + p];
+    const DProb& P = probs[ph * CF::kMaxProbs + p];
     kc = P.kc;
     ktiles = P.ktiles;
     tb = P.tb;
@@ -1096,7 +1102,7 @@ struct Prod {
     if (gw >= Gp) return;
     const int st = rng_at(gw, Tp, Gp), en = rng_at(gw + 1, Tp, Gp);
     left = en - st;
-    const DProb* P = probs + ph * kDecMaxProbs;
+    const DProb* P = probs + ph * CF::kMaxProbs;
     int q = 0;
     while (P[q].t0 + P[q].n_slabs * P[q].ktiles <= st) ++q;
     p = q;
@@ -1127,7 +1133,7 @@ struct Prod {
     if (t == ktiles) {
       t = 0;
       if (++s == nslabs && left > 0) {
-        const DProb* P = probs + ph * kDecMaxProbs;
+        const DProb* P = probs + ph * CF::kMaxProbs;
         do ++p; while (P[p].n_slabs == 0);
         load(probs, 0);
       }
@@ -1170,7 +1176,7 @@ __device__ __forceinline__ void run_phase(const DecArgs& a, Prod<NT, NMAT1, MOE>
   using CF = DecCfg<NT, NMAT1>;
   constexpr int kS = CF::kSlots;
   const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
-  const DProb* PP = probs + PH * kDecMaxProbs;
+  const DProb* PP = probs + PH * CF::kMaxProbs;
   extern __shared__ __align__(128) uint8_t smem[];
   const DecExpert* bxs = reinterpret_cast<const DecExpert*>(smem + CF::kOffMats);
   const int Tp = PH == 0 ? T0 : T1;
@@ -1387,13 +1393,13 @@ __global__ void __launch_bounds__(32 * DecCfg<NT, NMAT1>::kWarps, 1)
     // code in L2 instead of queueing behind the weight stream for it.
     const DProb* P0 = probs;
     int q0 = 0;
-    while (q0 < kDecMaxProbs - 1 && !(P0[q0].kind == 1 && P0[q0].n_slabs > 0)) ++q0;
+    while (q0 < CF::kMaxProbs - 1 && !(P0[q0].kind == 1 && P0[q0].n_slabs > 0)) ++q0;
     float* scratch = reinterpret_cast<float*>(ring);
     dec_finish<NT, NMAT1, MOE, NMAT1>(a, scratch, 0, q0, 0, 0, 1, 1, 1, gw, G, true);
     if (MOE) {
-      const DProb* P1 = probs + kDecMaxProbs;
+      const DProb* P1 = probs + CF::kMaxProbs;
       int q1 = 0;
-      while (q1 < kDecMaxProbs - 1 && !(P1[q1].kind == 1 && P1[q1].n_slabs > 0)) ++q1;
+      while (q1 < CF::kMaxProbs - 1 && !(P1[q1].kind == 1 && P1[q1].n_slabs > 0)) ++q1;
       dec_finish<NT, NMAT1, MOE, 1>(a, scratch, 1, q1, 0, 0, 1, 1, 1, gw, G, true);
     }
     __syncwarp();

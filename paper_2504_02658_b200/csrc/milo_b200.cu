@@ -1275,7 +1275,8 @@ extern "C" milo_status milo_gemm_w3a16(const milo_weight* w, const milo_comp* co
     a.ldo = n;
     const int r16 = a.lin.m[0].r16;
     const int64_t per_block_slabs = n / 64 + r16 / 16;
-    const int64_t max_blocks = std::max<int64_t>(1, std::min<int64_t>(kDecMaxBlocks, kCntCap / per_block_slabs));
+    const int64_t max_blocks =
+        std::max<int64_t>(1, std::min<int64_t>(DecCfg<1, 1>::kMaxBlocks, kCntCap / per_block_slabs));
     const size_t xs = a_dtype == 0 ? 4 : 2, cs = c_dtype == 0 ? 4 : 2;
     for (int64_t done = 0; done < m;) {
       const int64_t mm = std::min<int64_t>(m - done, max_blocks * m_pad);
@@ -1926,7 +1927,11 @@ milo_status moe_forward_impl(milo_moe* moe, const void* x, int64_t m, int32_t x_
   cudaStream_t stream = (cudaStream_t)stream_;
   // decode megakernel blocks: each touched expert's tokens in chunks of m_pad rows
   const int dec_mpad = m <= 8 ? 8 : 16;
-  const int64_t nb_dec = std::min<int64_t>(moe->E, m * moe->K) + (m * moe->K) / dec_mpad +
+  // bound on the blocks: t = min(E, mK) touched experts, an expert with c <= m
+  // entries needs ceil(c / m_pad) blocks (one each when m <= m_pad), so at most
+  // t + (mK - t) / m_pad, plus the shared experts' chunks
+  const int64_t n_ent = m * moe->K, t_max = std::min<int64_t>(moe->E, n_ent);
+  const int64_t nb_dec = t_max + (m <= dec_mpad ? 0 : (n_ent - t_max) / dec_mpad) +
                          (int64_t)moe->n_shared * ((m + dec_mpad - 1) / dec_mpad);
   if (!legacy_path() && m <= kDecMaxM && m * moe->K <= kDecMaxEntries && nb_dec <= kDecMaxBlocks &&
       moe->E <= 256 && moe->K <= 16 && moe->d / 64 <= 4096) {

@@ -258,3 +258,28 @@ def test_empty_token_batch(gpu, oracle):
     out = layer.forward(torch.empty((0, d), device="cuda"), torch.empty((0, E), device="cuda"))
     assert tuple(out.shape) == (0, d)
     assert layer.forward_host(np.empty((0, d), np.float32), np.empty((0, E), np.float32)).shape == (0, d)
+
+
+@pytest.mark.parametrize("m", [12, 16])
+def test_decode_path_beyond_64_blocks(gpu, oracle, m):
+    """64 routed experts, top-6, 2 shared: up to 66 (expert, chunk) blocks in one
+    decode launch (the DeepSeek-like shape; kDecMaxBlocks = 96)."""
+    import torch
+    E, K, d, f = 64, 6, 128, 128
+    ranks = [[(0, 8, 16)[(e + j) % 3] for j in range(3)] for e in range(E)]
+    o_ex, g_ex = _experts(oracle, gpu, E, d, f, ranks, seed=1300)
+    o_sh, g_sh = _experts(oracle, gpu, 2, d, f, [[64, 32, 64], [16, 0, 32]], seed=1900)
+    rng = np.random.default_rng(40 + m)
+    x = rng.normal(0, 1, (m, d)).astype(np.float32)
+    logits = rng.normal(0, 1, (m, E)).astype(np.float32)
+    for t in range(m):  # token t prefers experts 6t .. 6t + 5 (mod 64): all 64 touched
+        logits[t, (np.arange(K) + K * t) % E] += 8.0
+    ids, w = oracle.router_topk(logits, K, 1)
+    assert len(np.unique(ids)) == E  # 64 routed blocks + 2 shared-expert blocks
+    want = oracle.moe_forward(o_ex, o_sh, x, ids, w)
+    layer = gpu.MoELayer(g_ex, g_sh, top_k=K, score_mode=1)
+    l0 = gpu.launch_count()
+    out = layer.forward(torch.from_numpy(x).cuda(), torch.from_numpy(logits).cuda())
+    torch.cuda.synchronize()
+    assert gpu.launch_count() - l0 == 1  # one decode megakernel launch, not the legacy path
+    assert rel_err(out.cpu().numpy(), want) <= TOL_MOE
