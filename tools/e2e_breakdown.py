@@ -49,3 +49,6 @@ torch.cuda.synchronize()
 print("raw milo_moe_forward     med/mean us: %.1f %.1f" % wall(raw, 50)); torch.cuda.synchronize()
 print("torch.empty (cuda)       med/mean us: %.1f %.1f" % wall(lambda: torch.empty((m, spec.d), device="cuda")))
 print("current_stream           med/mean us: %.1f %.1f" % wall(lambda: torch.cuda.current_stream()))
+from paper_2504_02658_b200 import _stream_ptr
+print("_stream_ptr              med/mean us: %.1f %.1f" % wall(lambda: _stream_ptr()))
+print("MoELayer.forward (no sync) med/mean us: %.1f %.1f" % wall(lambda: layer.forward(xd, ld), 50)); torch.cuda.synchronize()
