@@ -59,7 +59,7 @@ namespace milo_dev {
 constexpr int kDecMaxBlocks = DEC_MAX_BLOCKS;  // (expert, 16-token chunk) blocks per launch
 constexpr int kDecMaxTok = 16;                    // token rows per block (NT = 2)
 constexpr int kDecMaxM = 64;                      // MoE decode path: m <= 64 (experts' tokens split into blocks)
-constexpr int kDecMaxEntries = 256;               // m * K routed entries
+constexpr int kDecMaxEntries = 384;               // m * K routed entries (DeepSeek top-6 at m = 64)
 constexpr int kDecKC = 8;                         // max k-tiles (32 k each) per ring slot
 #ifndef DEC_SLOT_BYTES
 #define DEC_SLOT_BYTES 8192

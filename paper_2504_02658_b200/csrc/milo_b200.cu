@@ -1933,7 +1933,11 @@ milo_status moe_forward_impl(milo_moe* moe, const void* x, int64_t m, int32_t x_
   const int64_t n_ent = m * moe->K, t_max = std::min<int64_t>(moe->E, n_ent);
   const int64_t nb_dec = t_max + (m <= dec_mpad ? 0 : (n_ent - t_max) / dec_mpad) +
                          (int64_t)moe->n_shared * ((m + dec_mpad - 1) / dec_mpad);
-  if (!legacy_path() && m <= kDecMaxM && m * moe->K <= kDecMaxEntries && nb_dec <= kDecMaxBlocks &&
+  static const int dec_max_m = [] {  // experiments: MILO_DEC_MAX_M caps the decode megakernel's batch
+    const char* e = getenv("MILO_DEC_MAX_M");
+    return e ? std::min(atoi(e), kDecMaxM) : kDecMaxM;
+  }();
+  if (!legacy_path() && m <= dec_max_m && m * moe->K <= kDecMaxEntries && nb_dec <= kDecMaxBlocks &&
       moe->E <= 256 && moe->K <= 16 && moe->d / 64 <= 4096) {
     DecArgs a{};
     a.moe = 1;

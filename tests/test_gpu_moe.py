@@ -260,10 +260,11 @@ def test_empty_token_batch(gpu, oracle):
     assert layer.forward_host(np.empty((0, d), np.float32), np.empty((0, E), np.float32)).shape == (0, d)
 
 
-@pytest.mark.parametrize("m", [12, 16])
+@pytest.mark.parametrize("m", [12, 16, 48, 64])
 def test_decode_path_beyond_64_blocks(gpu, oracle, m):
-    """64 routed experts, top-6, 2 shared: up to 66 (expert, chunk) blocks in one
-    decode launch (the DeepSeek-like shape; kDecMaxBlocks = 96)."""
+    """64 routed experts, top-6, 2 shared: 66 .. 92 (expert, chunk) blocks and up to
+    384 routed entries in one decode launch (the DeepSeek-like shape;
+    kDecMaxBlocks = 96, kDecMaxEntries = 384)."""
     import torch
     E, K, d, f = 64, 6, 128, 128
     ranks = [[(0, 8, 16)[(e + j) % 3] for j in range(3)] for e in range(E)]
@@ -281,5 +282,7 @@ def test_decode_path_beyond_64_blocks(gpu, oracle, m):
     l0 = gpu.launch_count()
     out = layer.forward(torch.from_numpy(x).cuda(), torch.from_numpy(logits).cuda())
     torch.cuda.synchronize()
-    assert gpu.launch_count() - l0 == 1  # one decode megakernel launch, not the legacy path
+    # the decode megakernel (+ the f32 -> binary16 row rounding above 16 tokens), not the
+    # multi-launch legacy or prefill paths
+    assert gpu.launch_count() - l0 <= (1 if m <= 16 else 2)
     assert rel_err(out.cpu().numpy(), want) <= TOL_MOE
