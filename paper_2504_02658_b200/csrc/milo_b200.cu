@@ -11,6 +11,8 @@
 #include <chrono>
 #include <functional>
 #include <map>
+#include <atomic>
+#include <climits>
 #include <mutex>
 #include <string>
 #include <utility>
@@ -1668,18 +1670,37 @@ milo_status moe_prefill(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype
   }
   // ---- plan on the host (the reference composition order)
   std::vector<int32_t> hids((size_t)m * std::max(K, 1));
-  if (K > 0) {  // routing ids to the host through a pinned buffer (a pageable D2H is a staged copy)
-    static thread_local int32_t* pin_ids = nullptr;
+  if (K > 0) {
+    // routing ids to the host: a one-CTA kernel writes them into mapped pinned
+    // memory followed by this call's epoch in a flag word, and the host spins on
+    // the flag (no D2H copy launch, no synchronise wake-up on the critical path)
+    static thread_local int32_t* pin_ids = nullptr;  // [cap ids | flag]
     static thread_local size_t pin_ids_n = 0;
+    static thread_local int32_t pub_epoch = 0;
     if (pin_ids_n < hids.size()) {
       if (pin_ids) cudaFreeHost(pin_ids);
       pin_ids = nullptr;
       pin_ids_n = 0;
-      CUDA_TRY(cudaMallocHost(&pin_ids, std::max<size_t>(hids.size(), 4096) * 4));
-      pin_ids_n = std::max<size_t>(hids.size(), 4096);
+      const size_t cap = std::max<size_t>(hids.size(), 4096);
+      CUDA_TRY(cudaMallocHost(&pin_ids, (cap + 32) * 4));
+      pin_ids_n = cap;
+      pin_ids[cap] = 0;
     }
-    CUDA_TRY(cudaMemcpyAsync(pin_ids, ids, hids.size() * 4, cudaMemcpyDeviceToHost, stream));
-    CUDA_TRY(cudaStreamSynchronize(stream));
+    volatile int32_t* flag = pin_ids + pin_ids_n;
+    pub_epoch = pub_epoch == INT32_MAX ? 1 : pub_epoch + 1;
+    const int32_t ep = pub_epoch;
+    int32_t* d_pin = nullptr;
+    CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_pin), pin_ids, 0));
+    CUDA_TRY(launch(publish_ids_kernel, dim3(1), dim3(256), 0, stream, false, (const int32_t*)ids,
+                    (int64_t)hids.size(), d_pin, (volatile int32_t*)(d_pin + pin_ids_n), ep));
+    for (uint32_t it = 1; *flag != ep; ++it) {
+      if ((it & 4095) == 0) {  // a failed stream never publishes: check it now and then
+        const cudaError_t q = cudaStreamQuery(stream);
+        if (q != cudaErrorNotReady && q != cudaSuccess) return fail(MILO_ERR_CUDA, "%s", cudaGetErrorString(q));
+        if (q == cudaSuccess && *flag != ep) return fail(MILO_ERR_CUDA, "prefill: routing ids not published");
+      }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
     std::memcpy(hids.data(), pin_ids, hids.size() * 4);
   }
   hmark("ids synced");

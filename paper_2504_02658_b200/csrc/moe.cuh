@@ -140,6 +140,20 @@ struct MoeRouteArgs {
 constexpr int kRouteThreads = 1024;
 constexpr int kRouteMaxE = 256;
 
+// Publishes the routing ids into mapped pinned host memory, then (after a
+// system-scope fence) the call's epoch into a host flag word: the prefill
+// planner spins on the flag instead of a D2H copy plus a stream synchronise.
+__global__ void publish_ids_kernel(const int32_t* __restrict__ ids, int64_t n, int32_t* __restrict__ host_ids,
+                                   volatile int32_t* host_flag, int32_t epoch) {
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) host_ids[i] = ids[i];
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    *host_flag = epoch;
+  }
+}
+
 __global__ void __launch_bounds__(kRouteThreads) moe_route_kernel(MoeRouteArgs a) {
   pdl_wait();
   __shared__ int32_t wtot[32][kRouteMaxE];  // per-warp per-expert counts of the round
