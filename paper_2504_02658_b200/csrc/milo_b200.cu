@@ -869,6 +869,27 @@ milo_status get_ws(cudaStream_t stream, size_t data_bytes, DecodeWs** out, int* 
   return MILO_OK;
 }
 
+// Prefill workspace of (device, stream), grown on demand and reused (stream
+// order makes reuse safe); kept apart from the decode workspace so no prefill
+// bytes can alias the decode kernel's epoch-tagged words.
+std::map<std::pair<int, cudaStream_t>, std::pair<void*, size_t>> g_pf_ws;
+milo_status get_pf_ws(cudaStream_t stream, size_t bytes, void** out) {
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(g_ws_mu);
+  auto& w = g_pf_ws[{dev, stream}];
+  if (w.second < bytes) {
+    const size_t cap = std::max(bytes, w.second + w.second / 4);
+    if (w.first) CUDA_TRY(cudaFreeAsync(w.first, stream));
+    w.first = nullptr;
+    w.second = 0;
+    CUDA_TRY(cudaMallocAsync(&w.first, cap, stream));
+    w.second = cap;
+  }
+  *out = w.first;
+  return MILO_OK;
+}
+
 template <int NT, int NMAT1, bool MOE>
 milo_status launch_decode(DecArgs a, const void* x, int32_t x_dtype, int64_t ldx, int nb_max,
                           int f_max, int r16_max, int64_t y_rows, cudaStream_t stream, int sms) {
@@ -1762,7 +1783,10 @@ milo_status moe_prefill(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype
   const size_t tab_bytes = 262144 + 2 * (((size_t)R * 4 + 255) & ~size_t(255));
   const size_t o_tab = ar.take(tab_bytes);
   void* mem = nullptr;
-  CUDA_TRY(cudaMallocAsync(&mem, ar.size, stream));
+  {
+    const milo_status ws_st = get_pf_ws(stream, ar.size, &mem);
+    if (ws_st != MILO_OK) return ws_st;
+  }
   uint8_t* base = static_cast<uint8_t*>(mem);
   __half* hbuf = reinterpret_cast<__half*>(base + o_h);
   float* Y = reinterpret_cast<float*>(base + o_y);
@@ -1928,7 +1952,6 @@ milo_status moe_prefill(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype
     g_pin.mode = 0;
   }
   pin_end(stream);
-  cudaFreeAsync(mem, stream);
   return st;
 }
 
