@@ -1857,7 +1857,7 @@ milo_status moe_prefill(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype
     dslot = reinterpret_cast<int32_t*>(upload(slot.data(), (size_t)R * 4));
     // ---- phase 1: x rows -> images, t1, t3; w1|w3 + LoRC + SwiGLU -> h
     img_t_phase(0);
-    hmark("phase1 imgs");
+    hmark(g_dry ? "dry: phase1 imgs" : "phase1 imgs launched");
     {
       std::vector<PfProblem> pv;
       for (size_t gi = 0; gi < groups.size(); ++gi) {
@@ -1891,7 +1891,9 @@ milo_status moe_prefill(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype
     }
     (void)tiles_tot;
     // ---- phase 2: h rows -> images, t2; w2 + LoRC -> Y slots
+    hmark(g_dry ? "dry: gemm1" : "gemm1 launched");
     if (st == MILO_OK) img_t_phase(1);
+    hmark(g_dry ? "dry: phase2 imgs" : "phase2 imgs launched");
     if (st == MILO_OK) {
       std::vector<PfProblem> pv;
       for (size_t gi = 0; gi < groups.size(); ++gi) {
