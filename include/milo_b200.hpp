@@ -147,11 +147,19 @@ class DeviceWeight {
     check(milo_weight_create(&d, &w));
     h_.reset(w);
   }
+  // From a packed-i3 MILO1 container (milo::load_packed, pack.cpp:345-400): the
+  // artifacts `milo quantize` / `milo pack` write (pipeline.cpp:324,398).
+  static DeviceWeight load(const std::string& path) {
+    milo_weight* w = nullptr;
+    check(milo_weight_load(path.c_str(), &w));
+    return DeviceWeight(w);
+  }
   const milo_weight* get() const { return h_.get(); }
   std::size_t rows() const { return info().first; }
   std::size_t cols() const { return info().second; }
 
  private:
+  explicit DeviceWeight(milo_weight* w) { h_.reset(w); }
   std::pair<std::size_t, std::size_t> info() const {
     uint64_t r = 0, c = 0;
     check(milo_weight_info(h_.get(), &r, &c, nullptr, nullptr));
@@ -182,9 +190,22 @@ class DeviceCompensator {
     check(milo_comp_create(&d, &h));
     h_.reset(h);
   }
+  // From the factor pair `milo quantize` writes (<name>.u.milo / <name>.v.milo,
+  // pipeline.cpp:233-283).
+  static DeviceCompensator load(const std::string& u_path, const std::string& v_path) {
+    milo_comp* h = nullptr;
+    check(milo_comp_load(u_path.c_str(), v_path.c_str(), &h));
+    return DeviceCompensator(h);
+  }
   const milo_comp* get() const { return h_.get(); }
+  std::size_t rank() const {
+    uint64_t r = 0;
+    check(milo_comp_info(h_.get(), nullptr, nullptr, &r, nullptr));
+    return r;
+  }
 
  private:
+  explicit DeviceCompensator(milo_comp* h) { h_.reset(h); }
   struct Del {
     void operator()(milo_comp* c) const { milo_comp_destroy(c); }
   };

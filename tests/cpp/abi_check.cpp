@@ -19,6 +19,10 @@ int main() {
       }
     }
   };
+  // container loaders (no device here: only that they compile and report a missing file)
+  expect("load missing", [&] { DeviceWeight::load("/nonexistent.milo"); }, ErrorCode::Io);
+  expect("comp missing", [&] { DeviceCompensator::load("/nonexistent.u.milo", "/nonexistent.v.milo"); },
+         ErrorCode::Io);
   PackedInt3Matrix p;
   p.rows = 16;
   p.cols = 48;  // not a multiple of 32
