@@ -221,6 +221,7 @@ def main():
         per = (spec.experts + ws - 1) // ws
         owned = [dev_expert(h) for h in routed_h[rank * per:(rank + 1) * per]]
         layer = MiloEPLayer(owned, shared, spec.experts, spec.top_k, spec.score_mode)
+        layer.ep.uniform_batch = True  # every rank runs the same batch (weak scaling by tokens)
     else:
         experts = [dev_expert(h) for h in routed_h]
         layer = mb.MoELayer(experts, shared, top_k=spec.top_k, score_mode=spec.score_mode)

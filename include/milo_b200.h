@@ -17,7 +17,12 @@
  *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream);
  *    device-pointer calls are stream-ordered and never synchronize the host.
  *  - Handles are immutable after creation and may be shared across streams and
- *    threads.  Per-call workspace is allocated stream-ordered (cudaMallocAsync).
+ *    threads.
+ *  - Workspace: the library keeps one scratch region per (device, stream) it is
+ *    called on (allocated stream-ordered with cudaMallocAsync, grown on demand,
+ *    reused by later calls on that stream; fresh regions are initialised on the
+ *    stream before first use).  milo_stream_release(stream) frees them, e.g.
+ *    before the caller destroys the stream.
  *  - Errors: every function returns milo_status; milo_last_error() returns a
  *    thread-local message for the last failure on the calling thread.  Input
  *    validation follows the reference's order (gemm.cpp:120-139) so the same
@@ -35,7 +40,7 @@
 extern "C" {
 #endif
 
-#define MILO_B200_ABI_VERSION 1
+#define MILO_B200_ABI_VERSION 2
 
 /* milo::ErrorCode (errors.hpp:9-20) in order, offset by one; plus CUDA. */
 typedef enum milo_status {
@@ -197,10 +202,11 @@ milo_status milo_moe_forward(milo_moe* moe, const void* x, int64_t m, int32_t x_
 milo_status milo_moe_forward_routed(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype,
                                     const int32_t* topk_ids, const float* topk_w, void* out,
                                     int32_t out_dtype, void* stream);
-/* Host-buffer end-to-end call: x (m x d f32) and logits (m x E f32) in host
- * memory, out (m x d f32) host; blocking. */
-milo_status milo_moe_forward_host(milo_moe* moe, const float* x, int64_t m,
-                                  const float* router_logits, float* out);
+/* Host-buffer end-to-end call: x (m x x_cols f32) and logits (m x logit_cols
+ * f32) in host memory, out (m x d f32) host; blocking.  MILO_ERR_SHAPE unless
+ * x_cols == d and logit_cols == E (checked before any buffer is touched). */
+milo_status milo_moe_forward_host(milo_moe* moe, const float* x, int64_t m, int64_t x_cols,
+                                  const float* router_logits, int64_t logit_cols, float* out);
 
 /* ---------------------------------------------- MILO1 container loaders
  * The reference's tensor-store container (tensor_store.cpp:96-131): "MILO1",
@@ -232,6 +238,11 @@ milo_status milo_ep_dispatch(const int32_t* ids, int64_t m, int32_t K, int32_t w
 /* out[t] = sum_k w[t,k] y[slot[t K + k]] in k order (f32), the EP combine. */
 milo_status milo_ep_combine(const float* y, const int32_t* slot, const float* wts, int64_t m, int32_t K,
                             int64_t d, float* out, void* stream);
+
+/* Frees the scratch regions kept for (current device, stream) after the
+ * stream's pending work (synchronizes that stream).  A later call on the same
+ * stream allocates them again. */
+milo_status milo_stream_release(void* stream);
 
 /* Kernel launches recorded by this library on the calling thread (for the
  * bench's gpu_launches claim). */

@@ -263,8 +263,10 @@ class MoELayer {
   // Host buffers: x (m x d), router logits (m x E) -> out (m x d).
   WeightMatrix forward(const WeightMatrix& x, const WeightMatrix& router_logits) const {
     WeightMatrix out(x.rows, x.cols);
+    if (router_logits.rows != x.rows) throw ShapeError("router logits rows != x rows");
     check(milo_moe_forward_host(h_.get(), x.data.data(), static_cast<int64_t>(x.rows),
-                                router_logits.data.data(), out.data.data()));
+                                static_cast<int64_t>(x.cols), router_logits.data.data(),
+                                static_cast<int64_t>(router_logits.cols), out.data.data()));
     return out;
   }
   // Device buffers, stream-ordered.

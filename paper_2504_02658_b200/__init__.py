@@ -137,7 +137,8 @@ def lib() -> C.CDLL:
         "milo_router_topk": [vp, i64, i32, i32, i32, vp, vp, vp],
         "milo_moe_forward": [vp, vp, i64, i32, vp, vp, i32, vp, vp, vp],
         "milo_moe_forward_routed": [vp, vp, i64, i32, vp, vp, vp, i32, vp],
-        "milo_moe_forward_host": [vp, f32p, i64, f32p, f32p],
+        "milo_moe_forward_host": [vp, f32p, i64, i64, f32p, i64, f32p],
+        "milo_stream_release": [vp],
         "milo_packed_load_host": [C.c_char_p, C.POINTER(_PackedDesc), C.POINTER(vp)],
         "milo_weight_load": [C.c_char_p, C.POINTER(vp)],
         "milo_comp_load": [C.c_char_p, C.c_char_p, C.POINTER(vp)],
@@ -157,6 +158,11 @@ def _check(status: int):
     if status:
         msg = lib().milo_last_error().decode(errors="replace")
         raise _ERRORS.get(status, MiloError)(msg)
+
+
+def stream_release(stream=None):
+    """Frees the scratch regions the library keeps for (current device, stream)."""
+    _check(lib().milo_stream_release(_stream_ptr(stream)))
 
 
 def launch_count() -> int:
@@ -496,9 +502,11 @@ class MoELayer:
     def forward_host(self, x: np.ndarray, router_logits: np.ndarray) -> np.ndarray:
         x = np.ascontiguousarray(x, dtype=np.float32)
         lg = np.ascontiguousarray(router_logits, dtype=np.float32)
-        out = np.empty_like(x)
-        _check(lib().milo_moe_forward_host(self._h, _np_ptr(x, f32p), x.shape[0],
-                                           _np_ptr(lg, f32p), _np_ptr(out, f32p)))
+        if x.ndim != 2 or lg.ndim != 2 or lg.shape[0] != x.shape[0]:
+            raise ShapeError(f"x {x.shape} / router logits {lg.shape}: need (m, d) / (m, E)")
+        out = np.empty((x.shape[0], self.d), np.float32)
+        _check(lib().milo_moe_forward_host(self._h, _np_ptr(x, f32p), x.shape[0], x.shape[1],
+                                           _np_ptr(lg, f32p), lg.shape[1], _np_ptr(out, f32p)))
         return out
 
     def __del__(self):

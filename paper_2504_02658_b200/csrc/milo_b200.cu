@@ -838,55 +838,120 @@ struct DecodeWs {
   int32_t* ctrl = nullptr;
   void* data = nullptr;
   size_t data_bytes = 0;
-  int epoch = 0;
+  cudaStream_t stream = nullptr;
+  std::vector<void*> retired;  // outgrown data regions (freed by milo_stream_release)
 };
 std::mutex g_ws_mu;
 long long* g_dbg = nullptr;  // milo_debug_timeline
 int g_dbg_flags = 0;
 std::map<std::pair<int, cudaStream_t>, DecodeWs> g_ws;
+// One process-wide epoch counter (under g_ws_mu): a call's epoch is unique
+// across every stream's workspace, so a word tagged by another stream's call
+// can never pass for this call's.  0 (the control block's initial value) and
+// 0xFFFFFFFF (the fill of fresh data regions) are never used; on wrap-around
+// every workspace is re-initialised on its own stream before the epoch is reused.
+uint32_t g_epoch = 0;
+
+milo_status ws_init(DecodeWs& w, bool ctrl, bool data) {
+  if (ctrl) CUDA_TRY(cudaMemsetAsync(w.ctrl, 0, kCtrlInts * 4, w.stream));
+  if (data && w.data) CUDA_TRY(cudaMemsetAsync(w.data, 0xFF, w.data_bytes, w.stream));
+  return MILO_OK;
+}
+
+milo_status next_epoch(int* epoch) {
+  if (++g_epoch == 0xFFFFFFFFu) {
+    for (auto& kv : g_ws) {
+      int cur = 0;
+      CUDA_TRY(cudaGetDevice(&cur));
+      CUDA_TRY(cudaSetDevice(kv.first.first));
+      const milo_status st = ws_init(kv.second, true, true);
+      CUDA_TRY(cudaSetDevice(cur));
+      if (st != MILO_OK) return st;
+    }
+    g_epoch = 1;
+  }
+  *epoch = (int)g_epoch;
+  return MILO_OK;
+}
 
 // Returns the workspace of (device, stream) with >= data_bytes of data space and
-// the epoch of this call.  Stream-ordered: a grown buffer frees the old one on
-// the same stream.
+// the epoch of this call.  Stream-ordered: fresh regions are filled with 0xFF
+// (a tag no call carries) before the kernel that uses them; an outgrown region
+// is retired, not freed, so a launch another host thread prepared with it
+// cannot run after its release.
 milo_status get_ws(cudaStream_t stream, size_t data_bytes, DecodeWs** out, int* epoch) {
   int dev = 0;
   CUDA_TRY(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lock(g_ws_mu);
   DecodeWs& w = g_ws[{dev, stream}];
+  w.stream = stream;
   if (!w.ctrl) {
     CUDA_TRY(cudaMalloc(&w.ctrl, kCtrlInts * 4));
     CUDA_TRY(cudaMemset(w.ctrl, 0, kCtrlInts * 4));
   }
   if (w.data_bytes < data_bytes) {
-    if (w.data) CUDA_TRY(cudaFreeAsync(w.data, stream));
+    if (w.data) w.retired.push_back(w.data);
     w.data = nullptr;
     w.data_bytes = 0;
     CUDA_TRY(cudaMallocAsync(&w.data, data_bytes, stream));
     w.data_bytes = data_bytes;
+    const milo_status st = ws_init(w, false, true);
+    if (st != MILO_OK) return st;
   }
-  *epoch = ++w.epoch;
+  const milo_status st = next_epoch(epoch);
+  if (st != MILO_OK) return st;
   *out = &w;
   return MILO_OK;
 }
 
 // Prefill workspace of (device, stream), grown on demand and reused (stream
 // order makes reuse safe); kept apart from the decode workspace so no prefill
-// bytes can alias the decode kernel's epoch-tagged words.
-std::map<std::pair<int, cudaStream_t>, std::pair<void*, size_t>> g_pf_ws;
+// bytes can alias the decode kernel's epoch-tagged words.  Outgrown regions are
+// retired like the decode ones.
+struct PfWs {
+  void* mem = nullptr;
+  size_t bytes = 0;
+  std::vector<void*> retired;
+};
+std::map<std::pair<int, cudaStream_t>, PfWs> g_pf_ws;
 milo_status get_pf_ws(cudaStream_t stream, size_t bytes, void** out) {
   int dev = 0;
   CUDA_TRY(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lock(g_ws_mu);
   auto& w = g_pf_ws[{dev, stream}];
-  if (w.second < bytes) {
-    const size_t cap = std::max(bytes, w.second + w.second / 4);
-    if (w.first) CUDA_TRY(cudaFreeAsync(w.first, stream));
-    w.first = nullptr;
-    w.second = 0;
-    CUDA_TRY(cudaMallocAsync(&w.first, cap, stream));
-    w.second = cap;
+  if (w.bytes < bytes) {
+    const size_t cap = std::max(bytes, w.bytes + w.bytes / 4);
+    if (w.mem) w.retired.push_back(w.mem);
+    w.mem = nullptr;
+    w.bytes = 0;
+    CUDA_TRY(cudaMallocAsync(&w.mem, cap, stream));
+    w.bytes = cap;
   }
-  *out = w.first;
+  *out = w.mem;
+  return MILO_OK;
+}
+
+// Frees every workspace this library keeps for (current device, stream): after
+// the stream's pending work, the decode control block and data regions (also
+// the retired ones) and the prefill region.
+milo_status release_stream_ws(cudaStream_t stream) {
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(g_ws_mu);
+  CUDA_TRY(cudaStreamSynchronize(stream));
+  auto it = g_ws.find({dev, stream});
+  if (it != g_ws.end()) {
+    for (void* p : it->second.retired) CUDA_TRY(cudaFree(p));
+    if (it->second.data) CUDA_TRY(cudaFree(it->second.data));
+    if (it->second.ctrl) CUDA_TRY(cudaFree(it->second.ctrl));
+    g_ws.erase(it);
+  }
+  auto jt = g_pf_ws.find({dev, stream});
+  if (jt != g_pf_ws.end()) {
+    for (void* p : jt->second.retired) CUDA_TRY(cudaFree(p));
+    if (jt->second.mem) CUDA_TRY(cudaFree(jt->second.mem));
+    g_pf_ws.erase(jt);
+  }
   return MILO_OK;
 }
 
@@ -983,6 +1048,10 @@ milo_status launch_decode(DecArgs a, const void* x, int32_t x_dtype, int64_t ldx
 }
 
 }  // namespace
+
+extern "C" milo_status milo_stream_release(void* stream) {
+  return release_stream_ws(static_cast<cudaStream_t>(stream));
+}
 
 
 // ---------------------------------------------------------------------------
@@ -2093,10 +2162,15 @@ extern "C" milo_status milo_ep_combine(const float* y, const int32_t* slot, cons
 
 constexpr size_t kHostZeroCopyMax = 256 * 1024;  // output bytes written over the host link directly
 
-extern "C" milo_status milo_moe_forward_host(milo_moe* moe, const float* x, int64_t m,
-                                             const float* logits, float* out) {
+extern "C" milo_status milo_moe_forward_host(milo_moe* moe, const float* x, int64_t m, int64_t x_cols,
+                                             const float* logits, int64_t logit_cols, float* out) {
   if (!moe) return fail(MILO_ERR_ARGUMENT, "null moe");
-  if (m <= 0) return m == 0 ? MILO_OK : fail(MILO_ERR_SHAPE, "negative token count");
+  if (m < 0) return fail(MILO_ERR_SHAPE, "negative token count");
+  // the reference's shape check order (gemm.cpp:135-136): activation columns first
+  if (x_cols != moe->d) return fail(MILO_ERR_SHAPE, "x has %lld columns, the layer's d is %d", (long long)x_cols, moe->d);
+  if (logit_cols != moe->E)
+    return fail(MILO_ERR_SHAPE, "router logits have %lld columns, the layer has %d experts", (long long)logit_cols, moe->E);
+  if (m == 0) return MILO_OK;
   if (!x || !out || (moe->E > 0 && !logits)) return fail(MILO_ERR_ARGUMENT, "null argument");
   cudaStream_t stream = nullptr;
   std::lock_guard<std::mutex> lock(moe->stage_mu);

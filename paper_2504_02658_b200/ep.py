@@ -66,12 +66,21 @@ class ExpertParallelMoE:
         m = x.shape[0]
         if ids is None:
             ids, weights = self.router_fn(logits)
-        if m * self.K <= self.fixed_cap_max:
-            return self._forward_fixed(x, ids, weights)
+        # Every rank must issue the same collectives: the exchange path and the
+        # fixed capacity follow the largest token count of the group, agreed by
+        # one small all-reduce unless the caller guarantees equal batches.
+        m_max = m
+        if self.world > 1 and not self.uniform_batch:
+            t = torch.tensor([m], dtype=torch.int64, device=x.device)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+            m_max = int(t.item())
+        if m_max * self.K <= self.fixed_cap_max:
+            return self._forward_fixed(x, ids, weights, m_max)
         return self._forward_varlen(x, ids, weights)
 
-    fixed_cap_max = 256  # entries per rank up to which the exchange uses a fixed capacity
-    capacity = None      # rows per peer of the fixed exchange; None: m K (same m on every rank)
+    fixed_cap_max = 256   # entries per rank up to which the exchange uses a fixed capacity
+    capacity = None       # rows per peer of the fixed exchange; None: max(m) K over the group
+    uniform_batch = False  # caller guarantees the same m on every rank (skips the agreement)
 
     def _combine(self, x, ids, weights, y_entries):
         m = x.shape[0]
@@ -86,12 +95,12 @@ class ExpertParallelMoE:
 
     device_kernels = False  # MiloEPLayer: dispatch / combine as CUDA kernels of the library
 
-    def _forward_fixed(self, x, ids, weights):
+    def _forward_fixed(self, x, ids, weights, m_max=None):
         """Decode-sized batches: every rank sends a fixed capacity C = m K rows to
         every peer (unused rows carry expert id -1, which the kernels skip), so
         the exchange needs no count all-to-all and no host synchronization."""
         m, dev, W = x.shape[0], x.device, self.world
-        C = self.capacity if self.capacity is not None else m * self.K
+        C = self.capacity if self.capacity is not None else (m_max or m) * self.K
         assert m * self.K <= C, "fixed-capacity exchange: m * top_k exceeds the capacity"
         if self.device_kernels:
             import paper_2504_02658_b200 as mb

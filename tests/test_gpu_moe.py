@@ -286,3 +286,21 @@ def test_decode_path_beyond_64_blocks(gpu, oracle, m):
     # multi-launch legacy or prefill paths
     assert gpu.launch_count() - l0 <= (1 if m <= 16 else 2)
     assert rel_err(out.cpu().numpy(), want) <= TOL_MOE
+
+
+def test_host_entry_shape_errors(gpu, oracle):
+    """milo_moe_forward_host checks x's and the logits' column counts against the
+    layer (d, E) before touching any buffer: ShapeError, as the reference's
+    gemm_w3a16 throws for A.cols != k (gemm.cpp:135-136)."""
+    E, K, d, f = 4, 2, 128, 256
+    _, g_ex = _experts(oracle, gpu, E, d, f, [[0, 0, 0]] * E, seed=520)
+    layer = gpu.MoELayer(g_ex, [], top_k=K)
+    x = np.zeros((3, d), np.float32)
+    lg = np.zeros((3, E), np.float32)
+    with pytest.raises(gpu.ShapeError):
+        layer.forward_host(np.zeros((3, d - 64), np.float32), lg)
+    with pytest.raises(gpu.ShapeError):
+        layer.forward_host(x, np.zeros((3, E - 1), np.float32))
+    with pytest.raises(gpu.ShapeError):
+        layer.forward_host(x, np.zeros((2, E), np.float32))
+    assert layer.forward_host(x, lg).shape == (3, d)
