@@ -111,39 +111,88 @@ def dist_env():
     return ws, rank, local
 
 
-def cpu_reference_time(spec, routed, shared, m, steps, seed, which="ref"):
-    """Times the reference CPU implementation (oracle/_ref: the reference's
-    own gemm_w3a16 composed per expert through its parallel_for), or our C
-    restatement if the reference library was not built.  Returns dict."""
-    from oracle.oracle import Comp, Oracle, Packed
-    kind = "reference" if which == "ref" and Oracle.available("ref") else "port"
-    o = Oracle("ref" if kind == "reference" else "oracle")
-    cores = os.cpu_count() or 1
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
-    def cv(P):
-        return Packed(P.rows, P.cols, 0, False, P.mode, 64, P.words, None, None, P.scales, P.zeros)
 
-    def cc(c):
-        if c is None:
-            return None
-        return Comp(c.rows, c.cols, c.rank, 1, None, None, c.qu_codes, c.qu_scales, c.qvt_codes,
-                    c.qvt_scales, 64)
+def host_inputs(spec, m, n_steps, seed):
+    """The synthetic per-step inputs both arms use: x (binary16 values, as the
+    kernels and gemm.cpp:144-146 round them) and fp32 router logits."""
+    rng = np.random.default_rng(seed)
+    xs = [rng.normal(0, 1, (m, spec.d)).astype(np.float16) for _ in range(n_steps)]
+    ls = [rng.normal(0, 1, (m, spec.experts)).astype(np.float32) for _ in range(n_steps)]
+    return xs, ls
 
-    ex = [{"w": [cv(P) for P in h.w], "c": [cc(c) for c in h.c]} for h in routed]
-    sh = [{"w": [cv(P) for P in h.w], "c": [cc(c) for c in h.c]} for h in shared]
-    rng = np.random.default_rng(seed + 99)
-    orc = Oracle("oracle")
-    times = []
-    for _ in range(steps):
-        x = rng.normal(0, 1, (m, spec.d)).astype(np.float32)
-        logits = rng.normal(0, 1, (m, spec.experts)).astype(np.float32)
-        t0 = time.perf_counter()
-        ids, w = orc.router_topk(logits, spec.top_k, spec.score_mode)
-        o.moe_forward(ex, sh, x, ids, w, n_threads=cores)
-        times.append(time.perf_counter() - t0)
-    return {"us": float(np.mean(times)) * 1e6, "kind": kind, "cores": cores,
-            "sample": f"{steps} x {spec.name} layer calls at batch {m} (all experts' weights "
-                      f"resident in host RAM; {cores} threads via parallel_for over active experts)"}
+
+def input_seed(args, m, rank=0):
+    return args.seed * 1000 + m * 16 + rank
+
+
+class CpuReference:
+    """The reference CPU implementation of the layer on the host cores: the
+    compiled reference's gemm_w3a16 (oracle/_ref) composed per expert, every
+    (expert, matrix, column slice) call through its parallel_for over all
+    threads (oracle/ref/ref_capi.cpp); our C restatement if oracle/_ref is
+    missing.  Weights are copied in and sliced once, outside any timing."""
+
+    def __init__(self, spec, routed, shared):
+        from oracle.oracle import Comp, Oracle, Packed, RefMoE
+        self.kind = "reference" if Oracle.available("ref") else "port"
+        self.cores = os.cpu_count() or 1
+        self.spec = spec
+        self.orc = Oracle("oracle")
+
+        def cv(P):
+            return Packed(P.rows, P.cols, 0, False, P.mode, 64, P.words, None, None, P.scales, P.zeros)
+
+        def cc(c):
+            if c is None:
+                return None
+            return Comp(c.rows, c.cols, c.rank, 1, None, None, c.qu_codes, c.qu_scales, c.qvt_codes,
+                        c.qvt_scales, 64)
+
+        self.ex = [{"w": [cv(P) for P in h.w], "c": [cc(c) for c in h.c]} for h in routed]
+        self.sh = [{"w": [cv(P) for P in h.w], "c": [cc(c) for c in h.c]} for h in shared]
+        self.h = RefMoE(Oracle("ref"), self.ex, self.sh, self.cores) if self.kind == "reference" else None
+
+    def forward(self, x, logits):
+        """One layer call (router + experts + combine) on the host; fp32 out."""
+        ids, w = self.orc.router_topk(logits, self.spec.top_k, self.spec.score_mode)
+        x = np.asarray(x, np.float32)
+        if self.h is not None:
+            return self.h.forward(x, ids, w), ids
+        return self.orc.moe_forward(self.ex, self.sh, x, ids, w, n_threads=self.cores), ids
+
+    def time(self, xs, ls):
+        times = []
+        for x, lg in zip(xs, ls):
+            t0 = time.perf_counter()
+            self.forward(x, lg)
+            times.append(time.perf_counter() - t0)
+        return float(np.mean(times)) * 1e6
+
+    def describe(self, steps, m):
+        how = ("the reference's gemm_w3a16 (oracle/_ref)" if self.kind == "reference"
+               else "the C restatement (oracle/milo_oracle.c)")
+        return (f"{steps} x {self.spec.name} layer calls at batch {m}: {how} per (touched expert, "
+                f"matrix, 128-column slice) through parallel_for on {self.cores} threads "
+                f"({cpu_model()}); weights resident in host RAM")
+
+
+def config_dict(spec, m, parallelism):
+    return {"workload": spec.name, "batch": m, "experts": spec.experts, "top_k": spec.top_k,
+            "d": spec.d, "f": spec.f, "shared_experts": spec.shared,
+            "ranks": list(spec.routed_ranks), "rank_shared": spec.rank_shared,
+            "parallelism": parallelism, "tokens_per_rank": m,
+            "inputs": "numpy default_rng(seed*1000 + 16 m + rank): x N(0,1) as binary16, logits N(0,1) f32",
+            "l2": "flushed between steps (256 MiB write + 256 MiB read, outside the timed events)"}
 
 
 def run_reference_arm(args, spec):
@@ -152,21 +201,24 @@ def run_reference_arm(args, spec):
         return
     from paper_2504_02658_b200.synth import build_host_layer
     routed, shared = build_host_layer(spec, seed=args.seed)
+    cpu = CpuReference(spec, routed, shared)
     steps = max(1, args.steps)
-    for _ in range(max(0, min(args.warmup, 1))):
-        cpu_reference_time(spec, routed, shared, args.batch, 1, args.seed)
-    res = cpu_reference_time(spec, routed, shared, args.batch, steps, args.seed)
+    m = args.batch
+    xs, ls = host_inputs(spec, m, args.warmup + steps, input_seed(args, m))
+    for i in range(min(args.warmup, 1)):
+        cpu.forward(xs[i], ls[i])
+    us = cpu.time(xs[args.warmup:], ls[args.warmup:])
     line = {
-        "impl": "reference", "metric": METRIC, "value": round(res["us"], 1), "unit": "us",
-        "n_gpus": ws, "steps": steps, "warmup": args.warmup, "ms_per_step": round(res["us"] / 1e3, 3),
-        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f16/f32",
-        "data": "synthetic", "config": {"workload": spec.name, "batch": args.batch,
-                                        "experts": spec.experts, "top_k": spec.top_k,
-                                        "d": spec.d, "f": spec.f},
-        "cpu_baseline": {"value": round(res["us"], 1), "unit": "us", "cores": res["cores"],
-                         "kind": res["kind"], "sample": res["sample"]},
-        "e2e": {"value": round(res["us"], 1), "unit": "us", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
+        "impl": "reference", "metric": METRIC, "value": round(us, 1), "unit": "us",
+        "n_gpus": ws, "steps": steps, "warmup": args.warmup, "ms_per_step": round(us / 1e3, 3),
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f16 (activations, de-quantized weights) / f32 accumulate",
+        "data": "synthetic (random-init INT3 g64 weights, symm-int3 LoRC, N(0,1) activations "
+                "and router logits)",
+        "config": config_dict(spec, m, "ep%d" % ws if ws > 1 else "single GPU"),
+        "cpu_baseline": {"value": round(us, 1), "unit": "us", "cores": cpu.cores, "kind": cpu.kind,
+                         "sample": cpu.describe(steps, m)},
+        "e2e": {"value": round(us, 1), "unit": "us", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
@@ -237,20 +289,18 @@ def main():
         torch.sum(flush_r)
     stream = torch.cuda.current_stream()
 
-    def make_inputs(m, n_steps, seed):
-        g = torch.Generator(device="cuda").manual_seed(seed * 1000 + rank)
-        xs = [torch.randn(m, spec.d, device="cuda", generator=g).half() for _ in range(n_steps)]
-        ls = [torch.randn(m, spec.experts, device="cuda", generator=g) for _ in range(n_steps)]
-        return xs, ls
+    def make_inputs(m, n_steps):
+        hx, hl = host_inputs(spec, m, n_steps, input_seed(args, m, rank))
+        return [torch.from_numpy(x).cuda() for x in hx], [torch.from_numpy(lg).cuda() for lg in hl], hx, hl
 
-    def time_steps(m, n_steps, warmup, profile=False):
-        xs, ls = make_inputs(m, warmup + n_steps, args.seed + m)
-        out = torch.empty(m, spec.d, device="cuda", dtype=torch.float16)
+    def time_steps(m, n_steps, warmup, profile=False, keep_first=False):
+        xs, ls, hx, hl = make_inputs(m, warmup + n_steps)
         keep = []  # same allocation pattern as the timed loop (outputs kept alive)
         for i in range(warmup):
-            keep.append(layer.forward(xs[i], ls[i], out_dtype=torch.float16, return_routing=True))
+            keep.append(layer.forward(xs[i], ls[i], return_routing=True))
         del keep
         ids_all = []
+        first = None
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                for _ in range(n_steps)]
         if ws > 1:
@@ -267,10 +317,11 @@ def main():
             flush_l2()
             s, e = evs[i]
             s.record(stream)
-            o, ids, _ = layer.forward(xs[warmup + i], ls[warmup + i], out_dtype=torch.float16,
-                                      return_routing=True)
+            o, ids, _ = layer.forward(xs[warmup + i], ls[warmup + i], return_routing=True)
             e.record(stream)
             ids_all.append(ids)
+            if keep_first and i == 0:
+                first = (o, hx[warmup], hl[warmup])
         torch.cuda.synchronize()
         if profile:
             mb.profile_enable(False)
@@ -279,12 +330,14 @@ def main():
             dist.barrier()
         ms = np.array([s.elapsed_time(e) for s, e in evs])
         ids_np = [i.cpu().numpy() for i in ids_all]
+        if keep_first:
+            return ms, ids_np, launches, (first[0].cpu().numpy(), first[1], first[2])
         return ms, ids_np, launches
 
     # ---------------- headline timed region ----------------
     m = args.batch
     with ClockSampler(local) as clk:
-        ms, ids_np, launches = time_steps(m, args.steps, args.warmup)
+        ms, ids_np, launches, first_step = time_steps(m, args.steps, args.warmup, keep_first=True)
     mean_ms = float(ms.mean())
     if ws > 1:
         t = torch.tensor([mean_ms], device="cuda")
@@ -373,13 +426,23 @@ def main():
                           "TFLOPs": round(fl / us / 1e6, 2), "roofline_us": round(t_roof, 2),
                           "roofline_frac": round(t_roof / us, 3)})
 
-    # ---------------- CPU baseline (rank 0, N=1) ----------------
-    cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu:
+    # ---------------- CPU reference: parity of a timed step + baseline (rank 0) ----------------
+    cpu = parity = None
+    if rank == 0 and not args.no_cpu:
         try:
-            res = cpu_reference_time(spec, routed_h, shared_h, m, 2, args.seed)
-            cpu = {"value": round(res["us"], 1), "unit": "us", "cores": res["cores"],
-                   "kind": res["kind"], "sample": res["sample"]}
+            ref = CpuReference(spec, routed_h, shared_h)
+            got, hx0, hl0 = first_step
+            want, ref_ids = ref.forward(hx0, hl0)
+            den = float(np.sqrt((want.astype(np.float64) ** 2).sum()))
+            parity = {"rel_err": float(np.sqrt(((got.astype(np.float64) - want) ** 2).sum()) / den),
+                      "ids_equal": bool(np.array_equal(ids_np[0], ref_ids)), "tol": 2.5e-4,
+                      "against": ref.kind, "step": "first timed step (same x / logits, fp32 out)"}
+            if ws == 1:
+                cpu_steps = 3
+                hx, hl = host_inputs(spec, m, cpu_steps, input_seed(args, m) + 7)
+                us = ref.time(hx, hl)
+                cpu = {"value": round(us, 1), "unit": "us", "cores": ref.cores, "kind": ref.kind,
+                       "sample": ref.describe(cpu_steps, m)}
         except Exception as exc:  # noqa: BLE001
             cpu = {"value": None, "unit": "us", "cores": os.cpu_count(), "kind": "port",
                    "sample": f"unavailable: {exc}"}
@@ -396,11 +459,7 @@ def main():
         "dtype": "f16 (activations, de-quantized weights) / f32 accumulate",
         "data": "synthetic (random-init INT3 g64 weights, symm-int3 LoRC, N(0,1) activations "
                 "and router logits)",
-        "config": {"workload": spec.name, "batch": m, "experts": spec.experts,
-                   "top_k": spec.top_k, "d": spec.d, "f": spec.f, "shared_experts": spec.shared,
-                   "ranks": list(spec.routed_ranks), "parallelism": f"ep{ws}" if use_ep else "single GPU",
-                   "tokens_per_rank": m,
-                   "l2": "flushed between steps (256 MiB write + 256 MiB read, outside the timed events)"},
+        "config": config_dict(spec, m, f"ep{ws}" if use_ep else "single GPU"),
         "achieved_GBps_layer": round(tot_bytes / (value_us * 1e-6) / 1e9, 1),
         "layer_bytes": int(tot_bytes), "layer_flops": int(tot_flops),
         "roofline": {"bound": bound, "kernel": dom_name, "achieved": round(achieved, 1), "peak": peak,
@@ -418,6 +477,7 @@ def main():
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
+        "parity": parity,
         "sweep": sweep,
     }
     print(json.dumps(line), flush=True)

@@ -219,6 +219,8 @@ class Oracle:
             self.lib.ref_moe_set_linear.restype = i
             self.lib.ref_moe_set_linear.argtypes = [C.c_void_p, i, i, u64, u64, u32p, u16p, u16p,
                                                     u64, u8p, f32p, u8p, f32p]
+            self.lib.ref_moe_prepare.restype = i
+            self.lib.ref_moe_prepare.argtypes = [C.c_void_p, i]
             self.lib.ref_moe_forward.restype = i
             self.lib.ref_moe_forward.argtypes = [C.c_void_p, f32p, u64, u64, i, i32p, f32p, i, f32p]
 
@@ -452,30 +454,59 @@ class Oracle:
                            _p(topk_ids, i32p), _p(topk_w, f32p), n_threads, _p(out, f32p))
             self._check(st)
             return out
-        # reference composition: shared experts appended to the top-k lists with weight 1
-        allx = list(experts) + list(shared)
-        h = self.lib.ref_moe_create(len(allx))
+        h = RefMoE(self, experts, shared, n_threads)
         try:
-            for e, ex in enumerate(allx):
-                for j in range(3):
-                    P = ex["w"][j]
-                    c = ex["c"][j]
-                    r = 0 if c is None else c.rank
-                    self._check(self.lib.ref_moe_set_linear(
-                        h, e, j, P.rows, P.cols, _p(P.words, u32p), _p(P.scales, u16p),
-                        _p(P.zeros, u16p), r, _p(c.qu_codes if r else None, u8p),
-                        _p(c.qu_scales if r else None, f32p), _p(c.qvt_codes if r else None, u8p),
-                        _p(c.qvt_scales if r else None, f32p)))
-            if shared:
-                ns = len(shared)
-                sid = np.tile(np.arange(len(experts), len(experts) + ns, dtype=np.int32), (m, 1))
-                ids2 = np.ascontiguousarray(np.concatenate([topk_ids, sid], 1))
-                w2 = np.ascontiguousarray(np.concatenate([topk_w, np.ones((m, ns), np.float32)], 1))
-            else:
-                ids2, w2 = topk_ids, topk_w
-            self._check(self.lib.ref_moe_forward(h, _p(x, f32p), m, d, ids2.shape[1],
-                                                 _p(ids2, i32p), _p(w2, f32p), n_threads,
-                                                 _p(out, f32p)))
+            return h.forward(x, topk_ids, topk_w)
         finally:
-            self.lib.ref_moe_destroy(h)
+            h.close()
+
+
+class RefMoE:
+    """A persistent MoE composition over the compiled reference (oracle/_ref):
+    experts copied in once and cut into column slices for `workers` threads
+    (ref_moe_prepare), so that forward() times only the reference's own
+    gemm_w3a16 calls (oracle/ref/ref_capi.cpp ref_moe_forward)."""
+
+    def __init__(self, o: "Oracle", experts, shared, workers: int = 1):
+        assert o.which == "ref"
+        self.o, self.lib = o, o.lib
+        self.n_routed, self.n_shared = len(experts), len(shared)
+        self.workers = workers
+        allx = list(experts) + list(shared)
+        self.h = self.lib.ref_moe_create(len(allx))
+        for e, ex in enumerate(allx):
+            for j in range(3):
+                P = ex["w"][j]
+                c = ex["c"][j]
+                r = 0 if c is None else c.rank
+                o._check(self.lib.ref_moe_set_linear(
+                    self.h, e, j, P.rows, P.cols, _p(P.words, u32p), _p(P.scales, u16p),
+                    _p(P.zeros, u16p), r, _p(c.qu_codes if r else None, u8p),
+                    _p(c.qu_scales if r else None, f32p), _p(c.qvt_codes if r else None, u8p),
+                    _p(c.qvt_scales if r else None, f32p)))
+        o._check(self.lib.ref_moe_prepare(self.h, workers))
+
+    def forward(self, x, topk_ids, topk_w):
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        topk_ids = np.ascontiguousarray(topk_ids, dtype=np.int32)
+        topk_w = np.ascontiguousarray(topk_w, dtype=np.float32)
+        m, d = x.shape
+        out = np.zeros((m, d), np.float32)
+        if self.n_shared:
+            # shared experts appended to the top-k lists with weight 1
+            sid = np.tile(np.arange(self.n_routed, self.n_routed + self.n_shared, dtype=np.int32), (m, 1))
+            ids2 = np.ascontiguousarray(np.concatenate([topk_ids, sid], 1))
+            w2 = np.ascontiguousarray(np.concatenate([topk_w, np.ones((m, self.n_shared), np.float32)], 1))
+        else:
+            ids2, w2 = topk_ids, topk_w
+        self.o._check(self.lib.ref_moe_forward(self.h, _p(x, f32p), m, d, ids2.shape[1],
+                                               _p(ids2, i32p), _p(w2, f32p), self.workers,
+                                               _p(out, f32p)))
         return out
+
+    def close(self):
+        if self.h:
+            self.lib.ref_moe_destroy(self.h)
+            self.h = None
+
+    __del__ = close

@@ -10,6 +10,7 @@
 // milo::gemm_w3a16 calls (proj/src/gemm.cpp:117-199) run through the
 // reference's own milo::parallel_for (proj/src/pipeline.cpp:26-53).
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -418,16 +419,91 @@ std::uint64_t ref_matrix_memory_bytes(std::uint64_t rows, std::uint64_t cols, st
 
 // --- MoE composition over the reference GEMM (CPU baseline) -----------------------
 // One expert = w1 (d x f), w3 (d x f), w2 (f x d) in the reference's k x n
-// orientation (synth.cpp:37-39), each a linear/asymmetric PackedInt3Matrix with
-// a symm-int3 compensator.  Routing is given (topk ids/weights per token); the
-// per-expert calls run through milo::parallel_for (pipeline.cpp:26-53).
+// orientation (synth.cpp:37-39), each a linear PackedInt3Matrix with an optional
+// symm-int3 compensator.  Routing is given (topk ids/weights per token).
+//
+// Threading: the reference's gemm_w3a16 is single-threaded; its output columns
+// are independent (C[i,j] accumulates over k in a fixed order per column, and
+// the compensator adds t V[:, j] per column), so every matrix is cut once into
+// column slices (multiples of 128: whole quant groups and whole n-tiles of the
+// GemmConfig tile (128,128), gemm.cpp:131-134) and the calls of a
+// phase -- (touched expert, w1 | w3, slice), then (touched expert, w2, slice) --
+// run through the reference's own milo::parallel_for (pipeline.cpp:26-53) over
+// all workers.  The result is bit-identical to the unsliced composition.
 struct RefLinear {
   PackedInt3Matrix w;
   std::optional<Compensator> comp;
+  // column slices (built on first use for a slice count)
+  std::size_t n_slices = 0;
+  std::vector<std::size_t> c0;  // first column of each slice (+ end)
+  std::vector<PackedInt3Matrix> ws;
+  std::vector<std::optional<Compensator>> cs;
 };
 struct RefExpert {
   RefLinear l[3];  // w1, w3, w2
 };
+
+// Columns [a, b) of a linear-layout, non-split packed matrix (a, b multiples of 128).
+PackedInt3Matrix slice_cols(const PackedInt3Matrix& p, std::size_t a, std::size_t b) {
+  PackedInt3Matrix q;
+  q.rows = p.rows;
+  q.cols = b - a;
+  q.layout = p.layout;
+  q.split = false;
+  q.mode = p.mode;
+  q.group_size = p.group_size;
+  const std::size_t gpr = p.cols / 32, qpr = p.cols / p.group_size;
+  q.words.reserve(p.rows * (b - a) / 32 * 3);
+  q.scales.reserve(p.rows * (b - a) / p.group_size);
+  for (std::size_t r = 0; r < p.rows; ++r) {
+    q.words.insert(q.words.end(), p.words.begin() + (r * gpr + a / 32) * 3,
+                   p.words.begin() + (r * gpr + b / 32) * 3);
+    q.scales.insert(q.scales.end(), p.scales.begin() + r * qpr + a / p.group_size,
+                    p.scales.begin() + r * qpr + b / p.group_size);
+    if (!p.zeros.empty())
+      q.zeros.insert(q.zeros.end(), p.zeros.begin() + r * qpr + a / p.group_size,
+                     p.zeros.begin() + r * qpr + b / p.group_size);
+  }
+  return q;
+}
+
+// Columns [a, b) of a compensator: U unchanged, V^T rows [a, b).
+std::optional<Compensator> slice_comp(const std::optional<Compensator>& c, std::size_t a, std::size_t b) {
+  if (!c) return std::nullopt;
+  Compensator s = *c;
+  s.cols = b - a;
+  if (c->storage == CompensatorStorage::Real) {
+    s.V.clear();
+    for (std::size_t r = 0; r < c->rank; ++r)
+      s.V.insert(s.V.end(), c->V.begin() + r * c->cols + a, c->V.begin() + r * c->cols + b);
+  } else {
+    const std::size_t gpr = c->rank == 0 ? 0 : (c->rank + c->qVt.group_size - 1) / c->qVt.group_size;
+    s.qVt.rows = b - a;
+    s.qVt.codes.assign(c->qVt.codes.begin() + a * c->rank, c->qVt.codes.begin() + b * c->rank);
+    s.qVt.scales.assign(c->qVt.scales.begin() + a * gpr, c->qVt.scales.begin() + b * gpr);
+  }
+  return s;
+}
+
+void ensure_slices(RefLinear& L, std::size_t want) {
+  const std::size_t groups = L.w.cols / 128;
+  const std::size_t n = std::max<std::size_t>(1, std::min(want, groups));
+  if (L.n_slices == n) return;
+  L.n_slices = n;
+  L.c0.assign(n + 1, 0);
+  L.ws.clear();
+  L.cs.clear();
+  for (std::size_t s = 0; s <= n; ++s) L.c0[s] = groups * s / n * 128;
+  for (std::size_t s = 0; s < n; ++s) {
+    if (n == 1) {
+      L.ws.push_back(L.w);
+      L.cs.push_back(L.comp);
+    } else {
+      L.ws.push_back(slice_cols(L.w, L.c0[s], L.c0[s + 1]));
+      L.cs.push_back(slice_comp(L.comp, L.c0[s], L.c0[s + 1]));
+    }
+  }
+}
 
 void* ref_moe_create(int n_experts) {
   auto* v = new std::vector<RefExpert>(static_cast<std::size_t>(n_experts));
@@ -444,12 +520,22 @@ int ref_moe_set_linear(void* h, int expert, int which, std::uint64_t rows, std::
   return guarded([&] {
     auto& ex = (*static_cast<std::vector<RefExpert>*>(h))[static_cast<std::size_t>(expert)];
     RefLinear& L = ex.l[which];
+    L = RefLinear{};
     L.w = make_packed(rows, cols, 0, 0, zeros ? 1 : 0, 64, words, nullptr, nullptr, scales, zeros);
     if (rank > 0)
       L.comp = make_comp(rows, cols, rank, 1, nullptr, nullptr, qu_codes, qu_scales, qvt_codes,
                          qvt_scales, 64);
     else
       L.comp.reset();
+  });
+}
+
+// Prepares the column slices for `workers` threads (outside any timed region).
+int ref_moe_prepare(void* h, int workers) {
+  return guarded([&] {
+    for (auto& ex : *static_cast<std::vector<RefExpert>*>(h))
+      for (auto& L : ex.l)
+        if (L.w.cols) ensure_slices(L, static_cast<std::size_t>(std::max(1, workers)));
   });
 }
 
@@ -470,23 +556,50 @@ int ref_moe_forward(void* h, const float* x, std::uint64_t m, std::uint64_t d, i
     std::vector<std::size_t> active;
     for (std::size_t e = 0; e < E; ++e)
       if (!rows_of[e].empty()) active.push_back(e);
-    std::vector<WeightMatrix> y(E);
+    const std::size_t want = static_cast<std::size_t>(std::max(1, workers));
+    for (std::size_t e : active)
+      for (auto& L : experts[e].l) ensure_slices(L, want);
     GemmConfig cfg;
     cfg.tile_shape = {128, 128};
-    parallel_for(active.size(), workers, [&](std::size_t ai) {
-      const std::size_t e = active[ai];
+    // gathered rows of every touched expert
+    std::vector<WeightMatrix> xe(E), h1(E), h3(E), y(E);
+    for (std::size_t e : active) {
       const auto& rows = rows_of[e];
-      WeightMatrix xe(rows.size(), d);
+      xe[e] = WeightMatrix(rows.size(), d);
       for (std::size_t i = 0; i < rows.size(); ++i)
-        std::memcpy(&xe.data[i * d], x + rows[i] * d, d * 4);
-      const RefExpert& ex = experts[e];
-      WeightMatrix h1 = gemm_w3a16(xe, ex.l[0].w, ex.l[0].comp, cfg);
-      WeightMatrix h3 = gemm_w3a16(xe, ex.l[1].w, ex.l[1].comp, cfg);
-      for (std::size_t i = 0; i < h1.data.size(); ++i) {
-        const float a = h1.data[i];
-        h1.data[i] = a / (1.0f + std::exp(-a)) * h3.data[i];
+        std::memcpy(&xe[e].data[i * d], x + rows[i] * d, d * 4);
+      const std::size_t f = experts[e].l[0].w.cols;
+      h1[e] = WeightMatrix(rows.size(), f);
+      h3[e] = WeightMatrix(rows.size(), f);
+      y[e] = WeightMatrix(rows.size(), d);
+    }
+    auto run_slice = [&](const RefLinear& L, std::size_t s, const WeightMatrix& a, WeightMatrix& c) {
+      const WeightMatrix part = gemm_w3a16(a, L.ws[s], L.cs[s], cfg);
+      const std::size_t w = L.c0[s + 1] - L.c0[s];
+      for (std::size_t i = 0; i < a.rows; ++i)
+        std::memcpy(&c.data[i * c.cols + L.c0[s]], &part.data[i * w], w * 4);
+    };
+    // phase 1: (expert, w1 | w3, slice)
+    std::vector<std::array<std::size_t, 3>> jobs;
+    for (std::size_t e : active)
+      for (std::size_t j = 0; j < 2; ++j)
+        for (std::size_t s = 0; s < experts[e].l[j].n_slices; ++s) jobs.push_back({e, j, s});
+    parallel_for(jobs.size(), workers, [&](std::size_t i) {
+      const auto [e, j, s] = jobs[i];
+      run_slice(experts[e].l[j], s, xe[e], j == 0 ? h1[e] : h3[e]);
+    });
+    for (std::size_t e : active)
+      for (std::size_t i = 0; i < h1[e].data.size(); ++i) {
+        const float a = h1[e].data[i];
+        h1[e].data[i] = a / (1.0f + std::exp(-a)) * h3[e].data[i];
       }
-      y[e] = gemm_w3a16(h1, ex.l[2].w, ex.l[2].comp, cfg);
+    // phase 2: (expert, w2, slice)
+    jobs.clear();
+    for (std::size_t e : active)
+      for (std::size_t s = 0; s < experts[e].l[2].n_slices; ++s) jobs.push_back({e, 2, s});
+    parallel_for(jobs.size(), workers, [&](std::size_t i) {
+      const auto [e, j, s] = jobs[i];
+      run_slice(experts[e].l[2], s, h1[e], y[e]);
     });
     std::vector<std::size_t> cursor(E, 0);
     std::fill(out, out + m * d, 0.0f);

@@ -203,3 +203,20 @@ def test_restatement_matches_compiled_reference_directly(oracle, ref):
         a = oracle.gemm_w3a16(A, P, comp, cfg)
         b = ref.gemm_w3a16(A, P, comp, cfg)
         assert (a.view(np.uint32) == b.view(np.uint32)).all()
+
+
+def test_reference_moe_column_slices_are_bit_identical(oracle, ref, g):
+    """bench.py's reference arm cuts every matrix into column slices so all host
+    threads work at batch 1 (oracle/ref/ref_capi.cpp ref_moe_forward); the
+    reference's columns are independent, so any slice count must give the same
+    bits as the unsliced composition, which equals the golden MoE output."""
+    from oracle.oracle import RefMoE
+    routed, shared = _moe_experts(g)
+    ids, w = oracle.router_topk(g["moe_logits"], int(g["moe_meta"][3]), 0)
+    outs = []
+    for workers in (1, 2, 3, 8):
+        h = RefMoE(ref, routed, shared, workers)
+        outs.append(h.forward(g["moe_x"], ids, w))
+        h.close()
+    for o in outs:
+        assert (o.view(np.uint32) == g["moe_out"].view(np.uint32)).all()
