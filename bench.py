@@ -233,7 +233,8 @@ def main():
     ap.add_argument("--batch", type=int, default=1)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-sweep", action="store_true")
-    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline timing")
+    ap.add_argument("--no-parity", action="store_true", help="skip the reference parity check")
     ap.add_argument("--ep", action="store_true", help="expert-parallel layer (default when N > 1)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -428,7 +429,7 @@ def main():
 
     # ---------------- CPU reference: parity of a timed step + baseline (rank 0) ----------------
     cpu = parity = None
-    if rank == 0 and not args.no_cpu:
+    if rank == 0 and not args.no_parity:
         try:
             ref = CpuReference(spec, routed_h, shared_h)
             got, hx0, hl0 = first_step
@@ -437,7 +438,7 @@ def main():
             parity = {"rel_err": float(np.sqrt(((got.astype(np.float64) - want) ** 2).sum()) / den),
                       "ids_equal": bool(np.array_equal(ids_np[0], ref_ids)), "tol": 2.5e-4,
                       "against": ref.kind, "step": "first timed step (same x / logits, fp32 out)"}
-            if ws == 1:
+            if ws == 1 and not args.no_cpu:
                 cpu_steps = 3
                 hx, hl = host_inputs(spec, m, cpu_steps, input_seed(args, m) + 7)
                 us = ref.time(hx, hl)
