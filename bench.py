@@ -411,6 +411,38 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_us = float(t.item())
 
+    # ---------------- configs[0]: the single 4096 x 14336 linear, r = 32 (N=1) ----------------
+    c1 = []
+    if not args.no_sweep and ws == 1 and args.config == "mixtral":
+        from paper_2504_02658_b200.pack import random_compensator
+        from paper_2504_02658_b200.synth import matrix_memory_bytes, packed_random_words
+        rng1 = np.random.default_rng(args.seed + 4242)
+        k1, n1, r1 = 4096, 14336, 32
+        W1 = mb.Weight(packed_random_words(k1, n1, rng1))
+        C1 = mb.Comp(random_compensator(k1, n1, r1, rng1))
+        for mm in (1, 16, 64, 256):
+            A1 = torch.from_numpy(np.random.default_rng(mm).normal(0, 1, (mm, k1)).astype(np.float16)).cuda()
+            o1 = torch.empty(mm, n1, device="cuda", dtype=torch.float32)
+            for _ in range(3):
+                mb.gemm_w3a16(A1, W1, C1, out=o1)
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(10)]
+            torch.cuda.synchronize()
+            for s_, e_ in ev:
+                flush_l2()
+                s_.record(stream)
+                mb.gemm_w3a16(A1, W1, C1, out=o1)
+                e_.record(stream)
+            torch.cuda.synchronize()
+            us = float(np.mean([s_.elapsed_time(e_) for s_, e_ in ev])) * 1e3
+            b = matrix_memory_bytes(k1, n1, r1) + 2 * mm * k1 + 4 * mm * n1
+            fl = 2 * mm * k1 * n1 + 2 * mm * r1 * (k1 + n1)
+            t_roof = max(b / (hbm * 1e9), fl / (float(peaks["bf16_tflops"]) * 1e12)) * 1e6
+            c1.append({"batch": mm, "us": round(us, 2), "GBps": round(b / us / 1e3, 1),
+                       "TFLOPs": round(fl / us / 1e6, 2), "roofline_us": round(t_roof, 2),
+                       "roofline_frac": round(t_roof / us, 3),
+                       "kernel": "decode_kernel (mma.sync)" if mm <= 16 else "pf_gemm_kernel (tcgen05)"})
+        del W1, C1
+
     # ---------------- batch sweep (N=1) ----------------
     sweep = []
     if not args.no_sweep and ws == 1:
@@ -480,6 +512,8 @@ def main():
         "cpu_baseline": cpu,
         "parity": parity,
         "sweep": sweep,
+        "c1_linear": {"workload": "configs[0]: single INT3 linear 4096x14336, g64, rank-32 LoRC, fp32 out",
+                      "sweep": c1} if c1 else None,
     }
     print(json.dumps(line), flush=True)
     if dist.is_initialized():

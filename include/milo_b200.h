@@ -202,6 +202,21 @@ milo_status milo_moe_forward(milo_moe* moe, const void* x, int64_t m, int32_t x_
 milo_status milo_moe_forward_routed(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype,
                                     const int32_t* topk_ids, const float* topk_w, void* out,
                                     int32_t out_dtype, void* stream);
+/* The MoE gate (router GEMM, x W_gate): logits[t][e] = sum_k half(x[t][k]) *
+ * gate[e][k] in fp32, in a fixed order restated bit-exactly by the oracle
+ * (oracle/milo_oracle.c or_router_gemm).  x: m x d (x_dtype) device rows,
+ * gate: E x d binary16 (device), logits: m x E fp32 (device). */
+milo_status milo_router_gemm(const void* x, int64_t m, int64_t d, int32_t x_dtype, const uint16_t* gate,
+                             int32_t n_experts, float* logits, void* stream);
+/* Attaches the gate weights (E x d binary16 bits, host memory; uploaded,
+ * blocking) to a layer so that milo_moe_forward_x routes from x itself.
+ * MILO_ERR_SHAPE unless E and d are the layer's. */
+milo_status milo_moe_set_gate(milo_moe* moe, const uint16_t* gate, int64_t n_experts, int64_t d);
+/* The whole MoE block from x: router GEMM -> top-k -> experts -> combine.
+ * MILO_ERR_CONFIG if no gate was attached.  topk_ids / topk_w optional. */
+milo_status milo_moe_forward_x(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype, void* out,
+                               int32_t out_dtype, int32_t* topk_ids, float* topk_w, void* stream);
+
 /* Host-buffer end-to-end call: x (m x x_cols f32) and logits (m x logit_cols
  * f32) in host memory, out (m x d f32) host; blocking.  MILO_ERR_SHAPE unless
  * x_cols == d and logit_cols == E (checked before any buffer is touched). */

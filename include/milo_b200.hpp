@@ -269,6 +269,16 @@ class MoELayer {
                                 static_cast<int64_t>(router_logits.cols), out.data.data()));
     return out;
   }
+  // The router gate (E x d binary16 bits, host), then forward_x routes from x itself.
+  void set_gate(const std::vector<std::uint16_t>& gate, int64_t n_experts, int64_t d) {
+    if (gate.size() != static_cast<std::size_t>(n_experts * d)) throw ShapeError("gate size != E * d");
+    check(milo_moe_set_gate(h_.get(), gate.data(), n_experts, d));
+  }
+  // Device buffers, stream-ordered: router GEMM -> top-k -> experts -> combine.
+  void forward_x(const void* x, int64_t m, milo_dtype x_dtype, void* out, milo_dtype out_dtype,
+                 void* stream) const {
+    check(milo_moe_forward_x(h_.get(), x, m, x_dtype, out, out_dtype, nullptr, nullptr, stream));
+  }
   // Device buffers, stream-ordered.
   void forward(const void* x, int64_t m, milo_dtype x_dtype, const float* logits, void* out,
                milo_dtype out_dtype, void* stream) const {

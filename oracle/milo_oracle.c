@@ -547,6 +547,28 @@ uint64_t or_matrix_memory_bytes(uint64_t rows, uint64_t cols, uint64_t rank, int
 /* MoE layer (new, see header)                                                  */
 /* ------------------------------------------------------------------------- */
 
+void or_router_gemm(const float* x, uint64_t m, uint64_t d, const uint16_t* gate, int E, float* logits) {
+  for (uint64_t t = 0; t < m; ++t)
+    for (int e = 0; e < E; ++e) {
+      float lane[32];
+      for (int l = 0; l < 32; ++l) {
+        float acc = 0.0f;
+        for (uint64_t k = (uint64_t)l; k < d; k += 32) {
+          const float a = or_half_to_float(or_float_to_half(x[t * d + k]));
+          const float g = or_half_to_float(gate[(uint64_t)e * d + k]);
+          acc = fmaf(a, g, acc);  /* the product is exact: one rounding, like the device FFMA */
+        }
+        lane[l] = acc;
+      }
+      for (int off = 16; off > 0; off >>= 1) {
+        float nxt[32];
+        for (int l = 0; l < 32; ++l) nxt[l] = lane[l] + lane[l ^ off];
+        memcpy(lane, nxt, sizeof(lane));
+      }
+      logits[t * (uint64_t)E + (uint64_t)e] = lane[0];
+    }
+}
+
 void or_router_topk(const float* logits, uint64_t m, int E, int K, int score_mode,
                     int32_t* ids, float* wts) {
   float* p = (float*)malloc((size_t)E * 4);

@@ -129,6 +129,11 @@ uint64_t or_matrix_memory_bytes(uint64_t rows, uint64_t cols, uint64_t rank, int
  *   score_mode 1 (DeepSeek): weights = softmax over all E logits, taken at the
  *                            top-k ids, not renormalized.
  * Softmax: w_i = exp(l_i - max) / sum_j exp(l_j - max), fp32, sum ascending. */
+/* The MoE gate, logits = half(x) W_gate^T (m x E), in the device's exact
+ * fp32 order: per (t, e), 32 lane sums over k = l (mod 32) ascending, then the
+ * xor tree 16, 8, 4, 2, 1 (paper_2504_02658_b200/csrc/moe.cuh
+ * router_gemm_kernel).  gate: E x d binary16 bits. */
+void or_router_gemm(const float* x, uint64_t m, uint64_t d, const uint16_t* gate, int E, float* logits);
 void or_router_topk(const float* logits, uint64_t m, int E, int K, int score_mode,
                     int32_t* topk_ids, float* topk_w);
 

@@ -190,6 +190,7 @@ class Oracle:
                                                    C.POINTER(_ORComp), C.POINTER(_ORCfg), f32p])
             self._ptc = self._f("pipeline_tail_check", i, [u64, C.POINTER(_ORCfg), i32p, i, i32p])
             self._router = self._f("router_topk", None, [f32p, u64, i, i, i, i32p, f32p])
+            self._rgemm = self._f("router_gemm", None, [f32p, u64, u64, u16p, i, f32p])
             self._moe = self._f("moe_forward", i, [C.POINTER(_ORExpert), i, C.POINTER(_ORExpert), i,
                                                    f32p, u64, u64, i, i32p, f32p, i, f32p])
         else:
@@ -421,6 +422,17 @@ class Oracle:
         return int(self._fnv(s.encode()))
 
     # ---- MoE (new layer, defined in milo_oracle.h) ----------------------------
+    def router_gemm(self, x: np.ndarray, gate_bits: np.ndarray) -> np.ndarray:
+        """The MoE gate in the device's exact fp32 order (or_router_gemm)."""
+        assert self.which == "oracle"
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        g = np.ascontiguousarray(gate_bits, dtype=np.uint16)
+        m, d = x.shape
+        E = g.shape[0]
+        out = np.zeros((m, E), np.float32)
+        self._rgemm(_p(x, f32p), m, d, _p(g, u16p), E, _p(out, f32p))
+        return out
+
     def router_topk(self, logits: np.ndarray, K: int, score_mode: int = 0):
         assert self.which == "oracle"
         logits = np.ascontiguousarray(logits, dtype=np.float32)

@@ -139,6 +139,9 @@ def lib() -> C.CDLL:
         "milo_moe_forward_routed": [vp, vp, i64, i32, vp, vp, vp, i32, vp],
         "milo_moe_forward_host": [vp, f32p, i64, i64, f32p, i64, f32p],
         "milo_stream_release": [vp],
+        "milo_router_gemm": [vp, i64, i64, i32, vp, i32, vp, vp],
+        "milo_moe_set_gate": [vp, u16p, i64, i64],
+        "milo_moe_forward_x": [vp, vp, i64, i32, vp, i32, vp, vp, vp],
         "milo_packed_load_host": [C.c_char_p, C.POINTER(_PackedDesc), C.POINTER(vp)],
         "milo_weight_load": [C.c_char_p, C.POINTER(vp)],
         "milo_comp_load": [C.c_char_p, C.c_char_p, C.POINTER(vp)],
@@ -438,6 +441,22 @@ class Expert:
         return _ExpertDesc(h(self.w1), h(self.w3), h(self.w2), h(self.c1), h(self.c3), h(self.c2))
 
 
+def router_gemm(x, gate, stream=None):
+    """The MoE gate on the device: logits (m, E) fp32 = half(x) gate^T, gate a
+    (E, d) float16 CUDA tensor (fixed fp32 order, oracle/milo_oracle.c or_router_gemm)."""
+    import torch
+    x = x.contiguous()
+    gate = gate.contiguous().half()
+    m, d = x.shape
+    E = gate.shape[0]
+    if gate.shape[1] != d:
+        raise ShapeError(f"gate {tuple(gate.shape)} vs x {tuple(x.shape)}")
+    logits = torch.empty((m, E), dtype=torch.float32, device=x.device)
+    _check(lib().milo_router_gemm(_dptr(x), m, d, F32 if x.dtype == torch.float32 else F16, _dptr(gate), E,
+                                  _dptr(logits), _stream_ptr(stream)))
+    return logits
+
+
 def router_topk(logits, top_k: int, score_mode: int = SCORE_SOFTMAX_TOPK, stream=None):
     import torch
     logits = logits.contiguous().float()
@@ -483,6 +502,31 @@ class MoELayer:
                                       F32 if out_dtype == torch.float32 else F16,
                                       _dptr(ids) if ids is not None else None,
                                       _dptr(w) if w is not None else None, _stream_ptr(stream)))
+        return (out, ids, w) if return_routing else out
+
+    def set_gate(self, gate):
+        """Attaches the router gate: (E, d) float16 values (numpy or torch, host or device)."""
+        g = gate.detach().cpu().numpy() if hasattr(gate, "detach") else np.asarray(gate)
+        g = np.ascontiguousarray(g.astype(np.float16)).view(np.uint16)
+        if g.ndim != 2:
+            raise ShapeError("gate must be (E, d)")
+        _check(lib().milo_moe_set_gate(self._h, _np_ptr(g, u16p), g.shape[0], g.shape[1]))
+
+    def forward_x(self, x, out_dtype=None, return_routing=False, stream=None):
+        """The whole MoE block from x: router GEMM (set_gate) -> top-k -> experts -> combine."""
+        import torch
+        x = x.contiguous()
+        m = x.shape[0]
+        out_dtype = out_dtype or torch.float32
+        out = torch.empty((m, self.d), dtype=out_dtype, device=x.device)
+        ids = w = None
+        if return_routing:
+            ids = torch.empty((m, self.top_k), dtype=torch.int32, device=x.device)
+            w = torch.empty((m, self.top_k), dtype=torch.float32, device=x.device)
+        _check(lib().milo_moe_forward_x(self._h, _dptr(x), m, F32 if x.dtype == torch.float32 else F16, _dptr(out),
+                                        F32 if out_dtype == torch.float32 else F16,
+                                        _dptr(ids) if ids is not None else None,
+                                        _dptr(w) if w is not None else None, _stream_ptr(stream)))
         return (out, ids, w) if return_routing else out
 
     def forward_routed(self, x, topk_ids, topk_w, out_dtype=None, stream=None):

@@ -1507,6 +1507,7 @@ struct milo_moe {
   void* dev_stage = nullptr;
   size_t stage_bytes = 0;
   std::mutex stage_mu;  // the staging is per handle; handles may be shared across threads
+  __half* gate = nullptr;  // optional router gate, E x d binary16 (milo_moe_set_gate)
 };
 
 extern "C" milo_status milo_moe_create(const milo_expert_desc* experts, int32_t n_experts,
@@ -1612,6 +1613,7 @@ extern "C" milo_status milo_moe_destroy(milo_moe* moe) {
   cudaFree(moe->dec_experts);
   if (moe->host_stage) cudaFreeHost(moe->host_stage);
   if (moe->dev_stage) cudaFree(moe->dev_stage);
+  if (moe->gate) cudaFree(moe->gate);
   delete moe;
   return MILO_OK;
 }
@@ -2161,6 +2163,53 @@ extern "C" milo_status milo_ep_combine(const float* y, const int32_t* slot, cons
 }
 
 constexpr size_t kHostZeroCopyMax = 256 * 1024;  // output bytes written over the host link directly
+
+extern "C" milo_status milo_router_gemm(const void* x, int64_t m, int64_t d, int32_t x_dtype, const uint16_t* gate,
+                                        int32_t E, float* logits, void* stream) {
+  if (m < 0 || d < 1 || E < 1) return fail(MILO_ERR_SHAPE, "router gemm: bad shape");
+  if (x_dtype != MILO_F32 && x_dtype != MILO_F16) return fail(MILO_ERR_ARGUMENT, "router gemm: x dtype");
+  if (m == 0) return MILO_OK;
+  if (!x || !gate || !logits) return fail(MILO_ERR_ARGUMENT, "null argument");
+  const int warps = 8;
+  const int64_t outs = m * E;
+  CUDA_TRY(launch(router_gemm_kernel, dim3((unsigned)((outs + warps - 1) / warps)), dim3(32 * warps), 0,
+                  (cudaStream_t)stream, true, x, x_dtype, d, m, d, reinterpret_cast<const __half*>(gate), E, logits));
+  return MILO_OK;
+}
+
+extern "C" milo_status milo_moe_set_gate(milo_moe* moe, const uint16_t* gate, int64_t E, int64_t d) {
+  if (!moe || !gate) return fail(MILO_ERR_ARGUMENT, "null argument");
+  if (E != moe->E || d != moe->d)
+    return fail(MILO_ERR_SHAPE, "gate is %lld x %lld, the layer needs %d x %d", (long long)E, (long long)d, moe->E,
+                moe->d);
+  void* g = nullptr;
+  CUDA_TRY(cudaMalloc(&g, (size_t)E * d * 2));
+  const cudaError_t e = cudaMemcpy(g, gate, (size_t)E * d * 2, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    cudaFree(g);
+    return fail(MILO_ERR_CUDA, "%s", cudaGetErrorString(e));
+  }
+  if (moe->gate) cudaFree(moe->gate);
+  moe->gate = static_cast<__half*>(g);
+  return MILO_OK;
+}
+
+extern "C" milo_status milo_moe_forward_x(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype, void* out,
+                                          int32_t out_dtype, int32_t* topk_ids, float* topk_w, void* stream_) {
+  if (!moe) return fail(MILO_ERR_ARGUMENT, "null moe");
+  if (!moe->gate || moe->E == 0) return fail(MILO_ERR_CONFIG, "no router gate attached (milo_moe_set_gate)");
+  if (m < 0) return fail(MILO_ERR_SHAPE, "negative token count");
+  if (m == 0) return MILO_OK;
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  float* logits = nullptr;  // per-call, stream-ordered
+  CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&logits), (size_t)m * moe->E * 4, stream));
+  milo_status st = milo_router_gemm(x, m, moe->d, x_dtype, reinterpret_cast<const uint16_t*>(moe->gate), moe->E,
+                                    logits, stream);
+  if (st == MILO_OK) st = milo_moe_forward(moe, x, m, x_dtype, logits, out, out_dtype, topk_ids, topk_w, stream);
+  const cudaError_t e = cudaFreeAsync(logits, stream);
+  if (st == MILO_OK && e != cudaSuccess) st = fail(MILO_ERR_CUDA, "%s", cudaGetErrorString(e));
+  return st;
+}
 
 extern "C" milo_status milo_moe_forward_host(milo_moe* moe, const float* x, int64_t m, int64_t x_cols,
                                              const float* logits, int64_t logit_cols, float* out) {

@@ -87,6 +87,35 @@ __global__ void router_topk_kernel(const float* __restrict__ logits, int64_t m, 
   topk_warp(logits + t * E, t, E, K, score_mode, ids, wts, threadIdx.x & 31);
 }
 
+// Router GEMM (the MoE gate, x W_gate): logits[t][e] = sum_k half(x[t][k]) *
+// gate[e][k] in fp32.  Bit-exact order, restated in oracle/milo_oracle.c
+// (or_router_gemm): lane l of the warp owning (t, e) sums the products of
+// k = l, l + 32, ... in ascending k (each product of two binary16 values is
+// exact in fp32), then the 32 lane sums meet in the xor tree 16, 8, 4, 2, 1.
+// The gate rows (E x d binary16) are read once per token block from L2.
+__global__ void router_gemm_kernel(const void* __restrict__ x, int32_t x_dtype, int64_t ldx, int64_t m,
+                                   int64_t d, const __half* __restrict__ gate, int32_t E,
+                                   float* __restrict__ logits) {
+  const int warps = blockDim.x >> 5, lane = threadIdx.x & 31;
+  const int64_t o = (int64_t)blockIdx.x * warps + (threadIdx.x >> 5);  // output index t * E + e
+  if (o >= m * E) return;
+  const int64_t t = o / E;
+  const int e = (int)(o - t * E);
+  const __half* g = gate + (int64_t)e * d;
+  float acc = 0.0f;
+  if (x_dtype == 0) {
+    const float* xr = static_cast<const float*>(x) + t * ldx;
+    for (int64_t k = lane; k < d; k += 32)
+      acc = __fmaf_rn(__half2float(__float2half_rn(xr[k])), __half2float(g[k]), acc);
+  } else {
+    const __half* xr = static_cast<const __half*>(x) + t * ldx;
+    for (int64_t k = lane; k < d; k += 32) acc = __fmaf_rn(__half2float(xr[k]), __half2float(g[k]), acc);
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (lane == 0) logits[o] = acc;
+}
+
 // ---------------------------------------------------------------------------
 // routing -> problem tables
 // ---------------------------------------------------------------------------

@@ -304,3 +304,34 @@ def test_host_entry_shape_errors(gpu, oracle):
     with pytest.raises(gpu.ShapeError):
         layer.forward_host(x, np.zeros((2, E), np.float32))
     assert layer.forward_host(x, lg).shape == (3, d)
+
+
+@pytest.mark.parametrize("m,x16", [(1, False), (7, True), (40, False), (130, True)])
+def test_router_gemm_bit_exact_and_forward_x(gpu, oracle, m, x16):
+    """The MoE gate on the device (router_gemm_kernel) gives the oracle's logits
+    bit for bit (same fixed fp32 order), so the routing ids of forward_x are
+    the oracle's; the layer output matches the oracle's composition."""
+    import torch
+    E, K, d, f = 8, 2, 256, 512
+    ranks = [[(8 * ((e + j) % 4)) for j in range(3)] for e in range(E)]
+    o_ex, g_ex = _experts(oracle, gpu, E, d, f, ranks, seed=140)
+    rng = np.random.default_rng(900 + m)
+    x = rng.normal(0, 1, (m, d)).astype(np.float32)
+    gate = rng.normal(0, 0.05, (E, d)).astype(np.float16)
+    want_logits = oracle.router_gemm(x, gate.view(np.uint16))
+    xt = torch.from_numpy(x).cuda()
+    if x16:
+        xt = xt.half()
+    got_logits = gpu.router_gemm(xt, torch.from_numpy(gate).cuda()).cpu().numpy()
+    assert np.array_equal(got_logits.view(np.uint32), want_logits.view(np.uint32))
+    ids, w = oracle.router_topk(want_logits, K, 0)
+    want = oracle.moe_forward(o_ex, [], x, ids, w)
+    layer = gpu.MoELayer(g_ex, [], top_k=K, score_mode=0)
+    with pytest.raises(gpu.ConfigError):
+        layer.forward_x(xt)
+    with pytest.raises(gpu.ShapeError):
+        layer.set_gate(gate[:, :64])
+    layer.set_gate(gate)
+    out, gids, gw = layer.forward_x(xt, return_routing=True)
+    assert np.array_equal(gids.cpu().numpy(), ids)
+    assert rel_err(out.cpu().numpy(), want) <= 2.5e-4

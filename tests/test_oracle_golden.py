@@ -220,3 +220,17 @@ def test_reference_moe_column_slices_are_bit_identical(oracle, ref, g):
         h.close()
     for o in outs:
         assert (o.view(np.uint32) == g["moe_out"].view(np.uint32)).all()
+
+
+def test_router_gemm_restatement_is_a_dot_product(oracle):
+    """or_router_gemm (the MoE gate in the device's fixed fp32 order) is the
+    product half(x) W_gate^T up to fp32 summation: checked against float64."""
+    rng = np.random.default_rng(12)
+    for m, d, E in [(1, 4096, 8), (5, 2048, 64), (3, 96, 4)]:
+        x = rng.normal(0, 1, (m, d)).astype(np.float32)
+        gate = (rng.normal(0, 0.02, (E, d))).astype(np.float16)
+        got = oracle.router_gemm(x, gate.view(np.uint16))
+        want = x.astype(np.float16).astype(np.float64) @ gate.astype(np.float64).T
+        assert np.allclose(got, want, rtol=1e-5, atol=1e-6 * np.abs(want).max())
+        # lane-order arithmetic: exactly reproducible
+        assert np.array_equal(got, oracle.router_gemm(x, gate.view(np.uint16)))
