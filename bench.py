@@ -270,11 +270,13 @@ def main():
     if use_ep:
         # expert parallel: rank r owns experts [r E / N, (r + 1) E / N),
         # tokens move over NCCL all-to-all-v; m tokens per rank (weak scaling)
-        from paper_2504_02658_b200.ep import MiloEPLayer
+        # the C++ layer over NCCL: router, dispatch, grouped ncclSend / ncclRecv exchanges,
+        # owned experts, shared experts and combine in one stream-ordered call
+        from paper_2504_02658_b200.ep import NativeEPLayer
         per = (spec.experts + ws - 1) // ws
         owned = [dev_expert(h) for h in routed_h[rank * per:(rank + 1) * per]]
-        layer = MiloEPLayer(owned, shared, spec.experts, spec.top_k, spec.score_mode)
-        layer.ep.uniform_batch = True  # every rank runs the same batch (weak scaling by tokens)
+        layer = NativeEPLayer(owned, shared, spec.experts, spec.top_k, spec.score_mode)
+        layer.capacity = 0  # every rank runs the same batch (weak scaling by tokens): C = m K
     else:
         experts = [dev_expert(h) for h in routed_h]
         layer = mb.MoELayer(experts, shared, top_k=spec.top_k, score_mode=spec.score_mode)
@@ -318,8 +320,13 @@ def main():
             flush_l2()
             s, e = evs[i]
             s.record(stream)
-            o, ids, _ = layer.forward(xs[warmup + i], ls[warmup + i], return_routing=True)
-            e.record(stream)
+            if use_ep:  # routing ids for the byte accounting are taken outside the events
+                o = layer.forward(xs[warmup + i], ls[warmup + i])
+                e.record(stream)
+                ids = mb.router_topk(ls[warmup + i], spec.top_k, spec.score_mode)[0]
+            else:
+                o, ids, _ = layer.forward(xs[warmup + i], ls[warmup + i], return_routing=True)
+                e.record(stream)
             ids_all.append(ids)
             if keep_first and i == 0:
                 first = (o, hx[warmup], hl[warmup])

@@ -259,6 +259,28 @@ milo_status milo_ep_combine(const float* y, const int32_t* slot, const float* wt
  * stream allocates them again. */
 milo_status milo_stream_release(void* stream);
 
+/* ------------------------------------- expert-parallel layer (NCCL, new)
+ * Rank r of W owns routed experts [r*per, (r+1)*per), per = ceil(E / W);
+ * shared experts are replicated.  NCCL is resolved at run time (libnccl.so.2
+ * already loaded into the process, else dlopen); without it these return
+ * MILO_ERR_CUDA.  comm is an ncclComm_t (the caller's, or milo_ep_comm_create
+ * from an id made by milo_ep_unique_id on one rank and broadcast). */
+typedef struct milo_ep_layer milo_ep_layer;
+milo_status milo_ep_unique_id(uint8_t* id, int64_t id_bytes); /* id_bytes >= 128 */
+milo_status milo_ep_comm_create(const uint8_t* id, int32_t world, int32_t rank, void** comm);
+milo_status milo_ep_comm_destroy(void* comm);
+/* local: a layer over this rank's owned experts with top_k = 1 (NULL if it owns
+ * none); shared: a layer holding only the shared experts (NULL if none). */
+milo_status milo_ep_layer_create(milo_moe* local, milo_moe* shared, int32_t n_experts, int32_t top_k,
+                                 int32_t score_mode, void* comm, milo_ep_layer** out);
+milo_status milo_ep_layer_destroy(milo_ep_layer* layer);
+/* One layer call on this rank's m tokens (x m x d, logits m x E fp32, out m x d
+ * fp32, device).  Fixed-capacity exchange: capacity rows per peer, >= m * top_k
+ * on every rank and equal across ranks (<= 0: m * top_k, equal batches).
+ * Stream-ordered; every rank of the communicator must call it. */
+milo_status milo_ep_forward(milo_ep_layer* layer, const void* x, int64_t m, int32_t x_dtype, const float* logits,
+                            float* out, int32_t capacity, void* stream);
+
 /* Kernel launches recorded by this library on the calling thread (for the
  * bench's gpu_launches claim). */
 uint64_t milo_launch_count(void);

@@ -139,6 +139,12 @@ def lib() -> C.CDLL:
         "milo_moe_forward_routed": [vp, vp, i64, i32, vp, vp, vp, i32, vp],
         "milo_moe_forward_host": [vp, f32p, i64, i64, f32p, i64, f32p],
         "milo_stream_release": [vp],
+        "milo_ep_unique_id": [vp, i64],
+        "milo_ep_comm_create": [vp, i32, i32, C.POINTER(vp)],
+        "milo_ep_comm_destroy": [vp],
+        "milo_ep_layer_create": [vp, vp, i32, i32, i32, vp, C.POINTER(vp)],
+        "milo_ep_layer_destroy": [vp],
+        "milo_ep_forward": [vp, vp, i64, i32, vp, vp, i32, vp],
         "milo_router_gemm": [vp, i64, i64, i32, vp, i32, vp, vp],
         "milo_moe_set_gate": [vp, u16p, i64, i64],
         "milo_moe_forward_x": [vp, vp, i64, i32, vp, i32, vp, vp, vp],

@@ -17,6 +17,7 @@
 #include <string>
 #include <utility>
 #include <vector>
+#include <type_traits>
 
 #include <cuda_fp16.h>
 
@@ -2158,7 +2159,7 @@ extern "C" milo_status milo_ep_combine(const float* y, const int32_t* slot, cons
   if (d % 4 != 0) return fail(MILO_ERR_SHAPE, "d must be a multiple of 4");
   const int64_t total = m * (d / 4);
   CUDA_TRY(launch(ep_combine_kernel, dim3((unsigned)std::min<int64_t>((total + 255) / 256, 1184)), dim3(256), 0,
-                  (cudaStream_t)stream, false, y, slot, wts, m, K, d, out));
+                  (cudaStream_t)stream, false, y, slot, wts, m, K, d, out, (const float*)nullptr));
   return MILO_OK;
 }
 
@@ -2619,3 +2620,6 @@ milo_status milo_comp_load(const char* u_path, const char* v_path, milo_comp** o
 }
 
 }  // extern "C"
+
+// Expert-parallel layer over NCCL (include/milo_b200.h milo_ep_*).
+#include "ep_nccl.cuh"

@@ -481,9 +481,10 @@ __global__ void ep_dispatch_kernel(const int32_t* __restrict__ ids, int32_t mK, 
 }
 
 // out[t] = sum_k w[t,k] y[slot[t K + k]] (k order, moe_combine semantics), f32.
+// extra (nullable): m x d f32 added after the routed sum (the shared experts).
 __global__ void ep_combine_kernel(const float* __restrict__ y, const int32_t* __restrict__ slot,
                                   const float* __restrict__ wts, int64_t m, int32_t K, int64_t d,
-                                  float* __restrict__ out) {
+                                  float* __restrict__ out, const float* __restrict__ extra) {
   const int64_t total = m * (d / 4);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t t = i / (d / 4), c4 = i % (d / 4);
@@ -498,7 +499,31 @@ __global__ void ep_combine_kernel(const float* __restrict__ y, const int32_t* __
       acc.z += w * v.z;
       acc.w += w * v.w;
     }
+    if (extra != nullptr) {
+      const float4 v = reinterpret_cast<const float4*>(extra)[i];
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    }
     reinterpret_cast<float4*>(out)[i] = acc;
+  }
+}
+
+// Received EP rows (ld halves, the local expert id as int32 at half-column d)
+// -> contiguous binary16 rows + ids + unit weights for the local grouped call.
+__global__ void ep_unpack_kernel(const __half* __restrict__ recv, int64_t rows, int64_t d, int64_t ld,
+                                 __half* __restrict__ x, int32_t* __restrict__ lids, float* __restrict__ ones) {
+  const int64_t d8 = d / 8;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows * (d8 + 1);
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / (d8 + 1), c = i % (d8 + 1);
+    if (c < d8) {
+      reinterpret_cast<uint4*>(x + r * d)[c] = reinterpret_cast<const uint4*>(recv + r * ld)[c];
+    } else {
+      lids[r] = *reinterpret_cast<const int32_t*>(recv + r * ld + d);
+      ones[r] = 1.0f;
+    }
   }
 }
 

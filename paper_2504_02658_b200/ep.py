@@ -71,7 +71,8 @@ class ExpertParallelMoE:
         # one small all-reduce unless the caller guarantees equal batches.
         m_max = m
         if self.world > 1 and not self.uniform_batch:
-            t = torch.tensor([m], dtype=torch.int64, device=x.device)
+            on_dev = dist.get_backend(self.group) == "nccl"
+            t = torch.tensor([m], dtype=torch.int64, device=x.device if on_dev else "cpu")
             dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
             m_max = int(t.item())
         if m_max * self.K <= self.fixed_cap_max:
@@ -94,6 +95,18 @@ class ExpertParallelMoE:
         return out
 
     device_kernels = False  # MiloEPLayer: dispatch / combine as CUDA kernels of the library
+    host_exchange = False   # device tensors exchanged through host copies (a gloo group, e.g. tests)
+
+    def _a2a_dev(self, t: torch.Tensor) -> torch.Tensor:
+        """all-to-all of equal splits; through host memory for a CPU backend."""
+        if self.host_exchange:
+            h = t.cpu()
+            r = torch.empty_like(h)
+            dist.all_to_all_single(r, h, group=self.group)
+            return r.to(t.device)
+        r = torch.empty_like(t)
+        dist.all_to_all_single(r, t, group=self.group)
+        return r
 
     def _forward_fixed(self, x, ids, weights, m_max=None):
         """Decode-sized batches: every rank sends a fixed capacity C = m K rows to
@@ -106,13 +119,14 @@ class ExpertParallelMoE:
             import paper_2504_02658_b200 as mb
             # rows and local expert ids in one buffer: one all-to-all for both
             send, _, slot = mb.ep_dispatch(ids, x, W, self.per, C, packed=True)
-            recv = torch.empty_like(send)
-            dist.all_to_all_single(recv, send, group=self.group)
+            recv = self._a2a_dev(send)
             recv_x = recv[:, :self.d].contiguous()
             recv_m = recv[:, self.d:self.d + 2].contiguous().view(torch.int32).view(-1)
-            y_recv = self.local_fn(recv_x, recv_m).to(torch.float32)
-            y_back = torch.empty_like(y_recv)
-            dist.all_to_all_single(y_back, y_recv, group=self.group)
+            if self.local_fn is not None:
+                y_recv = self.local_fn(recv_x, recv_m).to(torch.float32)
+            else:  # this rank owns no routed expert
+                y_recv = torch.zeros((recv_x.shape[0], self.d), dtype=torch.float32, device=x.device)
+            y_back = self._a2a_dev(y_recv.contiguous())
             out = mb.ep_combine(y_back, slot, weights)
             if self.shared_fn is not None:
                 out = out + self.shared_fn(x)
@@ -206,7 +220,7 @@ class MiloEPLayer:
         if self.shared is not None:
             def shared_fn(x):
                 return self.shared.forward(x.contiguous(), None)
-        self.ep = ExpertParallelMoE(n_experts, top_k, self.d, milo_local_fn(self.local),
+        self.ep = ExpertParallelMoE(n_experts, top_k, self.d, milo_local_fn(self.local) if self.local else None,
                                     shared_fn=shared_fn, router_fn=self._route, group=group)
         self.ep.device_kernels = True
 
@@ -225,3 +239,83 @@ class MiloEPLayer:
         ld = torch.from_numpy(router_logits).cuda(non_blocking=True)
         out = self.forward(xd, ld)
         return out.cpu().numpy()
+
+
+class NativeEPLayer:
+    """The expert-parallel layer in the C++ library over NCCL (milo_ep_forward):
+    router, dispatch, the two grouped ncclSend / ncclRecv exchanges, the owned
+    experts and the combine all run stream-ordered inside one C call.
+
+    The NCCL communicator is built from a unique id made on rank 0 and broadcast
+    over `group` (any torch.distributed backend), or passed explicitly as
+    (nccl_id, world, rank) -- world 1 needs no process group at all."""
+
+    def __init__(self, owned, shared, n_experts: int, top_k: int, score_mode: int = 0, group=None,
+                 nccl_id: bytes = None, world: int = None, rank: int = None):
+        import ctypes as C
+        import paper_2504_02658_b200 as mb
+        self.mb = mb
+        if world is None:
+            world = dist.get_world_size(group)
+            rank = dist.get_rank(group)
+        if nccl_id is None:
+            buf = (C.c_uint8 * 128)()
+            if rank == 0:
+                mb._check(mb.lib().milo_ep_unique_id(buf, 128))
+            if world > 1:
+                t = torch.tensor(list(bytes(buf)), dtype=torch.uint8)
+                if dist.get_backend(group) == "nccl":
+                    t = t.cuda()
+                dist.broadcast(t, src=0, group=group)
+                buf = (C.c_uint8 * 128)(*t.cpu().tolist())
+            nccl_id = bytes(buf)
+        idb = (C.c_uint8 * 128)(*nccl_id)
+        comm = C.c_void_p()
+        mb._check(mb.lib().milo_ep_comm_create(idb, world, rank, C.byref(comm)))
+        self._comm = comm
+        self.local = mb.MoELayer(owned, [], top_k=1, score_mode=0) if owned else None
+        self.shared = mb.MoELayer([], shared, top_k=1) if shared else None
+        self.E, self.K, self.world, self.rank = n_experts, top_k, world, rank
+        self.score_mode = score_mode
+        self.d = (owned or shared)[0].w1.rows
+        h = C.c_void_p()
+        mb._check(mb.lib().milo_ep_layer_create(self.local._h if self.local else None,
+                                                self.shared._h if self.shared else None, n_experts, top_k,
+                                                score_mode, comm, C.byref(h)))
+        self._h = h
+        self.capacity = 0  # rows per peer; 0: m * top_k (equal batches on every rank)
+
+    def forward(self, x, router_logits, out_dtype=None, return_routing=False, stream=None):
+        mb = self.mb
+        x = x.contiguous()
+        m = x.shape[0]
+        out = torch.empty((m, self.d), dtype=torch.float32, device=x.device)
+        lg = router_logits.contiguous().float()
+        mb._check(mb.lib().milo_ep_forward(self._h, mb._dptr(x), m, mb.F32 if x.dtype == torch.float32 else mb.F16,
+                                           mb._dptr(lg), mb._dptr(out), int(self.capacity), mb._stream_ptr(stream)))
+        if out_dtype is not None and out_dtype != torch.float32:
+            out = out.to(out_dtype)
+        if return_routing:
+            ids, w = mb.router_topk(lg, self.K, self.score_mode)
+            return out, ids, w
+        return out
+
+    def forward_host(self, x, router_logits):
+        xd = torch.from_numpy(x).cuda(non_blocking=True)
+        ld = torch.from_numpy(router_logits).cuda(non_blocking=True)
+        return self.forward(xd, ld).cpu().numpy()
+
+    def close(self):
+        mb = self.mb
+        if getattr(self, "_h", None):
+            mb.lib().milo_ep_layer_destroy(self._h)
+            self._h = None
+        if getattr(self, "_comm", None):
+            mb.lib().milo_ep_comm_destroy(self._comm)
+            self._comm = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 - interpreter shutdown
+            pass
