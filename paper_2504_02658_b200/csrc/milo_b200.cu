@@ -1142,10 +1142,10 @@ struct ImgTPlan {
       if (e != cudaSuccess) return e;
     }
     e = launch(pf_img_t_kernel, dim3((unsigned)blocks), dim3(256), kImgTSmem, stream, false,
-               (const ImgJob*)table, (int)jobs.size());
+               (const ImgJob*)table, (int)jobs.size(), (const int32_t*)nullptr);
     if (e != cudaSuccess || tps.empty()) return e;
     return launch(pf_t_images_kernel, dim3(256, (unsigned)tps.size()), dim3(256), 0, stream, false,
-                  (const TProb*)(table + jb), (int)tps.size());
+                  (const TProb*)(table + jb), (int)tps.size(), (const int32_t*)nullptr);
   }
 };
 
@@ -1155,10 +1155,11 @@ cudaError_t launch_t_batch(const std::vector<TProb>& v, int units, uint8_t* tabl
   if (v.empty()) return cudaSuccess;
   cudaError_t e = h2d_async(table, v.data(), v.size() * sizeof(TProb), stream);
   if (e != cudaSuccess) return e;
-  e = launch(pf_t_kernel, dim3(units), dim3(256), 0, stream, false, (const TProb*)table, (int)v.size());
+  e = launch(pf_t_kernel, dim3(units), dim3(256), 0, stream, false, (const TProb*)table, (int)v.size(),
+             (const int32_t*)nullptr);
   if (e != cudaSuccess) return e;
   return launch(pf_t_images_kernel, dim3(256, (unsigned)v.size()), dim3(256), 0, stream, false, (const TProb*)table,
-                (int)v.size());
+                (int)v.size(), (const int32_t*)nullptr);
 }
 TProb make_tprob(const void* x, int32_t x_dtype, int64_t ldx, const int32_t* row_ids, int64_t rows, int64_t k,
                  int ntok, const milo_comp* c, uint8_t* timg, float* part, int sms, int unit0, int* units,
@@ -1509,6 +1510,8 @@ struct milo_moe {
   size_t stage_bytes = 0;
   std::mutex stage_mu;  // the staging is per handle; handles may be shared across threads
   __half* gate = nullptr;  // optional router gate, E x d binary16 (milo_moe_set_gate)
+  PfExpertStatic* pf_static = nullptr;  // device: per expert, what moe_plan_kernel needs
+  int32_t rch_max[3] = {0, 0, 0};       // largest 64-rank chunk count per matrix
 };
 
 extern "C" milo_status milo_moe_create(const milo_expert_desc* experts, int32_t n_experts,
@@ -1598,9 +1601,36 @@ extern "C" milo_status milo_moe_create(const milo_expert_desc* experts, int32_t 
   if (err == cudaSuccess)
     err = cudaMemcpy(moe->dec_experts, dhost.data(), dhost.size() * sizeof(DecExpert),
                      cudaMemcpyHostToDevice);
+  {  // the prefill planner's static view (moe_plan_kernel)
+    std::vector<PfExpertStatic> ps(host.size());
+    for (size_t i = 0; i < host.size(); ++i)
+      for (int j = 0; j < 3; ++j) {
+        const milo_weight* w = moe->hw[i][j];
+        const milo_comp* c = moe->hc[i][j];
+        PfMatStatic& M = ps[i].m[j];
+        M.w = w->tiles;
+        M.k = (int32_t)w->rows;
+        M.n = (int32_t)w->cols;
+        M.mode = w->mode;
+        if (c && c->rank > 0) {
+          M.vimg = c->vimg;
+          M.ucodes = c->ucodes;
+          M.uscales = c->uscales;
+          M.ureal = c->ureal;
+          M.rank = (int32_t)c->rank;
+          M.gpr = c->gpr;
+          M.rch = c->rch;
+          moe->rch_max[j] = std::max(moe->rch_max[j], c->rch);
+        }
+      }
+    if (err == cudaSuccess) err = cudaMalloc(&moe->pf_static, ps.size() * sizeof(PfExpertStatic));
+    if (err == cudaSuccess)
+      err = cudaMemcpy(moe->pf_static, ps.data(), ps.size() * sizeof(PfExpertStatic), cudaMemcpyHostToDevice);
+  }
   if (err != cudaSuccess) {
     cudaFree(moe->dev_experts);
     cudaFree(moe->dec_experts);
+    cudaFree(moe->pf_static);
     delete moe;
     return fail(MILO_ERR_CUDA, "expert table upload failed: %s", cudaGetErrorString(err));
   }
@@ -1612,6 +1642,7 @@ extern "C" milo_status milo_moe_destroy(milo_moe* moe) {
   if (!moe) return MILO_OK;
   cudaFree(moe->dev_experts);
   cudaFree(moe->dec_experts);
+  cudaFree(moe->pf_static);
   if (moe->host_stage) cudaFreeHost(moe->host_stage);
   if (moe->dev_stage) cudaFree(moe->dev_stage);
   if (moe->gate) cudaFree(moe->gate);
@@ -2029,6 +2060,124 @@ milo_status moe_prefill(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype
   return st;
 }
 
+// The MoE prefill path with the plan on the device (moe_plan_kernel): router ->
+// plan -> per phase: activation images, LoRC t, the tcgen05 grouped GEMM ->
+// combine, all stream-ordered (no host synchronisation, graph-capturable).
+// Workspace regions are sized here for the worst routing of m tokens; the
+// launches use host grid bounds and read their sizes from the plan.
+milo_status moe_prefill_dev(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype, const float* logits,
+                            int32_t* ids, float* wts, void* out, int32_t out_dtype, cudaStream_t stream, int sms) {
+  const int E = moe->E, K = moe->K, S = moe->n_shared;
+  const int64_t d = moe->d, f_max = moe->f_max;
+  const int64_t G = E + S, R = m * K + (int64_t)S * m;
+  if (G > kPlanMaxGroups) return fail(MILO_ERR_CONFIG, "prefill: more than %d experts", kPlanMaxGroups);
+  if (K > 0 && logits)
+    CUDA_TRY(launch(router_topk_kernel, dim3((unsigned)((m + 7) / 8)), dim3(256), 0, stream, false, logits, m, E, K,
+                    moe->score_mode, ids, wts));
+  // ---- worst-case regions (tiles x ntok <= rows + 127 per group)
+  const int64_t rows_b = R + 127 * G;
+  int64_t kmax[3] = {d, d, 0};
+  for (int i = 0; i < (int)G; ++i) kmax[2] = std::max<int64_t>(kmax[2], (int64_t)moe->hw[i][2]->rows);
+  Arena ar;
+  const size_t o_img0 = ar.take((size_t)rows_b * d * 2 + 256 * G);
+  const size_t o_img1 = ar.take((size_t)rows_b * f_max * 2 + 256 * G);
+  size_t o_timg[3], o_part[3];
+  for (int j = 0; j < 3; ++j) {
+    o_timg[j] = ar.take((size_t)rows_b * moe->rch_max[j] * 256 + 256 * G);
+    o_part[j] = ar.take((size_t)(kmax[j] / kPfK) * R * moe->rch_max[j] * 256 + 256 * G);
+  }
+  const size_t o_h = ar.take((size_t)R * f_max * 2);
+  const size_t o_y = ar.take((size_t)R * d * 4);
+  const size_t o_tok = ar.take((size_t)R * 4);
+  const size_t o_slot = ar.take((size_t)R * 4);
+  size_t o_jobs[2], o_tps[2], o_probs[2], o_starts[2];
+  for (int ph = 0; ph < 2; ++ph) {
+    o_jobs[ph] = ar.take((size_t)G * sizeof(ImgJob));
+    o_tps[ph] = ar.take((size_t)G * (ph == 0 ? 2 : 1) * sizeof(TProb));
+    o_probs[ph] = ar.take((size_t)G * sizeof(PfProblem));
+    o_starts[ph] = ar.take((size_t)(G + 1) * 4);
+  }
+  const size_t o_counts = ar.take(32 * 4);
+  void* mem = nullptr;
+  {
+    const milo_status ws_st = get_pf_ws(stream, ar.size, &mem);
+    if (ws_st != MILO_OK) return ws_st;
+  }
+  uint8_t* b = static_cast<uint8_t*>(mem);
+  PfPlanArgs pa{};
+  pa.ids = ids;
+  pa.m = m;
+  pa.K = K;
+  pa.E = E;
+  pa.S = S;
+  pa.sms = sms;
+  pa.ex = moe->pf_static;
+  pa.x = x;
+  pa.x_dtype = x_dtype;
+  pa.d = d;
+  pa.f_max = f_max;
+  pa.tok = reinterpret_cast<int32_t*>(b + o_tok);
+  pa.slot = reinterpret_cast<int32_t*>(b + o_slot);
+  for (int ph = 0; ph < 2; ++ph) {
+    pa.jobs[ph] = reinterpret_cast<ImgJob*>(b + o_jobs[ph]);
+    pa.tps[ph] = reinterpret_cast<TProb*>(b + o_tps[ph]);
+    pa.probs[ph] = reinterpret_cast<PfProblem*>(b + o_probs[ph]);
+    pa.starts[ph] = reinterpret_cast<int32_t*>(b + o_starts[ph]);
+  }
+  pa.counts = reinterpret_cast<int32_t*>(b + o_counts);
+  pa.img[0] = b + o_img0;
+  pa.img[1] = b + o_img1;
+  for (int j = 0; j < 3; ++j) {
+    pa.timg[j] = b + o_timg[j];
+    pa.part[j] = b + o_part[j];
+  }
+  pa.h = reinterpret_cast<__half*>(b + o_h);
+  pa.Y = reinterpret_cast<float*>(b + o_y);
+  CUDA_TRY(launch(moe_plan_kernel, dim3(1), dim3(1024), 0, stream, false, pa));
+  static thread_local int configured_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured_dev != dev) {
+    CUDA_TRY(cudaFuncSetAttribute(pf_img_t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kImgTSmem));
+    CUDA_TRY(set_smem(pf_gemm_kernel<2, 1>, PfCfg<2, 1>::kBytes));
+    CUDA_TRY(set_smem(pf_gemm_kernel<1, 1>, PfCfg<1, 1>::kBytes));
+    configured_dev = dev;
+  }
+  for (int ph = 0; ph < 2; ++ph) {
+    const int32_t* cnt = pa.counts + 16 * ph;
+    // activation images (+ gathered rows) and LoRC t = x U -> hi / lo images
+    CUDA_TRY(launch(pf_img_t_kernel, dim3((unsigned)(sms * 8)), dim3(256), kImgTSmem, stream, false,
+                    (const ImgJob*)pa.jobs[ph], 0, cnt));
+    CUDA_TRY(launch(pf_t_kernel, dim3((unsigned)(sms * 8)), dim3(256), 0, stream, false, (const TProb*)pa.tps[ph], 0,
+                    cnt + 2));
+    CUDA_TRY(launch(pf_t_images_kernel, dim3(64, (unsigned)std::max<int64_t>(1, G * (ph == 0 ? 2 : 1))), dim3(256),
+                    0, stream, false, (const TProb*)pa.tps[ph], 0, cnt + 2));
+    // the grouped tcgen05 GEMM (persistent grid; items from the plan)
+    PfArgs a{};
+    a.dbg = g_dbg;
+    a.flags = g_dbg_flags;
+    a.problems = pa.probs[ph];
+    a.item_start = pa.starts[ph];
+    a.dev_counts = cnt + 4;
+    a.ntok_max = kPfN;
+    a.n_items = 1;
+    if (ph == 0) {
+      ProfScope ps(kProfGemv1, stream);
+      CUDA_TRY(launch(pf_gemm_kernel<2, 1>, dim3(sms), dim3(PfRoles<2, 1>::kThreads), PfCfg<2, 1>::kBytes, stream,
+                      false, a));
+    } else {
+      ProfScope ps(kProfGemv2, stream);
+      CUDA_TRY(launch(pf_gemm_kernel<1, 1>, dim3(sms), dim3(PfRoles<1, 1>::kThreads), PfCfg<1, 1>::kBytes, stream,
+                      false, a));
+    }
+  }
+  const int64_t total = m * (d / 4);
+  const int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)sms * 8);
+  CUDA_TRY(launch(moe_combine_kernel, dim3(grid), dim3(256), 0, stream, false, (const float*)pa.Y,
+                  (const int32_t*)ids, (const float*)wts, m, K, S, d, out, out_dtype));
+  return MILO_OK;
+}
+
 // logits != nullptr: the route kernel computes the top-k into ids / wts
 // (outputs); otherwise ids / wts are the given routing (inputs).
 milo_status moe_forward_impl(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype,
@@ -2082,7 +2231,11 @@ milo_status moe_forward_impl(milo_moe* moe, const void* x, int64_t m, int32_t x_
   }
   if (!legacy_path() && moe->prefill_ok && m > kDecMaxTok && m >= prefill_min_rows() / 2 &&
       (int64_t)m * std::max(1, moe->K) + (int64_t)moe->n_shared * m < (1 << 30))
-    return moe_prefill(moe, x, m, x_dtype, logits, ids, wts, out, out_dtype, stream, props.sms);
+  {
+    static const bool host_plan = getenv("MILO_PF_HOSTPLAN") != nullptr;  // A/B: the round-1 host planner
+    return host_plan ? moe_prefill(moe, x, m, x_dtype, logits, ids, wts, out, out_dtype, stream, props.sms)
+                     : moe_prefill_dev(moe, x, m, x_dtype, logits, ids, wts, out, out_dtype, stream, props.sms);
+  }
   // Token chunks keep every launch under the problem-table bound.
   const int nt = m <= 8 ? 1 : 2;
   const int m_pad = 8 * nt;

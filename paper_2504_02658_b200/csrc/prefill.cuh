@@ -113,6 +113,9 @@ struct PfArgs {
   int32_t n_problems;
   const int32_t* item_start;  // exclusive prefix of work items per problem (n_problems + 1)
   int32_t n_items;
+  // device-planned launches (moe_plan_kernel): n_problems / n_items / ntok_max are
+  // read from dev_counts[0..2] at kernel start (null: the host values above)
+  const int32_t* dev_counts;
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -206,7 +209,13 @@ __device__ __forceinline__ void ring_wait(uint64_t* bar, uint32_t parity) {
     mbar_wait(bar, parity);
 }
 template <int NMAT, int NG>
-__global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel(const __grid_constant__ PfArgs a) {
+__global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel(const __grid_constant__ PfArgs a_in) {
+  PfArgs a = a_in;
+  if (a.dev_counts != nullptr) {  // planned on the device: sizes from the plan
+    a.n_problems = a.dev_counts[0];
+    a.n_items = a.dev_counts[1];
+    a.ntok_max = a.dev_counts[2];
+  }
 
   constexpr int kPfDeqGroups = PfRoles<NMAT, NG>::kGroups;
   static_assert(kPfDeqGroups <= PfCfg<NMAT, NG>::kAS, "dequant groups must not outnumber A slots");
@@ -680,16 +689,16 @@ __device__ __forceinline__ void t_load_block(const TProb& P, int kb, int lc, int
   }
 }
 
-__global__ void __launch_bounds__(256) pf_t_kernel(const TProb* __restrict__ probs, int n_probs) {
-  __shared__ __align__(16) float sx[kTRows][68];  // rows 16 B aligned: float4 reads of 4 k
-  __shared__ float su[64][65];
+// One unit (problem, token tile, rank chunk, k split) of pf_t_kernel.
+__device__ __forceinline__ void pf_t_unit(const TProb* __restrict__ probs, int n_probs, int unit,
+                                          float (&sx)[kTRows][68], float (&su)[64][65]) {
   int lo = 0, hi = n_probs - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
-    if (probs[mid].unit0 <= (int)blockIdx.x) lo = mid; else hi = mid - 1;
+    if (probs[mid].unit0 <= unit) lo = mid; else hi = mid - 1;
   }
   const TProb& P = probs[lo];
-  int u = blockIdx.x - P.unit0;
+  int u = unit - P.unit0;
   const int tiles = (P.rows + kTRows - 1) / kTRows;
   const int ksi = u % P.ks;
   u /= P.ks;
@@ -748,7 +757,24 @@ __global__ void __launch_bounds__(256) pf_t_kernel(const TProb* __restrict__ pro
     const int row = tile * kTRows + rg * 8 + i;
     if (row < P.rows) P.part[((int64_t)ksi * P.rows + row) * r64 + rcol] = acc[i];
   }
-  (void)rcol;
+}
+
+// dev_counts (nullable): {n_probs, units} from moe_plan_kernel; the CTAs then
+// loop over the planned units (grid-stride), else CTA = unit.
+__global__ void __launch_bounds__(256) pf_t_kernel(const TProb* __restrict__ probs, int n_probs,
+                                                  const int32_t* __restrict__ dev_counts) {
+  __shared__ __align__(16) float sx[kTRows][68];  // rows 16 B aligned: float4 reads of 4 k
+  __shared__ float su[64][65];
+  if (dev_counts == nullptr) {
+    pf_t_unit(probs, n_probs, blockIdx.x, sx, su);
+    return;
+  }
+  n_probs = dev_counts[0];
+  const int units = dev_counts[1];
+  for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    pf_t_unit(probs, n_probs, u, sx, su);
+    __syncthreads();
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -779,18 +805,18 @@ struct ImgJob {
 };
 constexpr int kImgTSmem = (kPfN * 65 + 64 * 65) * 4;
 
-__global__ void __launch_bounds__(256) pf_img_t_kernel(const ImgJob* __restrict__ jobs, int n_jobs) {
+__device__ __forceinline__ void pf_img_t_unit(const ImgJob* __restrict__ jobs, int n_jobs, int blk) {
   extern __shared__ float imgt_sm[];
   float* sx = imgt_sm;             // [ntok][65]
   float* su = imgt_sm + kPfN * 65; // [64][65]
   int lo = 0, hi = n_jobs - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
-    if (jobs[mid].blk0 <= (int)blockIdx.x) lo = mid; else hi = mid - 1;
+    if (jobs[mid].blk0 <= blk) lo = mid; else hi = mid - 1;
   }
   const ImgJob& J = jobs[lo];
   const int ks = J.k / kPfK;
-  const int rel = blockIdx.x - J.blk0;
+  const int rel = blk - J.blk0;
   const int tile = rel / ks, st = rel % ks;
   const int ntok = J.ntok, tid = threadIdx.x;
   uint8_t* dst = J.img + (int64_t)rel * ntok * 128;
@@ -863,9 +889,28 @@ __global__ void __launch_bounds__(256) pf_img_t_kernel(const ImgJob* __restrict_
   }
 }
 
+// dev_counts (nullable): {n_jobs, blocks} written by moe_plan_kernel; the CTAs
+// then loop over the planned blocks (grid-stride), else CTA = block.
+__global__ void __launch_bounds__(256) pf_img_t_kernel(const ImgJob* __restrict__ jobs, int n_jobs,
+                                                      const int32_t* __restrict__ dev_counts) {
+  if (dev_counts == nullptr) {
+    pf_img_t_unit(jobs, n_jobs, blockIdx.x);
+    return;
+  }
+  n_jobs = dev_counts[0];
+  const int blocks = dev_counts[1];
+  for (int b = blockIdx.x; b < blocks; b += gridDim.x) {
+    pf_img_t_unit(jobs, n_jobs, b);
+    __syncthreads();
+  }
+}
+
 // Sums the k-split partials in split order and writes the hi / lo images.
-__global__ void pf_t_images_kernel(const TProb* __restrict__ probs, int n_probs) {
-  const TProb& P = probs[blockIdx.y];
+__global__ void pf_t_images_kernel(const TProb* __restrict__ probs, int n_probs,
+                                   const int32_t* __restrict__ dev_counts) {
+  if (dev_counts != nullptr) n_probs = dev_counts[0];
+  for (int pi = blockIdx.y; pi < n_probs; pi += gridDim.y) {
+  const TProb& P = probs[pi];
   const int r64 = P.rchunks * 64;
   const int ntok = P.ntok;
   const int tiles = (P.rows + ntok - 1) / ntok;
@@ -883,6 +928,301 @@ __global__ void pf_t_images_kernel(const TProb* __restrict__ probs, int n_probs)
     const uint32_t off = (uint32_t)r * 128u + (uint32_t)(((jj >> 3) ^ (r & 7)) << 4) + (uint32_t)((jj & 7) * 2);
     *reinterpret_cast<__half*>(base + off) = h;
     *reinterpret_cast<__half*>(base + ib + off) = l;
+  }
+  }  // probs
+}
+
+}  // namespace milo_dev
+
+namespace milo_dev {
+
+// ---------------------------------------------------------------------------
+// MoE prefill planned on the device (no host round trip: the whole layer call
+// is stream-ordered and graph-capturable).  One CTA turns the routing ids into
+// every table the prefill kernels read -- the reference composition order
+// (SURVEY.md section 8b): per expert, its (token, k) entries in ascending token
+// order, then the shared experts with every token -- and into the device-side
+// counts the launches use (their grids are host bounds; CTAs past the planned
+// work exit).  Workspace regions are sized on the host for the worst routing.
+// ---------------------------------------------------------------------------
+struct PfMatStatic {
+  const uint8_t* w;        // macro tiles
+  const uint8_t* vimg;     // V^T images (null: no LoRC)
+  const uint8_t* ucodes;
+  const float* uscales;
+  const float* ureal;
+  int32_t k, n, mode, rank, gpr, rch;
+};
+struct PfExpertStatic {
+  PfMatStatic m[3];  // w1, w3, w2
+};
+
+// counts[] layout (int32): per phase ph (0, 1) at 16 * ph:
+//   [0] n_jobs  [1] img blocks  [2] n_tprobs  [3] t units  [4] n_problems  [5] n_items  [6] ntok_max
+struct PfPlanArgs {
+  const int32_t* ids;             // m x K routing (-1 = unused)
+  int64_t m;
+  int32_t K, E, S, sms;
+  const PfExpertStatic* ex;       // E routed then S shared
+  const void* x;
+  int32_t x_dtype;
+  int64_t d, f_max;
+  // outputs
+  int32_t* tok;                   // R grouped rows: x row
+  int32_t* slot;                  // R grouped rows: Y slot
+  ImgJob* jobs[2];                // <= G each
+  TProb* tps[2];                  // <= 2G / G
+  PfProblem* probs[2];            // <= G each
+  int32_t* starts[2];             // G + 1 each
+  int32_t* counts;                // 32 ints
+  // regions (sized by the host for the worst case)
+  uint8_t* img[2];                // activation images per phase
+  uint8_t* timg[3];               // t images per matrix
+  uint8_t* part[3];               // t partials per matrix
+  __half* h;                      // R x f_max
+  float* Y;                       // (m K + S m) x d
+};
+
+__device__ __forceinline__ int pf_ntok_dev(int64_t rows) { return (int)min((int64_t)kPfN, (rows + 15) / 16 * 16); }
+__device__ __forceinline__ int pf_t_splits_dev(int64_t rows, int64_t k, int rch, int sms) {
+  const int row_tiles = (int)((rows + kTRows - 1) / kTRows);
+  return max(1, min((int)(k / 256), (kTCtasPerSm * sms) / max(1, row_tiles * rch)));
+}
+
+constexpr int kPlanMaxGroups = 256;  // >= E + S (kRouteMaxE)
+
+__global__ void __launch_bounds__(1024) moe_plan_kernel(PfPlanArgs a) {
+  __shared__ int32_t s_cnt[kPlanMaxGroups];   // rows per expert (routed, shared)
+  __shared__ int32_t s_off[kPlanMaxGroups];   // grouped row offset
+  __shared__ int32_t s_gexp[kPlanMaxGroups];  // group -> expert
+  __shared__ int64_t s_o[8][kPlanMaxGroups];  // per group: img1, img2, timg0..2, part0..2 byte offsets
+  __shared__ int32_t s_blk[2][kPlanMaxGroups], s_unit[3][kPlanMaxGroups], s_item[2][kPlanMaxGroups + 1];
+  __shared__ int32_t s_ng;
+  __shared__ int32_t s_shape[kPlanMaxGroups][3][4];  // per expert, matrix: k, n, rank, rch
+  __shared__ int32_t s_tp[2][kPlanMaxGroups];        // per group: first t-problem slot per phase
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nwarps = blockDim.x >> 5;
+  const int E = a.E, S = a.S, K = a.K;
+  const int64_t m = a.m, mK = m * K;
+  for (int i = tid; i < (E + S) * 3; i += blockDim.x) {  // one parallel pass over the static table
+    const PfMatStatic& M = a.ex[i / 3].m[i % 3];
+    s_shape[i / 3][i % 3][0] = M.k;
+    s_shape[i / 3][i % 3][1] = M.n;
+    s_shape[i / 3][i % 3][2] = M.rank;
+    s_shape[i / 3][i % 3][3] = M.rch;
+  }
+  // 1. rows per expert: one warp per expert scans the entries with ballots
+  for (int e = warp; e < E + S; e += nwarps) {
+    int64_t c = 0;
+    if (e < E) {
+      for (int64_t base = 0; base < mK; base += 32) {
+        const int64_t i = base + lane;
+        const bool hit = i < mK && a.ids[i] == e;
+        c += __popc(__ballot_sync(0xffffffffu, hit));
+      }
+    } else {
+      c = m;
+    }
+    if (lane == 0) s_cnt[e] = (int32_t)c;
+  }
+  __syncthreads();
+  // 2. groups (non-empty experts, expert order) and every per-group offset (serial: <= 512 groups)
+  if (tid == 0) {
+    int ng = 0;
+    int64_t off = 0, oimg[2] = {0, 0}, ot[3] = {0, 0, 0}, op[3] = {0, 0, 0};
+    int32_t blk[2] = {0, 0}, unit[3] = {0, 0, 0}, item[2] = {0, 0}, ntmax = 16;
+    int32_t ntp[2] = {0, 0};
+    for (int e = 0; e < E + S; ++e) {
+      const int64_t rows = s_cnt[e];
+      if (rows == 0) continue;
+      const int g = ng++;
+      s_gexp[g] = e;
+      s_off[g] = (int32_t)off;
+      const int nt = pf_ntok_dev(rows);
+      ntmax = max(ntmax, nt);
+      const int64_t tiles = (rows + nt - 1) / nt;
+      // images: phase 1 over d, phase 2 over this expert's f (regions sized with f_max)
+      s_o[0][g] = oimg[0];
+      oimg[0] += (tiles * (a.d / kPfK) * nt * 128 + 255) & ~int64_t(255);
+      s_o[1][g] = oimg[1];
+      oimg[1] += (tiles * (a.f_max / kPfK) * nt * 128 + 255) & ~int64_t(255);
+      s_blk[0][g] = blk[0];
+      blk[0] += (int32_t)(tiles * (a.d / kPfK));
+      s_blk[1][g] = blk[1];
+      blk[1] += (int32_t)(tiles * (s_shape[e][2][0] / kPfK));
+      s_tp[0][g] = ntp[0];
+      s_tp[1][g] = ntp[1];
+      for (int j = 0; j < 3; ++j) {
+        const int mk = s_shape[e][j][0], rank = s_shape[e][j][2], rch = s_shape[e][j][3];
+        s_o[2 + j][g] = ot[j];
+        s_o[5 + j][g] = op[j];
+        s_unit[j][g] = 0;
+        if (rank <= 0) continue;
+        ot[j] += (tiles * rch * 2 * nt * 128 + 255) & ~int64_t(255);
+        const int ks = pf_t_splits_dev(rows, mk, rch, a.sms);
+        op[j] += ((int64_t)max(mk / kPfK, ks) * rows * rch * 64 * 4 + 255) & ~int64_t(255);
+        const int ph = j == 2 ? 1 : 0;
+        s_unit[j][g] = unit[ph];  // unit0 of this t problem (phase-wide prefix)
+        unit[ph] += (int32_t)((rows + kTRows - 1) / kTRows) * rch * ks;
+        ++ntp[ph];
+      }
+      s_item[0][g] = item[0];
+      item[0] += (int32_t)((s_shape[e][0][1] / kPfM) * tiles);
+      s_item[1][g] = item[1];
+      item[1] += (int32_t)((s_shape[e][2][1] / kPfM) * tiles);
+      off += rows;
+    }
+    s_ng = ng;
+    s_item[0][ng] = item[0];
+    s_item[1][ng] = item[1];
+    for (int ph = 0; ph < 2; ++ph) {
+      int32_t* c = a.counts + 16 * ph;
+      c[0] = ng;
+      c[1] = blk[ph];
+      c[2] = ntp[ph];
+      c[3] = unit[ph];
+      c[4] = ng;
+      c[5] = item[ph];
+      c[6] = ntmax;
+    }
+  }
+  __syncthreads();
+  const int ng = s_ng;
+  // 3. grouped rows: token (x row) and Y slot, entries of an expert in (t, k) order
+  for (int g = warp; g < ng; g += nwarps) {
+    const int e = s_gexp[g];
+    int32_t* tok = a.tok + s_off[g];
+    int32_t* slot = a.slot + s_off[g];
+    if (e < E) {
+      int64_t pos = 0;
+      for (int64_t base = 0; base < mK; base += 32) {
+        const int64_t i = base + lane;
+        const bool hit = i < mK && a.ids[i] == e;
+        const unsigned b = __ballot_sync(0xffffffffu, hit);
+        if (hit) {
+          const int64_t p = pos + __popc(b & ((1u << lane) - 1u));
+          tok[p] = (int32_t)(i / K);
+          slot[p] = (int32_t)i;
+        }
+        pos += __popc(b);
+      }
+    } else {
+      for (int64_t t = lane; t < m; t += 32) {
+        tok[t] = (int32_t)t;
+        slot[t] = (int32_t)(mK + (int64_t)(e - E) * m + t);
+      }
+    }
+  }
+  // 4. per-group tables (thread per group)
+  for (int g = tid; g < ng; g += blockDim.x) {
+    const int e = s_gexp[g];
+    const PfExpertStatic& X = a.ex[e];
+    const int64_t rows = s_cnt[e], off = s_off[g];
+    const int nt = pf_ntok_dev(rows);
+    // activation image jobs (no fused t: pf_t_kernel computes t)
+    ImgJob J1{};
+    J1.x = a.x;
+    J1.x_dtype = a.x_dtype;
+    J1.ldx = a.d;
+    J1.row_ids = a.tok + off;
+    J1.rows = (int32_t)rows;
+    J1.k = (int32_t)a.d;
+    J1.ntok = nt;
+    J1.img = a.img[0] + s_o[0][g];
+    J1.blk0 = s_blk[0][g];
+    a.jobs[0][g] = J1;
+    ImgJob J2{};
+    J2.x = a.h + off * a.f_max;
+    J2.x_dtype = 1;
+    J2.ldx = a.f_max;
+    J2.row_ids = nullptr;
+    J2.rows = (int32_t)rows;
+    J2.k = X.m[2].k;
+    J2.ntok = nt;
+    J2.img = a.img[1] + s_o[1][g];
+    J2.blk0 = s_blk[1][g];
+    a.jobs[1][g] = J2;
+    // t problems: phase 1 in (group, w1, w3) order, phase 2 per group; the slot
+    // of a group's problem is its rank among the groups before it with a comp
+    int n0 = s_tp[0][g], n1 = s_tp[1][g];
+    for (int j = 0; j < 3; ++j) {
+      const PfMatStatic& M = X.m[j];
+      if (M.rank <= 0) continue;
+      TProb tp{};
+      if (j < 2) {
+        tp.x = a.x;
+        tp.x_dtype = a.x_dtype;
+        tp.ldx = a.d;
+        tp.row_ids = a.tok + off;
+      } else {
+        tp.x = a.h + off * a.f_max;
+        tp.x_dtype = 1;
+        tp.ldx = a.f_max;
+        tp.row_ids = nullptr;
+      }
+      tp.rows = (int32_t)rows;
+      tp.k = M.k;
+      tp.rank = M.rank;
+      tp.gpr = M.gpr;
+      tp.rchunks = M.rch;
+      tp.ks = pf_t_splits_dev(rows, M.k, M.rch, a.sms);
+      tp.ucodes = M.ucodes;
+      tp.uscales = M.uscales;
+      tp.ureal = M.ureal;
+      tp.timg = a.timg[j] + s_o[2 + j][g];
+      tp.part = reinterpret_cast<float*>(a.part[j] + s_o[5 + j][g]);
+      tp.ntok = nt;
+      tp.unit0 = s_unit[j][g];
+      if (j < 2)
+        a.tps[0][n0++] = tp;
+      else
+        a.tps[1][n1++] = tp;
+    }
+    // GEMM problems
+    PfProblem P1{};
+    P1.w[0] = X.m[0].w;
+    P1.w[1] = X.m[1].w;
+    P1.act = J1.img;
+    for (int j = 0; j < 2; ++j)
+      if (X.m[j].rank > 0) {
+        P1.vimg[j] = X.m[j].vimg;
+        P1.timg[j] = a.timg[j] + s_o[2 + j][g];
+        P1.rchunks[j] = X.m[j].rch;
+      }
+    P1.k = (int32_t)a.d;
+    P1.n = X.m[0].n;
+    P1.rows = (int32_t)rows;
+    P1.ntok = nt;
+    P1.mode = X.m[0].mode;
+    P1.kind = 1;
+    P1.out_dtype = 1;
+    P1.ldo = a.f_max;
+    P1.out = a.h + off * a.f_max;
+    a.probs[0][g] = P1;
+    PfProblem P2{};
+    P2.w[0] = X.m[2].w;
+    P2.act = J2.img;
+    if (X.m[2].rank > 0) {
+      P2.vimg[0] = X.m[2].vimg;
+      P2.timg[0] = a.timg[2] + s_o[4][g];
+      P2.rchunks[0] = X.m[2].rch;
+    }
+    P2.k = X.m[2].k;
+    P2.n = (int32_t)a.d;
+    P2.rows = (int32_t)rows;
+    P2.ntok = nt;
+    P2.mode = X.m[2].mode;
+    P2.kind = 0;
+    P2.out_dtype = 0;
+    P2.ldo = a.d;
+    P2.out = a.Y;
+    P2.row_map = a.slot + off;
+    a.probs[1][g] = P2;
+    a.starts[0][g] = s_item[0][g];
+    a.starts[1][g] = s_item[1][g];
+  }
+  if (tid == 0) {
+    a.starts[0][ng] = s_item[0][ng];
+    a.starts[1][ng] = s_item[1][ng];
   }
 }
 
