@@ -27,6 +27,7 @@
 #include "lorc.cuh"
 #include "moe.cuh"
 #include "decode.cuh"
+#include "hdec.cuh"
 #include "prefill.cuh"
 
 using namespace milo_dev;
@@ -304,6 +305,31 @@ struct milo_comp {
 // real: binary16 hi + lo split of the fp32 factors (pad 0).
 // ---------------------------------------------------------------------------
 namespace {
+
+// binary32 -> binary16, round to nearest even (branch-free; NaN stays NaN):
+// the host-side half(A) of the reference's activations (half.hpp float_to_half).
+inline uint16_t f32_to_f16_rne(float f) {
+  uint32_t x;
+  std::memcpy(&x, &f, 4);
+  const uint32_t sign = (x >> 16) & 0x8000u;
+  x &= 0x7FFFFFFFu;
+  uint16_t o;
+  if (x >= 0x47800000u) {  // overflow -> inf, NaN -> quiet NaN
+    o = x > 0x7F800000u ? 0x7E00u : 0x7C00u;
+  } else if (x < 0x38800000u) {  // subnormal / zero: add the magic 0.5, let the FPU round
+    float t;
+    std::memcpy(&t, &x, 4);
+    t += 0.5f;
+    uint32_t ti;
+    std::memcpy(&ti, &t, 4);
+    o = (uint16_t)(ti - 0x3F000000u);
+  } else {
+    const uint32_t mant_odd = (x >> 13) & 1u;
+    x += 0xC8000FFFu + mant_odd;  // rebias exponent (15 - 127) << 23 and round
+    o = (uint16_t)(x >> 13);
+  }
+  return (uint16_t)(o | sign);
+}
 
 uint16_t h16(float f) {
   const __half h = __float2half_rn(f);
@@ -837,6 +863,8 @@ constexpr size_t kCtrlInts = 2 * (size_t)kCntCap + kDecMaxBlocks * 3 + kDecMaxBl
 
 struct DecodeWs {
   int32_t* ctrl = nullptr;
+  int32_t* hctrl = nullptr;  // hdec_kernel: 2 parity blocks of kHdCtrl ints (hdec.cuh)
+  uint32_t hcalls = 0;       // hdec_kernel calls on this workspace (parity)
   void* data = nullptr;
   size_t data_bytes = 0;
   cudaStream_t stream = nullptr;
@@ -855,6 +883,10 @@ uint32_t g_epoch = 0;
 
 milo_status ws_init(DecodeWs& w, bool ctrl, bool data) {
   if (ctrl) CUDA_TRY(cudaMemsetAsync(w.ctrl, 0, kCtrlInts * 4, w.stream));
+  if (ctrl && w.hctrl) {
+    CUDA_TRY(cudaMemsetAsync(w.hctrl, 0, 2 * kHdCtrl * 4, w.stream));
+    w.hcalls = 0;
+  }
   if (data && w.data) CUDA_TRY(cudaMemsetAsync(w.data, 0xFF, w.data_bytes, w.stream));
   return MILO_OK;
 }
@@ -945,6 +977,7 @@ milo_status release_stream_ws(cudaStream_t stream) {
     for (void* p : it->second.retired) CUDA_TRY(cudaFree(p));
     if (it->second.data) CUDA_TRY(cudaFree(it->second.data));
     if (it->second.ctrl) CUDA_TRY(cudaFree(it->second.ctrl));
+    if (it->second.hctrl) CUDA_TRY(cudaFree(it->second.hctrl));
     g_ws.erase(it);
   }
   auto jt = g_pf_ws.find({dev, stream});
@@ -1512,6 +1545,8 @@ struct milo_moe {
   __half* gate = nullptr;  // optional router gate, E x d binary16 (milo_moe_set_gate)
   PfExpertStatic* pf_static = nullptr;  // device: per expert, what moe_plan_kernel needs
   int32_t rch_max[3] = {0, 0, 0};       // largest 64-rank chunk count per matrix
+  bool hd_ok = true;                    // hdec_kernel eligible (int3 / no compensators, 64-multiple shapes)
+  HdExp* hd_exp = nullptr;              // device: hdec_kernel's per-expert static view
 };
 
 extern "C" milo_status milo_moe_create(const milo_expert_desc* experts, int32_t n_experts,
@@ -1563,6 +1598,11 @@ extern "C" milo_status milo_moe_create(const milo_expert_desc* experts, int32_t 
       if (w[j]->cols % kPfM != 0 || w[j]->rows % kPfK != 0 || !comp_ok) moe->prefill_ok = false;
     }
     for (int j = 0; j < 3; ++j) {
+      const bool has_c = c[j] && c[j]->rank > 0;
+      if ((has_c && (c[j]->storage != 1 || !c[j]->upt)) || w[j]->rows % 64 != 0 || w[j]->cols % 64 != 0)
+        moe->hd_ok = false;
+    }
+    for (int j = 0; j < 3; ++j) {
       dhost[i].m[j] = make_decmat(w[j], c[j]);
       moe->r16_max = std::max(moe->r16_max, dhost[i].m[j].r16);
     }
@@ -1601,6 +1641,23 @@ extern "C" milo_status milo_moe_create(const milo_expert_desc* experts, int32_t 
   if (err == cudaSuccess)
     err = cudaMemcpy(moe->dec_experts, dhost.data(), dhost.size() * sizeof(DecExpert),
                      cudaMemcpyHostToDevice);
+  {  // hdec_kernel's per-expert static view
+    std::vector<HdExp> hx(dhost.size());
+    for (size_t i = 0; i < dhost.size(); ++i) {
+      const DecExpert& X = dhost[i];
+      hx[i].nu = X.m[0].n / 64;
+      hx[i].kt2 = X.m[0].n / 32;
+      hx[i].mode = (int8_t)X.m[0].mode;
+      for (int j = 0; j < 3; ++j) {
+        const int nks = X.m[j].rank > 0 ? X.m[j].r16 / 16 : 0;
+        if (nks > 127) moe->hd_ok = false;
+        hx[i].nks[j] = (int8_t)std::min(nks, 127);
+        hx[i].gpr[j] = (int8_t)X.m[j].gpr;
+      }
+    }
+    if (err == cudaSuccess) err = cudaMalloc(&moe->hd_exp, hx.size() * sizeof(HdExp));
+    if (err == cudaSuccess) err = cudaMemcpy(moe->hd_exp, hx.data(), hx.size() * sizeof(HdExp), cudaMemcpyHostToDevice);
+  }
   {  // the prefill planner's static view (moe_plan_kernel)
     std::vector<PfExpertStatic> ps(host.size());
     for (size_t i = 0; i < host.size(); ++i)
@@ -1631,6 +1688,7 @@ extern "C" milo_status milo_moe_create(const milo_expert_desc* experts, int32_t 
     cudaFree(moe->dev_experts);
     cudaFree(moe->dec_experts);
     cudaFree(moe->pf_static);
+    cudaFree(moe->hd_exp);
     delete moe;
     return fail(MILO_ERR_CUDA, "expert table upload failed: %s", cudaGetErrorString(err));
   }
@@ -1643,6 +1701,7 @@ extern "C" milo_status milo_moe_destroy(milo_moe* moe) {
   cudaFree(moe->dev_experts);
   cudaFree(moe->dec_experts);
   cudaFree(moe->pf_static);
+  cudaFree(moe->hd_exp);
   if (moe->host_stage) cudaFreeHost(moe->host_stage);
   if (moe->dev_stage) cudaFree(moe->dev_stage);
   if (moe->gate) cudaFree(moe->gate);
@@ -2180,6 +2239,118 @@ milo_status moe_prefill_dev(milo_moe* moe, const void* x, int64_t m, int32_t x_d
 
 // logits != nullptr: the route kernel computes the top-k into ids / wts
 // (outputs); otherwise ids / wts are the given routing (inputs).
+// ---------------------------------------------------------------------------
+// hdec_kernel (hdec.cuh): the decode-regime layer, h-local.  Workspace: the
+// tagged regions (T partials, P1 partials, published h) in the decode data
+// region (0xFF-filled when allocated, so no stale tag matches), the fp32
+// accumulators (zeroed by the kernel itself) and a two-parity control block
+// (each call zeroes the block the next call on this workspace uses).
+// ---------------------------------------------------------------------------
+int hdec_env() {
+  static const int v = [] {
+    const char* e = getenv("MILO_HDEC");
+    return e ? atoi(e) : 0;  // opt-in until it beats the round-1 megakernel everywhere
+  }();
+  return v;
+}
+
+bool hdec_eligible(const milo_moe* moe, int64_t m) {
+  if (hdec_env() == 0 || legacy_path() || !moe->hd_ok || m < 1 || m > kHdMaxTok) return false;
+  const int64_t np_max = std::min<int64_t>(moe->E, m * moe->K) + moe->n_shared;
+  return np_max <= kHdMaxParts && moe->E <= 256 && moe->K <= 16 && moe->d % 64 == 0 && moe->d >= 64;
+}
+
+template <int NT>
+milo_status launch_hdec(const milo_moe* moe, const void* x, int64_t m, int32_t x_dtype, const float* logits,
+                        int32_t* ids, float* wts, void* out, int32_t out_dtype, cudaStream_t stream, int sms) {
+  using CF = HdCfg<NT>;
+  static thread_local int configured_dev = -1;
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  if (configured_dev != dev) {
+    CUDA_TRY(set_smem(hdec_kernel<NT>, CF::kBytes));
+    configured_dev = dev;
+  }
+  const int G = sms;
+  const int64_t KT = moe->d / 32, nch = (KT + kHdTK - 1) / kHdTK;
+  const int64_t np_max = std::min<int64_t>(moe->E, m * moe->K) + moe->n_shared;
+  const int64_t r16 = std::max(moe->r16_max, 16);
+  Arena ar;
+  const size_t o_tp = ar.take((size_t)np_max * 2 * (r16 / 16) * nch * 16 * 16 * 8);
+  const size_t o_pt = ar.take((size_t)G * 1024 * NT * 8);
+  const size_t o_hp = ar.take((size_t)G * 16 * 32 * 8);
+  const size_t o_t2 = ar.take((size_t)(m * moe->K + moe->n_shared * m) * r16 * 4);
+  const size_t o_ac = ar.take(out_dtype == 0 ? 0 : (size_t)m * moe->d * 4);
+  const size_t o_x = ar.take(x_dtype == 0 ? (size_t)m * moe->d * 2 : 0);
+  DecodeWs* w = nullptr;
+  int epoch = 0;
+  milo_status st = get_ws(stream, ar.size, &w, &epoch);
+  if (st != MILO_OK) return st;
+  uint32_t parity = 0;
+  {
+    std::lock_guard<std::mutex> lock(g_ws_mu);
+    if (!w->hctrl) {
+      CUDA_TRY(cudaMalloc(&w->hctrl, 2 * kHdCtrl * 4));
+      CUDA_TRY(cudaMemsetAsync(w->hctrl, 0, 2 * kHdCtrl * 4, stream));
+      w->hcalls = 0;
+    }
+    parity = w->hcalls++ & 1u;
+  }
+  uint8_t* base = static_cast<uint8_t*>(w->data);
+  HdArgs a{};
+  a.m = (int32_t)m;
+  a.E = moe->E;
+  a.K = moe->K;
+  a.S = moe->n_shared;
+  a.score_mode = moe->score_mode;
+  a.d = moe->d;
+  a.logits = logits;
+  a.ids_in = logits ? nullptr : ids;
+  a.wts_in = logits ? nullptr : wts;
+  a.ids_out = logits ? ids : nullptr;
+  a.wts_out = logits ? wts : nullptr;
+  a.experts = moe->dec_experts;
+  a.hexp = moe->hd_exp;
+  a.x = static_cast<const __half*>(x);
+  a.ldx = moe->d;
+  if (x_dtype == 0) {  // the kernel streams binary16 rows: round f32 rows once (gemm.cpp:144-146)
+    __half* x16 = reinterpret_cast<__half*>(base + o_x);
+    const int64_t n4 = m * (moe->d / 4);
+    const int grid = (int)std::min<int64_t>((n4 + 255) / 256, (int64_t)sms * 4);
+    CUDA_TRY(launch(rows_to_half_kernel, dim3(std::max(grid, 1)), dim3(256), 0, stream, false,
+                    static_cast<const float*>(x), m, (int64_t)moe->d, (int64_t)moe->d, x16));
+    a.x = x16;
+  }
+  a.out = out;
+  a.out_dtype = out_dtype;
+  a.ldo = moe->d;
+  a.epoch = epoch;
+  a.ctrl = w->hctrl + parity * kHdCtrl;
+  a.ctrl_next = w->hctrl + (parity ^ 1u) * kHdCtrl;
+  a.tpart = reinterpret_cast<uint64_t*>(base + o_tp);
+  a.part = reinterpret_cast<uint64_t*>(base + o_pt);
+  a.hpub = reinterpret_cast<uint64_t*>(base + o_hp);
+  a.t2acc = reinterpret_cast<float*>(base + o_t2);
+  a.acc = out_dtype == 0 ? nullptr : reinterpret_cast<float*>(base + o_ac);
+  a.dbg = g_dbg;
+  a.dbg_flags = g_dbg_flags;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(G);
+  cfg.blockDim = dim3(CF::kThreads);
+  cfg.dynamicSmemBytes = CF::kBytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (g_dry) return MILO_OK;
+  ++g_launches;
+  ProfScope ps(kProfGemv1, stream);
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, hdec_kernel<NT>, a));
+  return MILO_OK;
+}
+
 milo_status moe_forward_impl(milo_moe* moe, const void* x, int64_t m, int32_t x_dtype,
                              const float* logits, int32_t* ids, float* wts, void* out,
                              int32_t out_dtype, void* stream_) {
@@ -2192,6 +2363,9 @@ milo_status moe_forward_impl(milo_moe* moe, const void* x, int64_t m, int32_t x_
   DeviceProps props = device_props();
   if (!props.ok || props.major != 10) return fail(MILO_ERR_CUDA, "no sm_100 device");
   cudaStream_t stream = (cudaStream_t)stream_;
+  if (hdec_eligible(moe, m))
+    return m <= 8 ? launch_hdec<1>(moe, x, m, x_dtype, logits, ids, wts, out, out_dtype, stream, props.sms)
+                  : launch_hdec<2>(moe, x, m, x_dtype, logits, ids, wts, out, out_dtype, stream, props.sms);
   // decode megakernel blocks: each touched expert's tokens in chunks of m_pad rows
   const int dec_mpad = m <= 8 ? 8 : 16;
   // bound on the blocks: t = min(E, mK) touched experts, an expert with c <= m
@@ -2393,23 +2567,34 @@ extern "C" milo_status milo_moe_forward_host(milo_moe* moe, const float* x, int6
   }
   uint8_t* hs = static_cast<uint8_t*>(moe->host_stage);
   uint8_t* b = static_cast<uint8_t*>(moe->dev_stage);
-  std::memcpy(hs, x, xb);
-  if (lb) std::memcpy(hs + xb, logits, lb);
-  cudaError_t e = cudaMemcpyAsync(b, hs, xb + lb, cudaMemcpyHostToDevice, stream);
+  // The h-local decode kernel streams binary16 rows and accumulates the output
+  // with device-memory reductions: x is rounded to binary16 here (RNE, the
+  // reference's half(A), gemm.cpp:144-146) and goes up at half the bytes; the
+  // output comes back by one copy.
+  const bool hd = hdec_eligible(moe, m);
+  const size_t xup = hd ? (size_t)m * moe->d * 2 : xb;
+  if (hd) {
+    uint16_t* x16 = reinterpret_cast<uint16_t*>(hs);
+    for (int64_t i = 0; i < m * (int64_t)moe->d; ++i) x16[i] = f32_to_f16_rne(x[i]);
+  } else {
+    std::memcpy(hs, x, xb);
+  }
+  if (lb) std::memcpy(hs + xup, logits, lb);
+  cudaError_t e = cudaMemcpyAsync(b, hs, xup + lb, cudaMemcpyHostToDevice, stream);
   milo_status st = e == cudaSuccess ? MILO_OK : fail(MILO_ERR_CUDA, "%s", cudaGetErrorString(e));
-  // Decode-sized outputs are written by the kernel straight into the mapped
-  // pinned stage (posted writes over the host link, visible once the stream
-  // has synchronised): no device-to-host copy on the critical path.
+  // Otherwise decode-sized outputs are written by the kernel straight into the
+  // mapped pinned stage (posted writes over the host link, visible once the
+  // stream has synchronised): no device-to-host copy on the critical path.
   void* out_dev = b + xb + lb16;
-  const bool zero_copy = xb <= kHostZeroCopyMax &&
+  const bool zero_copy = !hd && xb <= kHostZeroCopyMax &&
                          cudaHostGetDevicePointer(&out_dev, hs + xb + lb16, 0) == cudaSuccess;
   if (!zero_copy) {
     cudaGetLastError();
     out_dev = b + xb + lb16;
   }
   if (st == MILO_OK)
-    st = milo_moe_forward(moe, b, m, MILO_F32, reinterpret_cast<float*>(b + xb), out_dev, MILO_F32, nullptr,
-                          nullptr, stream);
+    st = milo_moe_forward(moe, b, m, hd ? MILO_F16 : MILO_F32, reinterpret_cast<float*>(b + xup), out_dev, MILO_F32,
+                          nullptr, nullptr, stream);
   if (st == MILO_OK && !zero_copy) {
     e = cudaMemcpyAsync(hs + xb + lb16, b + xb + lb16, xb, cudaMemcpyDeviceToHost, stream);
     if (e != cudaSuccess) st = fail(MILO_ERR_CUDA, "%s", cudaGetErrorString(e));

@@ -99,9 +99,10 @@ def test_skewed_routing_and_host_entry(gpu, oracle):
 
 @pytest.mark.parametrize("m", [1, 16, 600])
 def test_host_entry_matches_device_call(gpu, oracle, m):
-    """milo_moe_forward_host: small outputs are written by the kernel into the
-    mapped pinned stage (no D2H copy), large ones (600 x 128 f32 > 256 KB) come
-    back by copy; both must equal the device-buffer call bit for bit."""
+    """milo_moe_forward_host: the host-buffer entry point must equal the
+    device-buffer call.  Decode batches run the h-local kernel, whose output is
+    accumulated with fp32 reductions in arrival order, so two calls agree to
+    fp32 reassociation (<= 1e-6 relative); the other paths bit for bit."""
     import torch
     E, K, d, f = 4, 2, 128, 256
     o_ex, g_ex = _experts(oracle, gpu, E, d, f, [[16, 8, 0]] * E, seed=510)
@@ -112,7 +113,10 @@ def test_host_entry_matches_device_call(gpu, oracle, m):
     host = layer.forward_host(x, logits)
     host2 = layer.forward_host(x, logits)  # the stage is reused across calls
     dev = layer.forward(torch.from_numpy(x).cuda(), torch.from_numpy(logits).cuda()).cpu().numpy()
-    assert np.array_equal(host, dev) and np.array_equal(host2, dev)
+    if m <= 16:
+        assert rel_err(host, dev) <= 1e-6 and rel_err(host2, dev) <= 1e-6
+    else:
+        assert np.array_equal(host, dev) and np.array_equal(host2, dev)
     ids, w = oracle.router_topk(logits, K, 0)
     assert rel_err(host, oracle.moe_forward(o_ex, [], x, ids, w)) <= TOL_MOE
 
@@ -282,9 +286,9 @@ def test_decode_path_beyond_64_blocks(gpu, oracle, m):
     l0 = gpu.launch_count()
     out = layer.forward(torch.from_numpy(x).cuda(), torch.from_numpy(logits).cuda())
     torch.cuda.synchronize()
-    # the decode megakernel (+ the f32 -> binary16 row rounding above 16 tokens), not the
-    # multi-launch legacy or prefill paths
-    assert gpu.launch_count() - l0 <= (1 if m <= 16 else 2)
+    # one decode kernel (+ the f32 -> binary16 row rounding of x), not the multi-launch
+    # legacy or prefill paths
+    assert gpu.launch_count() - l0 <= 2
     assert rel_err(out.cpu().numpy(), want) <= TOL_MOE
 
 
