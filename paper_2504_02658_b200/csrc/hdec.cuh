@@ -54,6 +54,7 @@ constexpr int kHdCtrl = 4 + kHdMaxParts;        // per-parity control ints
 constexpr int kHdTK = 16;                       // U pseudo tiles per T item
 constexpr int kHdV2K = 8;                       // V2 rank steps per V2 item
 constexpr int kHdScr = 68;                      // epilogue scratch row stride (floats)
+constexpr int kHdDbgG = 1024;                   // timeline layout: regions sized for this many CTAs
 
 // Per-expert static view (host-built, 16 B).
 struct HdExp {
@@ -72,6 +73,7 @@ struct HdArgs {
   float* wts_out;
   const DecExpert* experts;  // E routed then S shared
   const HdExp* hexp;
+  const uint8_t* w2maps;  // per expert: a 128-byte TMA map of W2's slab-major tiles (boxes of 8 slabs x 2 k-tiles)
   const __half* x;       // binary16 rows, ld = ldx
   int64_t ldx;
   void* out;
@@ -86,7 +88,7 @@ struct HdArgs {
   float* t2acc;          // fp32, zeroed by the kernel
   float* acc;            // f16 output: fp32 accumulator m x d (zeroed by the kernel)
   long long* dbg;       // optional timeline: [grid][128] consumer warp 0, then [grid][64] producer stamps
-  int32_t dbg_flags;    // experiments: bit 0 no output reductions, bit 1 no P2 epilogue, bit 2 no copies, bit 4 producers alone (no copies, no waits), bit 5 no P1 compute, bit 6 no L2 prefetch
+  int32_t dbg_flags;    // experiments: bit 0 no output reductions, bit 1 no P2 epilogue, bit 2 no copies, bit 4 producers alone (no copies, no waits), bit 5 no P1 compute, bit 6 no L2 prefetch, bit 7 no P2 compute
 };
 
 struct HPart {
@@ -123,24 +125,27 @@ enum : uint8_t {
 // slower than 8 at 168: 1.31 us per 24-tile stage vs 1.47 us per 32).
 template <int NT>
 struct HdCfg {
-  static constexpr int kCons = 8;                      // consumer warps
-  static constexpr int kThreads = 32 * (kCons + kHdProd);
-  // NT = 1: three 58 KB stages (32 P1 k-steps for one token) -- the per-stage consumer
-  // overhead (~0.4 us: data wait + instruction fetch around the compute) is paid half as
-  // often as with five 37 KB stages; NT = 2: four 37 KB stages.
-  static constexpr int kStage = NT == 1 ? 59520 : 37888;  // ring stage bytes
+  // NT = 1: 12 consumer warps (3 per SM sub-partition: at 2 the de-quantization stalls on
+  // its own latencies) in 152 registers after setmaxnreg (the producer warpgroup drops to
+  // 40), three 48.5 KB stages; NT = 2: 8 consumer warps, four 37 KB stages.
+  static constexpr int kCtasPerSm = 1;
+  static constexpr int kCons = NT == 1 ? 12 : 8;       // consumer warps
+  static constexpr bool kSetMaxNreg = NT == 1;         // producer warpgroup (4 warps: 2 producers, 2 idle)
+  static constexpr int kConsRegs = 152, kProdRegs = 40;
+  static constexpr int kThreads = 32 * (kCons + (kSetMaxNreg ? 4 : kHdProd));
+  static constexpr int kStage = NT == 1 ? 49664 : 37888;  // ring stage bytes
   static constexpr int kNS = NT == 1 ? 3 : 4;          // ring stages
-  static constexpr int kP2 = NT == 1 ? 32 : 16;        // P2 d-slabs per stage
+  static constexpr int kP2 = NT == 1 ? 24 : 16;        // P2 d-slabs per stage
   // P1 k-steps per stage for `rows` tokens (multiples of the consumer warps)
   static __device__ __forceinline__ int ksp(int rows) {
-    return NT == 1 ? (rows == 1 ? 32 : 24) : (rows <= 8 ? 16 : 8);
+    return NT == 1 ? (rows <= 4 ? 24 : 12) : (rows <= 8 ? 16 : 8);
   }
   static constexpr int kFV = (kStage - 2048) / 1024 < 32 ? (kStage - 2048) / 1024 : 32;  // V rank steps per FIN-V stage
   static constexpr int kFU = kStage / 1280;            // U2 rank groups per FIN-U stage
   static constexpr int kOffRing = 0;
   static constexpr int kOffRed = kNS * kStage;
-  static constexpr int kScrBytes = kCons * 8 * NT * kHdScr * 4;               // P2 / V2 epilogue scratch
-  static constexpr int kTreeBytes = (kCons / 2) * 32 * NT * 32 * 4;           // P1 reduction tree
+  static constexpr int kScrBytes = 0;                                          // (epilogues shuffle in registers)
+  static constexpr int kTreeBytes = 4 * 32 * NT * 32 * 4;                      // P1 reduction: 4 slots
   static constexpr int kFvBytes = 8 * NT * (16 * kFV + 8) * 4;                // FIN-V t image
   static constexpr int kRed0 = kScrBytes + 8 * NT * (16 * kHdV2K + 8) * 4;    // + V2's t2 image
   static constexpr int kRedBytes = kRed0 > kTreeBytes ? (kRed0 > kFvBytes ? kRed0 : kFvBytes)
@@ -186,10 +191,41 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 template <int NT>
 __device__ __forceinline__ void cons_bar() { named_bar_sync(1, 32 * HdCfg<NT>::kCons); }
 
-// Range owner: CTA i holds pairs [i T / G, (i + 1) T / G).
-__device__ __forceinline__ int hd_owner(long long x, long long T, int G) {
-  return (int)(((x + 1) * (long long)G - 1) / T);
-}
+// The grid's split of the unit pairs: CTA i holds [lo(i), lo(i + 1)).  CTAs that also
+// run a T item (round-robin from CTA 0) or a V2 item (round-robin from CTA G - 1) get
+// kHdTCost / kHdVCost fewer pairs, so the grid still finishes together:
+//   lo(i) = floor(i (Tot + X nT + Y nV) / G) - X T(i) - Y V(i),
+// T(i), V(i) = the T / V2 items owned by CTAs below i.
+constexpr int kHdTCost = 0, kHdVCost = 0;  // pairs (one pair ~ 1792 B of weights); 40 / 30 measured no better (noise-level)
+struct HRange {
+  long long Tot, Sum;
+  int G, nT, nV, X, Y;
+  __device__ __forceinline__ void init(long long tot, int g, int nt, int nv) {
+    Tot = tot;
+    G = g;
+    nT = nt;
+    nV = nv;
+    const long long R = (tot + g - 1) / g;
+    X = (int)(R / 4 < kHdTCost ? R / 4 : kHdTCost);
+    Y = (int)(R / 4 < kHdVCost ? R / 4 : kHdVCost);
+    Sum = tot + (long long)X * nt + (long long)Y * nv;
+  }
+  __device__ __forceinline__ long long lo(int i) const {
+    if (i >= G) return Tot;
+    const long long t = (long long)(nT / G) * i + min(i, nT % G);
+    const long long v = (long long)(nV / G) * i + max(0, nV % G - G + i);
+    const long long r = (long long)i * Sum / G - (long long)X * t - (long long)Y * v;
+    return r < 0 ? 0 : (r > Tot ? Tot : r);
+  }
+  __device__ __forceinline__ int owner(long long x) const {  // the CTA whose range holds pair x
+    int a = 0, b = G - 1;
+    while (a < b) {
+      const int mid = (a + b + 1) >> 1;
+      if (lo(mid) <= x) a = mid; else b = mid - 1;
+    }
+    return a;
+  }
+};
 
 // B fragments of 32 k from a binary16 [row][.] image in shared memory (row
 // stride rs halves, rows >= nrows read as zero) at column kb.
@@ -216,12 +252,14 @@ __device__ __forceinline__ void load_bs(BTile<NT>& b, const __half* base, int rs
 // the participant changes: a dependent global load per stage would cost an L2
 // round trip, ~1 us under the weight stream).
 struct HMats {
+  const uint8_t* w2map;
   const uint8_t* w[3];
   const uint8_t* upt[3];
   const uint8_t* vft[3];
   const float* vstep[3];
   int gpr[3];
-  __device__ __forceinline__ void load(const DecExpert& X) {
+  __device__ __forceinline__ void load(const DecExpert& X, const uint8_t* map) {
+    w2map = map;
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
       w[i] = X.m[i].w;
@@ -235,16 +273,18 @@ struct HMats {
 
 // Copies of a copy event: count, and copy i (src, bytes, destination offset).
 struct HCopy {
-  const uint8_t* src;
+  const uint8_t* src;  // 1D: bytes; TMA (tma != 0): the tensor map, box at (x, y)
   uint32_t bytes, dst;
+  int tma, x, y;
 };
+constexpr int kW2Box = 8;  // slabs per W2 TMA box (box = 8 slabs x 1792 B = 14336 B)
 __device__ __forceinline__ int ev_ncopies(const HEv& ev, const HPart& P) {
   switch (ev.type) {
     case EV_T: return 1 + P.rows;
     case EV_P1: return 2 + P.rows;
     case EV_FV: return 2;
     case EV_FU: return ev.n;
-    case EV_P2: return ev.n;
+    case EV_P2: return (ev.n + kW2Box - 1) / kW2Box;
     case EV_V2: return ev.n + 1;
     default: return 0;
   }
@@ -255,14 +295,14 @@ __device__ __forceinline__ uint32_t ev_bytes(const HEv& ev, const HPart& P) {
     case EV_P1: return ev.n * (2 * kTileBytes + 64 * P.rows);
     case EV_FV: return ev.n * kVftInt3Bytes + 256 * P.gpr[ev.mat];
     case EV_FU: return ev.n * 2 * kPseudoInt3Bytes;
-    case EV_P2: return ev.n * 2 * kTileBytes;
+    case EV_P2: return (ev.n + kW2Box - 1) / kW2Box * kW2Box * 2 * kTileBytes;
     case EV_V2: return ev.n * (ev.mat * kVftInt3Bytes + 256 * P.gpr[2]);
     default: return 0;
   }
 }
 // x rows (binary16) of k-tiles [k0, k0 + n) at offset xo of the stage, row stride n * 64 + 16 B.
 __device__ __forceinline__ HCopy x_copy(const HdArgs& a, const HPart& P, int r, int k0, int n, uint32_t xo) {
-  HCopy c;
+  HCopy c{};
   c.src = reinterpret_cast<const uint8_t*>(a.x + (int64_t)P.xrow[r] * a.ldx + (int64_t)k0 * 32);
   c.bytes = n * 64;
   c.dst = xo + r * (n * 64 + 16);
@@ -270,7 +310,7 @@ __device__ __forceinline__ HCopy x_copy(const HdArgs& a, const HPart& P, int r, 
 }
 __device__ __forceinline__ HCopy ev_copy(const HdArgs& a, const HMats& X, const HEv& ev, const HPart& P, int KT,
                                          int i) {
-  HCopy c{nullptr, 0u, 0u};
+  HCopy c{nullptr, 0u, 0u, 0, 0, 0};
   switch (ev.type) {
     case EV_T: {
       if (i > 0) return x_copy(a, P, i - 1, ev.a, ev.n, ev.n * kPseudoInt3Bytes);
@@ -303,10 +343,13 @@ __device__ __forceinline__ HCopy ev_copy(const HdArgs& a, const HMats& X, const 
       c.dst = i * 2 * kPseudoInt3Bytes;
       break;
     }
-    case EV_P2: {
-      c.src = X.w[2] + ((int64_t)(ev.a + (ev.aux + i) % ev.mat) * P.kt2 + 2 * ev.c) * kTileBytes;
-      c.bytes = 2 * kTileBytes;
-      c.dst = i * 2 * kTileBytes;
+    case EV_P2: {  // box i: slabs [a + 8 i, a + 8 i + 8), k-tiles 2c, 2c + 1 (u64 column 224 c)
+      c.src = X.w2map;
+      c.tma = 1;
+      c.x = 224 * ev.c;
+      c.y = ev.a + kW2Box * i;
+      c.bytes = kW2Box * 2 * kTileBytes;
+      c.dst = i * kW2Box * 2 * kTileBytes;
       break;
     }
     case EV_V2: {
@@ -332,67 +375,45 @@ __device__ __forceinline__ HCopy ev_copy(const HdArgs& a, const HMats& X, const 
 // (S0 from acc[0], S1 from acc[1] when `two`): scattered to the warp's scratch as
 // [slab][tok][64], then 16-byte reductions.
 template <int NT>
-__device__ __forceinline__ void hd_epilogue2(const HdArgs& a, const HPart& P, float* scr,
-                                             const float (&acc)[2][4][NT][4], int S0, int S1, bool two, int lane) {
+__device__ __forceinline__ void hd_epi_slab(const HdArgs& a, const HPart& P, const float (&acc)[4][NT][4], int S,
+                                            int lane) {
   const int g = lane >> 2, q = lane & 3;
   float* dst = a.out_dtype == 0 ? static_cast<float*>(a.out) : a.acc;
   const int64_t ld = a.out_dtype == 0 ? a.ldo : a.d;
+  if (P.rows <= 2) {  // decode: reductions straight from the fragments (lanes q == 0 hold tokens 0, 1)
+    if (q == 0 && !(a.dbg_flags & 1)) {
 #pragma unroll
-  for (int x = 0; x < 2; ++x) {
-    if (x == 1 && !two) break;
+      for (int tk = 0; tk < 2; ++tk) {
+        if (tk >= P.rows) break;
+        float* row = dst + (int64_t)P.xrow[tk] * ld + S * 64 + g;
+        const float w = P.wt[tk];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int tok = 8 * nt + 2 * q + (e & 1), n = 16 * i + g + 8 * (e >> 1);
-          scr[tok * kHdScr + n] = acc[x][i][nt][e];
+        for (int i = 0; i < 4; ++i) {
+          red_add_f32(row + 16 * i, w * acc[i][0][tk]);
+          red_add_f32(row + 16 * i + 8, w * acc[i][0][2 + tk]);
         }
-    __syncwarp();
-    const int S = x ? S1 : S0;
-    for (int v = lane; v < P.rows * 16; v += 32) {
-      const int tok = v >> 4, c4 = v & 15;
-      float4 val = *reinterpret_cast<const float4*>(scr + tok * kHdScr + 4 * c4);
-      const float w = P.wt[tok];
-      val.x *= w;
-      val.y *= w;
-      val.z *= w;
-      val.w *= w;
-      if (!(a.dbg_flags & 1)) red_add_v4(dst + (int64_t)P.xrow[tok] * ld + S * 64 + 4 * c4, val);
+      }
     }
-    __syncwarp();
+    return;
   }
-}
-
-template <int NT>
-__device__ __forceinline__ void hd_epilogue(const HdArgs& a, const HPart& P, float* scr, const float (&acc)[4][NT][4],
-                                            int S, int lane) {
-  const int g = lane >> 2, q = lane & 3;
+  // 4 consecutive columns (lanes g .. g + 3 of one q) gathered into lanes g % 4 == 0,
+  // then one 16-byte reduction per (column quad, token)
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
+        const float v = acc[i][nt][e];
+        const float v1 = __shfl_down_sync(0xffffffffu, v, 4);
+        const float v2 = __shfl_down_sync(0xffffffffu, v, 8);
+        const float v3 = __shfl_down_sync(0xffffffffu, v, 12);
         const int tok = 8 * nt + 2 * q + (e & 1), n = 16 * i + g + 8 * (e >> 1);
-        scr[tok * kHdScr + n] = acc[i][nt][e];
+        if ((g & 3) == 0 && tok < P.rows && !(a.dbg_flags & 1)) {
+          const float w = P.wt[tok];
+          red_add_v4(dst + (int64_t)P.xrow[tok] * ld + S * 64 + n, make_float4(w * v, w * v1, w * v2, w * v3));
+        }
       }
-  __syncwarp();
-  float* dst = a.out_dtype == 0 ? static_cast<float*>(a.out) : a.acc;
-  const int64_t ld = a.out_dtype == 0 ? a.ldo : a.d;
-  const int nv = P.rows * 16;
-  for (int v = lane; v < nv; v += 32) {
-    const int tok = v >> 4, c4 = v & 15;
-    float4 val = *reinterpret_cast<const float4*>(scr + tok * kHdScr + 4 * c4);
-    const float w = P.wt[tok];
-    val.x *= w;
-    val.y *= w;
-    val.z *= w;
-    val.w *= w;
-    if (!(a.dbg_flags & 1)) red_add_v4(dst + (int64_t)P.xrow[tok] * ld + S * 64 + 4 * c4, val);
-  }
-  __syncwarp();
 }
 
 __device__ __forceinline__ void wait_count(const int32_t* p, int v) {
@@ -424,17 +445,17 @@ __device__ __forceinline__ float& accel(float (&acc)[2][4][NT][4], int x) {
 
 // ------------------------------------------------------------------ the kernel
 template <int NT>
-__global__ void __launch_bounds__(HdCfg<NT>::kThreads, 1) hdec_kernel(const __grid_constant__ HdArgs a) {
+__global__ void __launch_bounds__(HdCfg<NT>::kThreads, HdCfg<NT>::kCtasPerSm) hdec_kernel(const __grid_constant__ HdArgs a) {
   using CF = HdCfg<NT>;
   constexpr int kHdCons = CF::kCons, kHdThreads = CF::kThreads, kHdStage = CF::kStage;
   constexpr int kCT = 32 * kHdCons;  // consumer threads
   constexpr int NS = CF::kNS;
   constexpr int kAcc = 32 * NT;  // accumulator values per lane of a P1 piece
-  static_assert(CF::kBytes <= 227 * 1024, "hdec shared memory");
-  static_assert(NT != 1 || (32 * (2 * kTileBytes + 64) + 16 <= kHdStage && 24 * (2 * kTileBytes + 8 * 64) + 8 * 16 <= kHdStage), "P1 stage");
+  static_assert(CF::kBytes * CF::kCtasPerSm <= (CF::kCtasPerSm == 1 ? 227 * 1024 : 226 * 1024), "hdec shared memory");
+  static_assert(NT != 1 || (24 * (2 * kTileBytes + 4 * 64) + 4 * 16 <= kHdStage && 12 * (2 * kTileBytes + 8 * 64) + 8 * 16 <= kHdStage), "P1 stage");
   static_assert(NT != 2 || (16 * (2 * kTileBytes + 8 * 64) + 8 * 16 <= kHdStage && 8 * (2 * kTileBytes + 16 * 64) + 16 * 16 <= kHdStage), "P1 stage");
   static_assert(CF::kP2 * 2 * kTileBytes <= kHdStage, "P2 stage");
-  static_assert(kHdTK * kPseudoInt3Bytes + 16 * (kHdTK * 64 + 16) <= kHdStage, "T stage");
+  static_assert(kHdTK * kPseudoInt3Bytes + 8 * NT * (kHdTK * 64 + 16) <= kHdStage, "T stage");
   static_assert(CF::kFV * kVftInt3Bytes + 2048 <= kHdStage && CF::kFU * 2 * kPseudoInt3Bytes <= kHdStage, "FIN stages");
   extern __shared__ __align__(128) uint8_t smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -593,8 +614,14 @@ __global__ void __launch_bounds__(HdCfg<NT>::kThreads, 1) hdec_kernel(const __gr
   }
   if (dbg != nullptr && tid == 0) dbg[1] = globaltimer();
   const long long Tot = (long long)U * (KT + KT / 2);
+  HRange rng;
+  rng.init(Tot, G, nT, nV);
 
   if (warp >= kHdCons) {
+    if constexpr (CF::kSetMaxNreg) {  // registers from the producer warpgroup to the consumers
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(CF::kProdRegs));
+      if (warp >= kHdCons + kHdProd) return;  // the warpgroup's idle warps
+    }
     // ---------------- producer warps: both walk every event; producer p streams the stages
     // n with n % kHdProd == p and publishes their descriptors once the next copy event
     // (whoever streams it) shows that no more trailing flags follow.  The walk is plain
@@ -609,7 +636,7 @@ __global__ void __launch_bounds__(HdCfg<NT>::kThreads, 1) hdec_kernel(const __gr
     long long twait = 0;
     HMats X;
     const int UPr = KT + KT / 2, d64 = d / 64, nchT = (KT + kHdTK - 1) / kHdTK;
-    const long long lo = (long long)cta * Tot / G, hi = (long long)(cta + 1) * Tot / G;
+    const long long lo = rng.lo(cta), hi = rng.lo(cta + 1);
     // The event walk, as one state machine over register scalars with a single
     // emit site (an inlined emit per event kind made the producer ~10K SASS
     // instructions and thrashed the SM sub-partitions' instruction caches).
@@ -714,16 +741,16 @@ __global__ void __launch_bounds__(HdCfg<NT>::kThreads, 1) hdec_kernel(const __gr
             have = true;
           } else if (p1b == p1a) {  // no P1 part: a P2 tail, h comes from the tail holder
             hwait = true;
-            tail = (uint16_t)hd_owner((long long)pu * UPr + KT - 1, Tot, G);
+            tail = (uint16_t)rng.owner((long long)pu * UPr + KT - 1);
             sub = 3;
-            k = q0;
+            k = 0;
           } else if (p1b < KT) {
             hd.flags |= F_HEADPUB;
             sub = 3;
-            k = q0;
+            k = 0;
           } else {
             hd.flags |= F_FINBEGIN;
-            hd.head = (uint16_t)(p1a > 0 ? hd_owner((long long)pu * UPr, Tot, G) : cta);
+            hd.head = (uint16_t)(p1a > 0 ? rng.owner((long long)pu * UPr) : cta);
             sub = 1;
             mt = 0;
             k = 0;
@@ -756,17 +783,18 @@ __global__ void __launch_bounds__(HdCfg<NT>::kThreads, 1) hdec_kernel(const __gr
           } else {
             if (P.nks[2] > 0) hd.flags |= F_T2DONE;
             sub = 3;
-            k = q0;
+            k = 0;
           }
-        } else {  // P2 stages, slab order rotated per CTA (spreads the output reductions)
-          if (k < q1) {
-            const int len = q1 - q0;
+        } else {  // P2 stages (contiguous slab ranges for the TMA boxes), their order rotated
+                  // per CTA so the grid's output reductions do not all hit the same columns at once
+          const int nst = (q1 - q0 + CF::kP2 - 1) / CF::kP2;
+          if (k < nst) {
+            const int kk = (k + cta) % nst;
             ev.type = EV_P2;
-            ev.a = q0;
-            ev.mat = len;
-            ev.aux = (k - q0 + cta * 5) % len;
-            ev.n = min(CF::kP2, q1 - k);
-            k += ev.n;
+            ev.a = q0 + kk * CF::kP2;
+            ev.n = min(CF::kP2, q1 - ev.a);
+            ev.mat = 0;
+            ++k;
             have = true;
           } else {
             sub = -1;
@@ -812,7 +840,7 @@ __global__ void __launch_bounds__(HdCfg<NT>::kThreads, 1) hdec_kernel(const __gr
       if ((n & (kHdProd - 1)) == p) {
         const HPart& P = parts[ev.j];
         if (ev.j != xj) {
-          X.load(a.experts[P.e]);
+          X.load(a.experts[P.e], a.w2maps + (int64_t)P.e * 128);
           xj = ev.j;
         }
         const uint32_t r = (uint32_t)(n / NS);
@@ -827,9 +855,13 @@ __global__ void __launch_bounds__(HdCfg<NT>::kThreads, 1) hdec_kernel(const __gr
         const int nc = nocopy ? 0 : ev_ncopies(ev, P);
         for (int i = lane; i < nc; i += 32) {
           const HCopy c = ev_copy(a, X, ev, P, KT, i);
-          bulk_g2s_hint(ring + s * kHdStage + c.dst, c.src, c.bytes, &full[s], pol);
+          if (c.tma)
+            tma_2d_g2s_hint(ring + s * kHdStage + c.dst, c.src, c.x, c.y, &full[s], pol);
+          else
+            bulk_g2s_hint(ring + s * kHdStage + c.dst, c.src, c.bytes, &full[s], pol);
         }
         held = s;
+        if (dbg != nullptr && lane == 0 && n < 64) a.dbg[(int64_t)kHdDbgG * 128 + (int64_t)cta * 64 + n] = globaltimer();
       }
       hd = HDesc{};
       hd.type = (uint8_t)ev.type;
@@ -870,6 +902,7 @@ __global__ void __launch_bounds__(HdCfg<NT>::kThreads, 1) hdec_kernel(const __gr
   }
 
   // ---------------- consumer warps
+  if constexpr (CF::kSetMaxNreg) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(CF::kConsRegs));
   if (a.dbg_flags & 16) return;
   DqConsts* dqs = reinterpret_cast<DqConsts*>(smem + CF::kOffDq);
   if (tid < 2) dqs[tid] = make_dq_consts(tid);
@@ -878,7 +911,7 @@ __global__ void __launch_bounds__(HdCfg<NT>::kThreads, 1) hdec_kernel(const __gr
   const int ct = tid;  // consumer thread 0 .. kCT - 1
   int n = 0, nev = 0;
   long long cwait = 0;
-  bool zero_seen = false, t2_flushed = false;
+  bool zero_seen = false;
   int tc_tag = -1;  // participant whose t (ranks <= 64) is in tcache
   const int nch = (KT + kHdTK - 1) / kHdTK;
   int slot = 0;
@@ -886,8 +919,14 @@ __global__ void __launch_bounds__(HdCfg<NT>::kThreads, 1) hdec_kernel(const __gr
   for (;;) {
     {
       const long long t0 = dbg != nullptr ? clock64() : 0;
+      const long long g0 = dbg != nullptr && tid == 0 ? globaltimer() : 0;
       mbar_wait(&full[slot], fph);
       if (dbg != nullptr) cwait += clock64() - t0;
+      if (dbg != nullptr && tid == 0 && n < 64) {
+        long long* w = a.dbg + (int64_t)kHdDbgG * 192 + ((int64_t)cta * 64 + n) * 2;
+        w[0] = g0;
+        w[1] = globaltimer();
+      }
     }
     ++n;
     const HDesc D = desc[slot];
@@ -944,19 +983,21 @@ __global__ void __launch_bounds__(HdCfg<NT>::kThreads, 1) hdec_kernel(const __gr
       BTile<NT> b0, b1;
       load_bs<NT>(b0, hbuf, 72, 16, 0, g, q);
       load_bs<NT>(b1, hbuf, 72, 16, 32, g, q);
-      float* scr = red + warp * (8 * NT * kHdScr);
       // warp w: slab pairs (w + 2 kCons p, w + 2 kCons p + kCons), p = 0 .. kP2 / (2 kCons) - 1
       constexpr int L2 = kHdCons;
       float acc2[2][4][NT][4];
+      const int p2_end = (a.dbg_flags & 128) ? 0 : D.n;  // experiment bit 7: no P2 compute
 #pragma unroll 1
-      for (int l = warp; l < D.n; l += 2 * kHdCons) {
+      for (int l = warp; l < p2_end; l += 2 * kHdCons) {
         const bool two = l + L2 < D.n;
 #pragma unroll
         for (int x = 0; x < kAcc; ++x) accel<NT>(acc2, x) = 0.0f;
         tile_real<NT, 2, 2>(st + l * 2 * kTileBytes, two ? L2 * 2 * kTileBytes : 0, b0, acc2, dq, lane);
         tile_real<NT, 2, 2>(st + l * 2 * kTileBytes + kTileBytes, two ? L2 * 2 * kTileBytes : 0, b1, acc2, dq, lane);
-        if (!(a.dbg_flags & 2))
-          hd_epilogue2<NT>(a, P, scr, acc2, D.a + (D.aux + l) % D.mat, D.a + (D.aux + l + L2) % D.mat, two, lane);
+        if (!(a.dbg_flags & 2)) {
+          hd_epi_slab<NT>(a, P, acc2[0], D.a + l, lane);
+          if (two) hd_epi_slab<NT>(a, P, acc2[1], D.a + l + L2, lane);
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[slot]);
@@ -970,16 +1011,6 @@ __global__ void __launch_bounds__(HdCfg<NT>::kThreads, 1) hdec_kernel(const __gr
         ++nev;
       }
       continue;
-    }
-    if ((D.type == EV_V2 || (D.flags & F_END)) && !t2_flushed) {
-      // this CTA's units are done: publish their t2 contributions (one fence)
-      t2_flushed = true;
-      cons_bar<NT>();
-      if (ct == 0) {
-        __threadfence();
-        for (int j = 0; j < kHdMaxParts; ++j)
-          if (pend[j] > 0) atomicAdd(&a.ctrl[4 + j], (int)pend[j]);
-      }
     }
     if (D.flags & F_END) break;
     const HPart& P = parts[D.j];
@@ -1194,8 +1225,7 @@ __global__ void __launch_bounds__(HdCfg<NT>::kThreads, 1) hdec_kernel(const __gr
         }
         cons_bar<NT>();
         const float* vst = reinterpret_cast<const float*>(st + D.n * nk * kVftInt3Bytes);
-        float* scr = red + warp * (8 * NT * kHdScr);
-        for (int l = warp; l < D.n; l += kHdCons) {
+          for (int l = warp; l < D.n; l += kHdCons) {
           float acc[4][NT][4], Dm[4][NT][4];
 #pragma unroll
           for (int i = 0; i < 4; ++i)
@@ -1260,7 +1290,7 @@ __global__ void __launch_bounds__(HdCfg<NT>::kThreads, 1) hdec_kernel(const __gr
               }
             }
           }
-          hd_epilogue<NT>(a, P, scr, acc, D.c + l, lane);
+          hd_epi_slab<NT>(a, P, acc, D.c + l, lane);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[slot]);
@@ -1271,20 +1301,22 @@ __global__ void __launch_bounds__(HdCfg<NT>::kThreads, 1) hdec_kernel(const __gr
 
     // ---- trailing steps of this stage
     if (D.flags & (F_HEADPUB | F_FINBEGIN)) {
-      // tree reduction of accP over the consumer warps (fixed order) into warp 0
-      cons_bar<NT>();  // red may still hold other warps' epilogue scratch
-#pragma unroll
+      // reduction of accP over the consumer warps into warp 0, in a fixed order through
+      // at most 4 warp slots of red: fold the top 4 warps onto the 4 below them while
+      // more than 8 remain, then halve
+      cons_bar<NT>();
+#pragma unroll 1
       for (int cnt = kHdCons; cnt > 1;) {
-        const int hf = (cnt + 1) / 2;
-        if (warp >= hf && warp < cnt)
+        const int k = cnt > 8 ? 4 : cnt / 2;  // writers [cnt - k, cnt) -> readers [cnt - 2k, cnt - k)
+        if (warp >= cnt - k && warp < cnt)
 #pragma unroll
-          for (int x = 0; x < kAcc; ++x) red[((warp - hf) * kAcc + x) * 32 + lane] = accel<NT>(accP, x);
+          for (int x = 0; x < kAcc; ++x) red[((warp - (cnt - k)) * kAcc + x) * 32 + lane] = accel<NT>(accP, x);
         cons_bar<NT>();
-        if (warp < cnt - hf)
+        if (warp >= cnt - 2 * k && warp < cnt - k)
 #pragma unroll
-          for (int x = 0; x < kAcc; ++x) accel<NT>(accP, x) += red[(warp * kAcc + x) * 32 + lane];
+          for (int x = 0; x < kAcc; ++x) accel<NT>(accP, x) += red[((warp - (cnt - 2 * k)) * kAcc + x) * 32 + lane];
         cons_bar<NT>();
-        cnt = hf;
+        cnt -= k;
       }
       if (warp == 0) {
         if (D.flags & F_HEADPUB) {
@@ -1296,7 +1328,7 @@ __global__ void __launch_bounds__(HdCfg<NT>::kThreads, 1) hdec_kernel(const __gr
 #pragma unroll
           for (int x = 0; x < kAcc; ++x) hs[x] = 0.0f;
           for (int c2 = D.head; c2 < cta; ++c2) {
-            if ((long long)c2 * Tot / G == (long long)(c2 + 1) * Tot / G) continue;  // empty range
+            if (rng.lo(c2) == rng.lo(c2 + 1)) continue;  // empty range
             const uint64_t* pp = a.part + (int64_t)c2 * 1024 * NT + lane;
             uint64_t wv[kAcc];
 #pragma unroll
@@ -1334,8 +1366,9 @@ __global__ void __launch_bounds__(HdCfg<NT>::kThreads, 1) hdec_kernel(const __gr
         }
       }
     }
-    if (D.flags & F_T2DONE) {  // counted now, published before the V2 items (one fence per CTA)
-      if (ct == 0) ++pend[D.j];
+    if (D.flags & F_T2DONE) {  // the unit's t2 reductions (all consumer warps) -> the expert's counter
+      cons_bar<NT>();
+      if (ct == 0) asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(a.ctrl + 4 + D.j) : "memory");
     }
     if (dbg != nullptr && tid == 0 && nev < 60) {
       dbg[4 + 2 * nev] = D.type | (D.n << 8) | ((long long)D.flags << 16) | ((long long)D.j << 32);

@@ -1,5 +1,6 @@
 // C-ABI implementation (include/milo_b200.h): handle management, reference-
 // order validation, workspace planning and kernel launches.  Host C++.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -1547,6 +1548,7 @@ struct milo_moe {
   int32_t rch_max[3] = {0, 0, 0};       // largest 64-rank chunk count per matrix
   bool hd_ok = true;                    // hdec_kernel eligible (int3 / no compensators, 64-multiple shapes)
   HdExp* hd_exp = nullptr;              // device: hdec_kernel's per-expert static view
+  uint8_t* hd_w2maps = nullptr;         // device: per expert, a 128-byte TMA map of W2's tiles
 };
 
 extern "C" milo_status milo_moe_create(const milo_expert_desc* experts, int32_t n_experts,
@@ -1657,6 +1659,24 @@ extern "C" milo_status milo_moe_create(const milo_expert_desc* experts, int32_t 
     }
     if (err == cudaSuccess) err = cudaMalloc(&moe->hd_exp, hx.size() * sizeof(HdExp));
     if (err == cudaSuccess) err = cudaMemcpy(moe->hd_exp, hx.data(), hx.size() * sizeof(HdExp), cudaMemcpyHostToDevice);
+    // W2 of every expert as a 2D tensor of u64: rows = 64-column slabs, columns = the
+    // slab's k-run (f / 32 tiles x 112 u64); boxes of 8 slabs x 2 k-tiles feed a P2 stage
+    std::vector<CUtensorMap> maps(dhost.size());
+    for (size_t i = 0; i < dhost.size() && moe->hd_ok; ++i) {
+      const DecMat& M = dhost[i].m[2];
+      const cuuint64_t kt2 = (cuuint64_t)M.k / 32, nslabs = (cuuint64_t)M.n / 64;
+      const cuuint64_t dims[2] = {kt2 * 112, nslabs};
+      const cuuint64_t strides[1] = {kt2 * 896};
+      const cuuint32_t box[2] = {224, (cuuint32_t)kW2Box};
+      const cuuint32_t estr[2] = {1, 1};
+      const CUresult r = cuTensorMapEncodeTiled(&maps[i], CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, (void*)M.w, dims, strides,
+                                                box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) moe->hd_ok = false;  // the h-local kernel needs the map
+    }
+    static_assert(sizeof(CUtensorMap) == 128, "tensor map size");
+    if (err == cudaSuccess) err = cudaMalloc(&moe->hd_w2maps, maps.size() * 128);
+    if (err == cudaSuccess) err = cudaMemcpy(moe->hd_w2maps, maps.data(), maps.size() * 128, cudaMemcpyHostToDevice);
   }
   {  // the prefill planner's static view (moe_plan_kernel)
     std::vector<PfExpertStatic> ps(host.size());
@@ -1689,6 +1709,7 @@ extern "C" milo_status milo_moe_create(const milo_expert_desc* experts, int32_t 
     cudaFree(moe->dec_experts);
     cudaFree(moe->pf_static);
     cudaFree(moe->hd_exp);
+    cudaFree(moe->hd_w2maps);
     delete moe;
     return fail(MILO_ERR_CUDA, "expert table upload failed: %s", cudaGetErrorString(err));
   }
@@ -1702,6 +1723,7 @@ extern "C" milo_status milo_moe_destroy(milo_moe* moe) {
   cudaFree(moe->dec_experts);
   cudaFree(moe->pf_static);
   cudaFree(moe->hd_exp);
+  cudaFree(moe->hd_w2maps);
   if (moe->host_stage) cudaFreeHost(moe->host_stage);
   if (moe->dev_stage) cudaFree(moe->dev_stage);
   if (moe->gate) cudaFree(moe->gate);
@@ -2271,7 +2293,7 @@ milo_status launch_hdec(const milo_moe* moe, const void* x, int64_t m, int32_t x
     CUDA_TRY(set_smem(hdec_kernel<NT>, CF::kBytes));
     configured_dev = dev;
   }
-  const int G = sms;
+  const int G = sms * CF::kCtasPerSm;
   const int64_t KT = moe->d / 32, nch = (KT + kHdTK - 1) / kHdTK;
   const int64_t np_max = std::min<int64_t>(moe->E, m * moe->K) + moe->n_shared;
   const int64_t r16 = std::max(moe->r16_max, 16);
@@ -2311,6 +2333,7 @@ milo_status launch_hdec(const milo_moe* moe, const void* x, int64_t m, int32_t x
   a.wts_out = logits ? wts : nullptr;
   a.experts = moe->dec_experts;
   a.hexp = moe->hd_exp;
+  a.w2maps = moe->hd_w2maps;
   a.x = static_cast<const __half*>(x);
   a.ldx = moe->d;
   if (x_dtype == 0) {  // the kernel streams binary16 rows: round f32 rows once (gemm.cpp:144-146)

@@ -80,6 +80,17 @@ __device__ __forceinline__ void bulk_g2s_hint(void* dst_smem, const void* src_gm
       : "memory");
 }
 
+// 2D tensor (TMA) tile load global -> shared, completing on an mbarrier; `tmap` is the
+// generic address of a CUtensorMap in global memory (written before the launch).
+__device__ __forceinline__ void tma_2d_g2s_hint(void* dst_smem, const void* tmap, int x, int y, uint64_t* bar,
+                                                uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst_smem)),
+      "l"(tmap), "r"(x), "r"(y), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
 // Orders this thread's prior generic-proxy shared-memory accesses before
 // subsequent async-proxy (TMA/bulk copy) accesses.
 __device__ __forceinline__ void fence_proxy_async() {

@@ -24,8 +24,8 @@ lg = torch.randn(m, spec.experts, device="cuda")
 run = lambda: layer.forward(x, lg)
 for _ in range(3):
     run()
-G = torch.cuda.get_device_properties(0).multi_processor_count
-dbg = torch.zeros(G * 192, dtype=torch.int64, device="cuda")
+G = 1024  # kHdDbgG (hdec.cuh): the timeline regions are sized for 1024 CTAs
+dbg = torch.zeros(G * 320, dtype=torch.int64, device="cuda")
 L0 = mb.lib()
 L0.milo_debug_flags.argtypes = [ctypes.c_int]
 L0.milo_debug_flags(int(os.environ.get("HD_FLAGS", "0")))
@@ -44,6 +44,9 @@ L.milo_debug_timeline(None)
 dd = dbg.cpu().numpy()
 d = dd[:G * 128].reshape(G, 128)
 pr = dd[G * 128:G * 192].reshape(G, 64)
+cw = dd[G * 192:G * 320].reshape(G, 64, 2)
+G = int((d[:, 0] > 0).sum())  # CTAs of the launch
+d, pr, cw = d[:G], pr[:G], cw[:G]
 t0 = d[:, 0].min()
 NAMES = {1: "T", 2: "P1", 3: "HEADPUB", 4: "FINBEGIN", 5: "FV", 6: "FINH", 7: "FU", 8: "T2DONE", 9: "HWAIT",
          10: "P2", 11: "V2"}
@@ -81,8 +84,39 @@ for c in [0, 1, G // 2, G - 1, int(np.argmax(d[:, 2]))]:
         seq.append(f"{NAMES.get(code & 0xFF, code & 0xFF)}{(code >> 8) & 0xFF}@{(t - t0) / 1e3:.1f}")
     print(f"cta {c}: s0 {(d[c, 1] - t0) / 1e3:.1f} end {(d[c, 2] - t0) / 1e3:.1f}: " + " ".join(seq))
 
-for c in [0, G - 1]:
-    v = pr[c][:63].reshape(21, 3)
-    print(f"producer cta {c} (generated / slot free / issued, us):",
-          " | ".join(f"{(a_ - t0) / 1e3:.1f} {(b_ - t0) / 1e3:.1f} {(c_ - t0) / 1e3:.1f}" for a_, b_, c_ in v if a_ > 0))
+for c in [0, G // 2]:
+    print(f"cta {c}: stage: issued -> consumer waits from .. to (us); copy latency seen = end - issue when the consumer waited")
+    lat = []
+    for k in range(64):
+        if pr[c, k] <= 0 or cw[c, k, 1] <= 0:
+            continue
+        iss, w0, w1 = (pr[c, k] - t0) / 1e3, (cw[c, k, 0] - t0) / 1e3, (cw[c, k, 1] - t0) / 1e3
+        waited = w1 - w0 > 0.05
+        if waited:
+            lat.append(w1 - iss)
+        print(f"   {k:2d}: issued {iss:6.1f}  wait {w0:6.1f} -> {w1:6.1f} ({w1 - w0:4.2f})" + (f"  latency {w1 - iss:4.2f}" if waited else ""))
+    if lat:
+        print("   median latency when waited:", np.median(lat))
 
+# per event kind: data wait vs processing (consumer warp 0 of every CTA; stage index = event index
+# only while every event has a stage, i.e. the first 60 events)
+print("per event kind (all CTAs): mean data-wait / mean processing after the wait (us)")
+agg = {}
+for c in range(G):
+    nev = int(d[c, 125])
+    for i in range(min(nev, 60)):
+        code, tend = int(d[c, 4 + 2 * i]), d[c, 5 + 2 * i]
+        w0, w1 = cw[c, i, 0], cw[c, i, 1]
+        if w1 <= 0 or i >= 64:
+            continue
+        kname = NAMES.get(code & 0xFF, code & 0xFF)
+        fl = (code >> 16) & 0xFF
+        if kname == "P1" and fl & 4:
+            kname = "P1+FINBEGIN"
+        elif kname == "P1" and fl & 2:
+            kname = "P1+HEADPUB"
+        a_ = agg.setdefault(kname, [[], []])
+        a_[0].append((w1 - w0) / 1e3)
+        a_[1].append((tend - w1) / 1e3)
+for k_, (wv, pv) in agg.items():
+    print(f"  {k_:12s} n={len(wv):5d} wait {np.mean(wv):5.2f}  proc {np.mean(pv):5.2f} (med {np.median(pv):5.2f})")
