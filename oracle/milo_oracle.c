@@ -616,13 +616,24 @@ typedef struct {
 static void run_expert(moe_job* j) {
   const or_expert* ex = j->ex;
   const uint64_t mr = j->n_rows, d = j->d, f = ex->w[0].cols;
+  /* tile shape per matrix: (128, 128) where it divides, else one of the reference's other
+     allowed shapes (gemm.cpp:23-30: 64x256, 256x64); the tile only orders the fp32 sums */
   or_gemm_cfg cfg = {128, 128, 64, ex->w[0].mode, 4, 0};
+#define PICK_TILE(W)                                                        \
+  do {                                                                      \
+    const uint64_t kk = (W).rows, nn = (W).cols;                            \
+    if (kk % 128 == 0 && nn % 128 == 0) { cfg.tile_k = 128; cfg.tile_n = 128; } \
+    else if (kk % 256 == 0 && nn % 64 == 0) { cfg.tile_k = 256; cfg.tile_n = 64; } \
+    else if (kk % 64 == 0 && nn % 256 == 0) { cfg.tile_k = 64; cfg.tile_n = 256; } \
+  } while (0)
+  PICK_TILE(ex->w[0]);
   float* xe = (float*)malloc(mr * d * 4 + 4);
   for (uint64_t i = 0; i < mr; ++i) memcpy(xe + i * d, j->x + j->rows[i] * d, d * 4);
   float* h1 = (float*)malloc(mr * f * 4 + 4);
   float* h3 = (float*)malloc(mr * f * 4 + 4);
   int st = or_gemm_w3a16(xe, mr, d, &ex->w[0], ex->has_comp[0] ? &ex->c[0] : NULL, &cfg, h1);
   cfg.mode = ex->w[1].mode;
+  PICK_TILE(ex->w[1]);
   if (!st) st = or_gemm_w3a16(xe, mr, d, &ex->w[1], ex->has_comp[1] ? &ex->c[1] : NULL, &cfg, h3);
   if (!st) {
     for (uint64_t i = 0; i < mr * f; ++i) {
@@ -630,8 +641,10 @@ static void run_expert(moe_job* j) {
       h1[i] = a / (1.0f + expf(-a)) * h3[i];
     }
     cfg.mode = ex->w[2].mode;
+    PICK_TILE(ex->w[2]);
     st = or_gemm_w3a16(h1, mr, f, &ex->w[2], ex->has_comp[2] ? &ex->c[2] : NULL, &cfg, j->y);
   }
+#undef PICK_TILE
   j->status = st;
   free(xe);
   free(h1);

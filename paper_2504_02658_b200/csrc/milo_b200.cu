@@ -2433,7 +2433,31 @@ milo_status moe_forward_impl(milo_moe* moe, const void* x, int64_t m, int32_t x_
     return host_plan ? moe_prefill(moe, x, m, x_dtype, logits, ids, wts, out, out_dtype, stream, props.sms)
                      : moe_prefill_dev(moe, x, m, x_dtype, logits, ids, wts, out, out_dtype, stream, props.sms);
   }
-  // Token chunks keep every launch under the problem-table bound.
+  // Shapes the prefill kernel cannot take (e.g. f % 128 == 64) beyond the decode
+  // megakernel's batch: independent token chunks, each one decode-megakernel call.
+  if (!legacy_path() && m > dec_max_m && moe->E <= 256 && moe->K <= 16 && moe->d / 64 <= 4096) {
+    int64_t c = dec_max_m;
+    auto fits = [&](int64_t cm) {
+      const int64_t ne = cm * moe->K, tm = std::min<int64_t>(moe->E, ne), mp = cm <= 8 ? 8 : 16;
+      const int64_t nb = tm + (cm <= mp ? 0 : (ne - tm) / mp) + (int64_t)moe->n_shared * ((cm + mp - 1) / mp);
+      return ne <= kDecMaxEntries && nb <= kDecMaxBlocks;
+    };
+    while (c > 1 && !fits(c)) c /= 2;
+    if (fits(c)) {
+      const size_t xs = x_dtype == 0 ? 4 : 2, os = out_dtype == 0 ? 4 : 2;
+      for (int64_t t0 = 0; t0 < m; t0 += c) {
+        const int64_t mm = std::min(c, m - t0);
+        const milo_status st = moe_forward_impl(
+            moe, static_cast<const uint8_t*>(x) + t0 * moe->d * xs, mm, x_dtype, logits ? logits + t0 * moe->E : nullptr,
+            ids ? ids + t0 * moe->K : nullptr, wts ? wts + t0 * moe->K : nullptr,
+            static_cast<uint8_t*>(out) + t0 * moe->d * os, out_dtype, stream_);
+        if (st != MILO_OK) return st;
+      }
+      return MILO_OK;
+    }
+  }
+  // The round-1 multi-launch path: only with MILO_LEGACY=1 (A/B) or shapes outside every
+  // kernel's limits.  Token chunks keep every launch under the problem-table bound.
   const int nt = m <= 8 ? 1 : 2;
   const int m_pad = 8 * nt;
   const int64_t per_tok = std::max(1, moe->K) + moe->n_shared;
