@@ -42,7 +42,7 @@ def build(force: bool = False, verbose: bool = False, variant: str = "", defines
         return LIB
     os.makedirs(os.path.dirname(out), exist_ok=True)
     cmd = [NVCC, *ARCH, *FLAGS, *(f"-D{d}" for d in defines), "-I", os.path.join(ROOT, "include"), "-o", out + ".tmp",
-           os.path.join(CSRC, "milo_b200.cu"), "-lcuda"]
+           os.path.join(CSRC, "milo_b200.cu")]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = res.stdout + res.stderr
     with open(out + ".ptxas.log" if variant else os.path.join(LIB_DIR, "ptxas.log"), "w") as f:

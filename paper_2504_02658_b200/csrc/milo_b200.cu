@@ -1669,9 +1669,22 @@ extern "C" milo_status milo_moe_create(const milo_expert_desc* experts, int32_t 
       const cuuint64_t strides[1] = {kt2 * 896};
       const cuuint32_t box[2] = {224, (cuuint32_t)kW2Box};
       const cuuint32_t estr[2] = {1, 1};
-      const CUresult r = cuTensorMapEncodeTiled(&maps[i], CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, (void*)M.w, dims, strides,
-                                                box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      // the driver entry point is resolved at run time: no link-time libcuda dependency
+      using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+      static EncodeFn encode = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+          fn = nullptr;
+        return reinterpret_cast<EncodeFn>(fn);
+      }();
+      const CUresult r = encode ? encode(&maps[i], CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, (void*)M.w, dims, strides, box,
+                                         estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE)
+                                : CUDA_ERROR_NOT_SUPPORTED;
       if (r != CUDA_SUCCESS) moe->hd_ok = false;  // the h-local kernel needs the map
     }
     static_assert(sizeof(CUtensorMap) == 128, "tensor map size");
