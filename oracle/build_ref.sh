@@ -28,3 +28,11 @@ wait
 g++ -shared -o "$OUT/libmilo_ref.so" "$OBJ"/*.o -lpthread
 rm -rf "$OBJ"
 echo "built $OUT/libmilo_ref.so"
+# INTEGRATION.md section 2 compiled: the reference's types / gemm_w3a16 beside the B200
+# library through include/milo_b200.hpp (needs the B200 library built first)
+B200="$HERE/../paper_2504_02658_b200/lib/libmilo_b200.so"
+if [ -f "$B200" ]; then
+  g++ $CXXFLAGS -I"$HERE/../include" "$HERE/ref/b200_binding_check.cpp" "$OUT/libmilo_ref.so" "$B200" \
+    -Wl,-rpath,'$ORIGIN' -Wl,-rpath,'$ORIGIN/../../paper_2504_02658_b200/lib' -o "$OUT/b200_binding_check"
+  echo "built $OUT/b200_binding_check"
+fi
