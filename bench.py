@@ -186,10 +186,31 @@ class CpuReference:
                 f"({cpu_model()}); weights resident in host RAM")
 
 
+def rank_summary(spec):
+    """The compensator ranks of the benchmarked layer: the frozen plan's policy and
+    per-matrix ranks (w1, w3, w2 per expert), else the config's rank vector."""
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from paper_2504_02658_b200.synth import expert_ranks, load_rank_plan
+    plan = load_rank_plan(spec)
+    if plan is None:
+        return {"routed": list(spec.routed_ranks), "shared": spec.rank_shared}
+    routed = [expert_ranks(spec, e, plan) for e in range(spec.experts)]
+    flat = [r for t in routed for r in t]
+    out = {"plan": f"{spec.plan}.plan.json ({plan.policy}, the reference's plan_ranks; "
+                   "tools/make_rank_plans.py)", "avg_routed": round(float(np.mean(flat)), 2),
+           "min_routed": int(min(flat)), "max_routed": int(max(flat))}
+    if spec.experts <= 8:
+        out["routed_w1_w3_w2"] = routed
+    if spec.shared:
+        out["shared"] = [plan.ranks[f"layer0.shared_expert{s}.{w}"] for s in range(spec.shared)
+                         for w in ("w1", "w3", "w2")]
+    return out
+
+
 def config_dict(spec, m, parallelism):
     return {"workload": spec.name, "batch": m, "experts": spec.experts, "top_k": spec.top_k,
             "d": spec.d, "f": spec.f, "shared_experts": spec.shared,
-            "ranks": list(spec.routed_ranks), "rank_shared": spec.rank_shared,
+            "ranks": rank_summary(spec),
             "parallelism": parallelism, "tokens_per_rank": m,
             "inputs": "numpy default_rng(seed*1000 + 16 m + rank): x N(0,1) as binary16, logits N(0,1) f32",
             "l2": "flushed between steps (256 MiB write + 256 MiB read, outside the timed events)"}

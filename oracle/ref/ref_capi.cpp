@@ -17,6 +17,7 @@
 #include <optional>
 #include <random>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "milo/errors.hpp"
@@ -26,6 +27,8 @@
 #include "milo/pack.hpp"
 #include "milo/pipeline.hpp"
 #include "milo/quant.hpp"
+#include "milo/rank_policy.hpp"
+#include "milo/stats.hpp"
 #include "milo/synth.hpp"
 #include "milo/tensor_store.hpp"
 
@@ -612,6 +615,77 @@ int ref_moe_forward(void* h, const float* x, std::uint64_t m, std::uint64_t d, i
         const std::size_t r = cursor[static_cast<std::size_t>(e)]++;
         const float* yr = &y[static_cast<std::size_t>(e)].data[r * d];
         for (std::size_t j = 0; j < d; ++j) out[t * d + j] += w * yr[j];
+      }
+  });
+}
+
+// A rank plan by the reference's own pipeline pieces, for a one-layer model of
+// `experts` routed experts (layer0.expert<x>.w1|w2|w3, synth.cpp:32-48) plus `shared`
+// shared experts (layer0.shared_expert<s>.*, StructureTag::SharedExpert): per-matrix
+// kurtosis (stats.cpp) of the reference's synthetic StudentTMix weights
+// (synth_matrix, df_min = 5: heavier tails for higher expert indices), then
+// plan_ranks(manifest, stats, parse_policy(policy)) (rank_policy.cpp:94-164).  Weights
+// are synthesized at stats_rows x stats_cols (their per-expert distribution does not
+// depend on the shape; 0 = the model's shape).  ranks: (experts + shared) x 3 in
+// w1, w3, w2 order; kurt: experts x 3.  Returns 0, or the ErrorCode + 1.
+int ref_plan_synth(int experts, int shared, std::uint64_t model_dim, std::uint64_t ffn_dim,
+                   std::uint64_t stats_rows, std::uint64_t stats_cols, std::uint64_t seed,
+                   const char* policy, int32_t* ranks, double* kurt) {
+  return guarded([&] {
+    SynthSpec spec;
+    spec.layers = 1;
+    spec.experts = experts;
+    spec.model_dim = model_dim;
+    spec.ffn_dim = ffn_dim;
+    spec.seed = seed;
+    spec.expert_dist = ExpertDist::StudentTMix;
+    spec.expert_df_min = 5.0;
+    ModelManifest man = synth_manifest(spec);
+    for (int s = 0; s < shared; ++s)
+      for (const char* w : {"w1", "w2", "w3"}) {
+        MatrixEntry e;
+        e.name = "layer0.shared_expert" + std::to_string(s) + "." + w;
+        e.rows = std::string(w) == "w2" ? ffn_dim : model_dim;
+        e.cols = std::string(w) == "w2" ? model_dim : ffn_dim;
+        e.structure_tag = StructureTag::SharedExpert;
+        man.layers[0].matrices.push_back(e);
+      }
+    std::vector<const MatrixEntry*> exp;
+    for (const MatrixEntry* e : man.all_matrices())
+      if (e->structure_tag == StructureTag::Expert) exp.push_back(e);
+    std::vector<double> k(exp.size());
+    std::vector<std::thread> pool;
+    const unsigned nt = std::max(1u, std::thread::hardware_concurrency());
+    for (unsigned t = 0; t < nt; ++t)
+      pool.emplace_back([&, t] {
+        for (std::size_t i = t; i < exp.size(); i += nt) {
+          MatrixEntry e = *exp[i];
+          if (stats_rows) {
+            e.rows = stats_rows;
+            e.cols = stats_cols;
+          }
+          k[i] = kurtosis(synth_matrix(spec, e));
+        }
+      });
+    for (auto& th : pool) th.join();
+    std::map<std::string, MatrixStats> stats;
+    for (std::size_t i = 0; i < exp.size(); ++i) {
+      MatrixStats s;
+      s.name = exp[i]->name;
+      s.kurtosis = k[i];
+      s.structure_tag = StructureTag::Expert;
+      stats[s.name] = s;
+    }
+    const RankPlan plan = plan_ranks(man, stats, parse_policy(policy));
+    const char* order[3] = {"w1", "w3", "w2"};
+    for (int x = 0; x < experts + shared; ++x)
+      for (int j = 0; j < 3; ++j) {
+        const std::string name = x < experts ? "layer0.expert" + std::to_string(x) + "." + order[j]
+                                             : "layer0.shared_expert" + std::to_string(x - experts) + "." + order[j];
+        ranks[x * 3 + j] = static_cast<int32_t>(plan.ranks.at(name));
+        if (x < experts)
+          for (std::size_t i = 0; i < exp.size(); ++i)
+            if (exp[i]->name == name) kurt[x * 3 + j] = k[i];
       }
   });
 }

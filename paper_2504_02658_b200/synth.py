@@ -9,6 +9,7 @@ the reference's k x n orientation (synth.cpp:37-39), SURVEY.md section 8.
 """
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass, field
 from typing import List, Optional
 
@@ -30,18 +31,33 @@ class ConfigSpec:
     f_shared: int = 0
     rank_shared: int = 0
     routed_ranks: tuple = (16,)
+    plan: Optional[str] = None  # frozen rank plan (plans/<plan>.plan.json), else routed_ranks / rank_shared
 
 
+# Ranks: frozen plans made by the reference's own plan_ranks (tools/make_rank_plans.py:
+# Kurtosis-16 over the reference's synthetic StudentTMix experts; DeepSeek adds
+# Dense-512 for the shared experts) -- adaptive, ragged per matrix (0 .. 54 for Mixtral).
 CONFIGS = {
-    # configs[1]: Mixtral-8x7B MoE layer, 8 experts top-2, adaptive (ragged) ranks
+    # configs[1]: Mixtral-8x7B MoE layer, 8 experts top-2
     "mixtral": ConfigSpec("mixtral-8x7b-layer", 4096, 14336, 8, 2, 0,
-                          routed_ranks=(16, 32, 8, 24, 16, 0, 32, 16)),
-    # configs[2]: DeepSeek-MoE-16B layer, 64 routed (f=1408) top-6 + 2 shared, ragged ranks
+                          routed_ranks=(16, 32, 8, 24, 16, 0, 32, 16), plan="mixtral"),
+    # configs[2]: DeepSeek-MoE-16B layer, 64 routed (f=1408) top-6 + 2 shared
     "deepseek": ConfigSpec("deepseek-moe-16b-layer", 2048, 1408, 64, 6, 1, shared=2,
-                           f_shared=1408, rank_shared=512, routed_ranks=(16, 0, 32, 8, 16, 24)),
+                           f_shared=1408, rank_shared=512, routed_ranks=(16, 0, 32, 8, 16, 24), plan="deepseek"),
     # configs[4]: Arctic-480B-shaped layer, 128 experts top-2
-    "arctic": ConfigSpec("arctic-480b-layer", 7168, 4864, 128, 2, 0, routed_ranks=(16, 8, 32, 16)),
+    "arctic": ConfigSpec("arctic-480b-layer", 7168, 4864, 128, 2, 0, routed_ranks=(16, 8, 32, 16),
+                         plan="arctic"),
 }
+
+PLAN_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "plans")
+
+
+def load_rank_plan(spec: ConfigSpec):
+    """The config's frozen plan (policy, {matrix name: rank}) or None."""
+    if spec.plan is None:
+        return None
+    from .artifacts import load_plan
+    return load_plan(os.path.join(PLAN_DIR, spec.plan + ".plan.json"))
 
 
 def packed_random_words(rows: int, cols: int, rng: np.random.Generator,
@@ -63,7 +79,10 @@ class HostExpert:
     ranks: List[int] = field(default_factory=list)
 
 
-def expert_ranks(spec: ConfigSpec, e: int) -> List[int]:
+def expert_ranks(spec: ConfigSpec, e: int, plan=None) -> List[int]:
+    """Ranks of w1, w3, w2 of routed expert e (plan names: synth.cpp:32-48)."""
+    if plan is not None:
+        return [plan.ranks[f"layer0.expert{e}.{w}"] for w in ("w1", "w3", "w2")]
     r = spec.routed_ranks
     return [r[(3 * e + j) % len(r)] for j in range(3)]
 
@@ -71,16 +90,18 @@ def expert_ranks(spec: ConfigSpec, e: int) -> List[int]:
 def build_host_layer(spec: ConfigSpec, seed: int = 0):
     """Host-side packed experts (routed, shared) for a config."""
     rng = np.random.default_rng(seed)
+    plan = load_rank_plan(spec)
     routed, shared = [], []
     for e in range(spec.experts):
-        ranks = expert_ranks(spec, e)
+        ranks = expert_ranks(spec, e, plan)
         dims = [(spec.d, spec.f), (spec.d, spec.f), (spec.f, spec.d)]
         routed.append(HostExpert([packed_random_words(k, n, rng) for k, n in dims],
                                  [random_compensator(k, n, r, rng) for (k, n), r in zip(dims, ranks)],
                                  ranks))
     for s in range(spec.shared):
         dims = [(spec.d, spec.f_shared), (spec.d, spec.f_shared), (spec.f_shared, spec.d)]
-        ranks = [spec.rank_shared] * 3
+        ranks = ([plan.ranks[f"layer0.shared_expert{s}.{w}"] for w in ("w1", "w3", "w2")] if plan is not None
+                 else [spec.rank_shared] * 3)
         shared.append(HostExpert([packed_random_words(k, n, rng) for k, n in dims],
                                  [random_compensator(k, n, r, rng) for (k, n), r in zip(dims, ranks)],
                                  ranks))

@@ -12,6 +12,7 @@ import pytest
 from oracle.oracle import Comp, GemmCfg, OracleError, Packed
 
 GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "golden_v1.npz")
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 @pytest.fixture(scope="module")
@@ -234,3 +235,37 @@ def test_router_gemm_restatement_is_a_dot_product(oracle):
         assert np.allclose(got, want, rtol=1e-5, atol=1e-6 * np.abs(want).max())
         # lane-order arithmetic: exactly reproducible
         assert np.array_equal(got, oracle.router_gemm(x, gate.view(np.uint16)))
+
+
+def test_frozen_rank_plans_are_the_references():
+    """paper_2504_02658_b200/plans/*.plan.json (the benchmark layers' ranks) are what the
+    reference's plan_ranks gives (tools/make_rank_plans.py); re-derived here when the
+    compiled reference is present (Mixtral: 24 matrices of 4096 x 14336 synthetic weights)."""
+    import json
+    from paper_2504_02658_b200.artifacts import load_plan
+    from paper_2504_02658_b200.synth import CONFIGS, PLAN_DIR
+    for name, spec in CONFIGS.items():
+        path = os.path.join(PLAN_DIR, f"{spec.plan}.plan.json")
+        plan = load_plan(path)
+        routed = [plan.ranks[f"layer0.expert{e}.{w}"] for e in range(spec.experts) for w in ("w1", "w3", "w2")]
+        assert abs(np.mean(routed) - 16.0) < 1e-9, name  # Kurtosis-16: total = 16 x #expert matrices
+        assert plan.policy.endswith("Kurtosis-16")
+        if spec.shared:
+            assert all(plan.ranks[f"layer0.shared_expert{s}.{w}"] == 512
+                       for s in range(spec.shared) for w in ("w1", "w3", "w2"))
+    lib_path = os.path.join(ROOT, "oracle", "_ref", "libmilo_ref.so")
+    if not os.path.exists(lib_path):
+        return
+    import ctypes
+    lib = ctypes.CDLL(lib_path)
+    f = lib.ref_plan_synth
+    f.restype = ctypes.c_int
+    f.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                  ctypes.c_uint64, ctypes.c_uint64, ctypes.c_char_p, ctypes.c_void_p, ctypes.c_void_p]
+    spec = CONFIGS["mixtral"]
+    ranks = np.zeros(spec.experts * 3, np.int32)
+    kurt = np.zeros(spec.experts * 3, np.float64)
+    assert f(spec.experts, 0, spec.d, spec.f, 0, 0, 0, b"Kurtosis-16", ranks.ctypes.data, kurt.ctypes.data) == 0
+    frozen = json.load(open(os.path.join(PLAN_DIR, "mixtral.plan.json")))["ranks"]
+    want = [frozen[f"layer0.expert{e}.{w}"] for e in range(spec.experts) for w in ("w1", "w3", "w2")]
+    assert ranks.tolist() == want
