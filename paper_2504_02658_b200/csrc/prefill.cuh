@@ -303,7 +303,11 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
 
   if (warp == kPfProdWarp) {
     // ======================= packed-weight producer =======================
-    if (lane == 0) {
+    // A stage's NG x NMAT x 2 copies are issued by as many lanes in parallel: one
+    // thread serialises its bulk copies at ~300 cycles each (tools/micro/bulk_issue.cu).
+    constexpr int kCopies = NG * NMAT * 2;
+    if (lane < kCopies) {
+      const int ng = lane / (NMAT * 2), mat = (lane / 2) % NMAT, sl = lane & 1;
       int ps = 0;
       uint32_t pph = 0;
       for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
@@ -315,15 +319,12 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
           ring_wait(&p_empty[ps], pph ^ 1);
 
           uint8_t* sP = smem + CF::kOffP + ps * CF::kStageP;
-          mbar_arrive_expect_tx(&p_full[ps], (uint32_t)CF::kStageP);
+          if (lane == 0) mbar_arrive_expect_tx(&p_full[ps], (uint32_t)CF::kStageP);
+          __syncwarp((1u << kCopies) - 1u);
           const int kst = (st + nt * 13) % ks;  // rotated k order per n-tile (spreads L2 hot spots)
-          for (int ng = 0; ng < NG; ++ng)
-            for (int mat = 0; mat < NMAT; ++mat)
-              for (int sl = 0; sl < 2; ++sl) {
-                const uint8_t* src = P.w[mat] + ((int64_t)(2 * (NG * nt + ng) + sl) * kts + 2 * kst) * kTileBytes;
-                bulk_g2s(sP + ((ng * NMAT + mat) * 2 + sl) * 2 * kTileBytes, src, 2 * kTileBytes, &p_full[ps]);
-              }
-          if (item == (int)blockIdx.x) pf_trace(st, 0);
+          const uint8_t* src = P.w[mat] + ((int64_t)(2 * (NG * nt + ng) + sl) * kts + 2 * kst) * kTileBytes;
+          bulk_g2s(sP + ((ng * NMAT + mat) * 2 + sl) * 2 * kTileBytes, src, 2 * kTileBytes, &p_full[ps]);
+          if (item == (int)blockIdx.x && lane == 0) pf_trace(st, 0);
 
           if (++ps == PS) {
             ps = 0;
@@ -331,7 +332,7 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
           }
         }
       }
-      pf_dbg(1);
+      if (lane == 0) pf_dbg(1);
     }
   } else if (warp == kPfBWarp) {
     // ======================= activation / t image producer =======================
