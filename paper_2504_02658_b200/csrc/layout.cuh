@@ -135,6 +135,56 @@ __device__ __forceinline__ void unit_dequant(uint32_t W0, uint32_t W1, uint32_t 
   }
 }
 
+// Code (c - bias) of slot t (0..4) of one packed word, as in unit_codes.
+template <int T>
+__device__ __forceinline__ __half2 slot_code(uint32_t W, uint32_t magic, const DqConsts& k) {
+  if (T == 0) return __hadd2(u32_as_h2(and_or<0x00070007u>(W, magic)), k.c0);
+  if (T == 1) return __hfma2(u32_as_h2(and_or<0x00380038u>(W, magic)), k.r8, k.c1);
+  if (T == 2) return __hfma2(u32_as_h2(and_or<0x01C001C0u>(W, magic)), k.r64, k.c2);
+  if (T == 3) return __hadd2(u32_as_h2(and_or<0x00070007u>(W >> 9, magic)), k.c0);
+  return __hfma2(u32_as_h2(and_or<0x00380038u>(W >> 9, magic)), k.r8, k.c1);
+}
+
+// Half a unit: the 8 pairs pp = 8 IH .. 8 IH + 7 (n subtiles i = 2 IH, 2 IH + 1),
+// out[4 il + r] = pair 8 IH + 4 il + r -- for consumers whose threads own only
+// half of a unit's 64 n (the prefill kernel's TMEM lane quarters).  Same
+// arithmetic per pair as unit_dequant (bit-identical weights).
+template <int IH>
+__device__ __forceinline__ void half_unit_dequant(uint32_t W0, uint32_t W1, uint32_t W2,
+                                                  const uint32_t (&S)[2], const uint32_t (&O)[2],
+                                                  const DqConsts& k, uint32_t (&out)[8]) {
+  uint32_t magic = 0x64006400u;
+  asm volatile("" : "+r"(magic));
+  __half2 e[8];
+  if (IH == 0) {
+    e[0] = slot_code<0>(W0, magic, k);
+    e[1] = slot_code<1>(W0, magic, k);
+    e[2] = slot_code<2>(W0, magic, k);
+    e[3] = slot_code<3>(W0, magic, k);
+    e[4] = slot_code<4>(W0, magic, k);
+    e[5] = slot_code<0>(W1, magic, k);
+    e[6] = slot_code<1>(W1, magic, k);
+    e[7] = slot_code<2>(W1, magic, k);
+  } else {
+    e[0] = slot_code<3>(W1, magic, k);
+    e[1] = slot_code<4>(W1, magic, k);
+    e[2] = slot_code<0>(W2, magic, k);
+    e[3] = slot_code<1>(W2, magic, k);
+    e[4] = slot_code<2>(W2, magic, k);
+    e[5] = slot_code<3>(W2, magic, k);
+    e[6] = slot_code<4>(W2, magic, k);
+    const uint32_t v = and_or<0x00040004u>(W2 >> 13,
+                                           and_or<0x00020002u>(W1 >> 14,
+                                                               and_or<0x00010001u>(W0 >> 15, magic)));
+    e[7] = __hadd2(u32_as_h2(v), k.c0);
+  }
+#pragma unroll
+  for (int pp = 0; pp < 8; ++pp) {
+    const int h = (pp & 3) >> 1;
+    out[pp] = h2_as_u32(__hfma2(e[pp], u32_as_h2(S[h]), u32_as_h2(O[h])));
+  }
+}
+
 // Raw integer codes of the 16 pairs of one unit (lo in bits 0..7, hi in 8..15).
 __device__ __forceinline__ void unit_raw_codes(uint32_t W0, uint32_t W1, uint32_t W2,
                                                uint32_t (&c)[16]) {

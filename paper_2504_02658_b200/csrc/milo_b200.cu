@@ -2248,7 +2248,7 @@ milo_status moe_prefill_dev(milo_moe* moe, const void* x, int64_t m, int32_t x_d
                     0, stream, false, (const TProb*)pa.tps[ph], 0, cnt + 2));
     // the grouped tcgen05 GEMM (persistent grid; items from the plan)
     PfArgs a{};
-    a.dbg = g_dbg;
+    a.dbg = g_dbg ? g_dbg + ph * kPfDbgLongs : nullptr;  // one timeline region per phase
     a.flags = g_dbg_flags;
     a.problems = pa.probs[ph];
     a.item_start = pa.starts[ph];

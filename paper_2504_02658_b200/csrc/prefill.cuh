@@ -29,63 +29,73 @@
 
 namespace milo_dev {
 
-#ifndef PF_NG2_AS
-#define PF_NG2_AS 3
-#endif
 #ifndef PF_NG2_GROUPS
 #define PF_NG2_GROUPS 3
 #endif
-#ifndef PF_NG2_PS
-#define PF_NG2_PS 6
+#ifndef PF_PS2
+#define PF_PS2 10  // packed ring stages of the two-matrix / two-n-tile variants
 #endif
-#ifndef PF_NG2_B
-#define PF_NG2_B 64
+#ifndef PF_PROF_MMA
+#define PF_PROF_MMA 0
+#endif
+#ifndef PF_B_KB
+#define PF_B_KB 96  // activation / t image ring (KB)
 #endif
 constexpr int kPfM = 128;              // output columns per tile (UMMA M)
 constexpr int kPfN = 128;              // tokens per tile (UMMA N, TMEM columns)
 constexpr int kPfK = 64;               // k per stage (128 B of binary16 per operand row)
 constexpr int kPfImg = kPfN * kPfK * 2;  // 16 KB: one operand image (128 rows x 128 B)
 constexpr int kPfPackedPerMat = 2 * 2 * kTileBytes;  // 2 slabs x 2 k-tiles = 3584 B
-constexpr int kPfGroupWarps = 4;       // warps per dequant group (one group per in-flight stage)
+constexpr int kPfGroupWarps = 4;       // warps per dequant group = the 4 TMEM lane quarters
 constexpr int kPfEpiWarps = 4;         // warps 0..3: TMEM lanes 32 w .. 32 w + 31
 constexpr int kPfProdWarp = 4;         // packed-weight producer
 constexpr int kPfMmaWarp = 5;
 constexpr int kPfBWarp = 6;            // activation / t image producer
-constexpr int kPfDeqWarp0 = 7;
+constexpr int kPfMmaWarp2 = 7;          // second MMA issuer (one thread issues <= 1 MMA per ~55 cycles)
+constexpr int kPfWaitWarp = 8;          // waits on the A / B rings for the issuers
+constexpr int kPfDeqWarp0 = 9;
+constexpr int kPfTraceStages = 256;    // debug timeline: CTA 0's first stages (PfArgs::dbg)
+constexpr int kPfDbgLongs = 148 * 8 + kPfTraceStages * 8;  // dbg region of one launch
 // NG = n-tiles (128 output columns each) per work item: the item's activation
 // image of a stage feeds NG MMAs (NG accumulators), so activation traffic per
-// FLOP drops by NG -- the activation ring, not the tensor core, bounds the
-// NG = 1 kernel (one 16 KB image per 128 x 128 x 64 MMA, ~2 us copy latency).
-// Groups <= A-ring slots: a group that starts stage st has only seen stage
+// FLOP drops by NG.
+// Groups <= A slots: a group that starts stage st has only seen stage
 // st - groups consumed, and its parity wait on the slot is unambiguous only
 // if the slot's barrier is at most one phase behind (st - 2 AS consumed).
 template <int NMAT, int NG = 1>
 struct PfRoles {
-  static constexpr int kGroups = NG == 2 ? PF_NG2_GROUPS : (NMAT == 1 ? 4 : 3);  // stages de-quantized concurrently
+  static constexpr int kGroups = NG == 2 ? PF_NG2_GROUPS : 3;  // stages de-quantized concurrently
   static constexpr int kDeqWarps = kGroups * kPfGroupWarps;
   static constexpr int kThreads = 32 * (kPfDeqWarp0 + kDeqWarps);
 };
 
+// The de-quantized weights (the MMA's A operand, W^T) live in TENSOR memory:
+// TMEM columns 256..511 hold kAS stages of NG x NMAT 128-row x 64-k binary16
+// tiles (32 columns each), written by the dequant warps with tcgen05.st and
+// read by tcgen05.mma straight from TMEM -- no shared-memory round trip for
+// the weights (the smem-A design moved 32 KB st.shared + 32 KB MMA reads per
+// two-matrix stage through the 128 B/clk shared-memory port, its bound at
+// small token tiles).  Columns 0..255 hold the fp32 accumulators (double
+// buffered when NG x NMAT x ntok fits 128 columns).  Shared memory keeps the
+// packed-weight ring and the activation / t image ring.
 template <int NMAT, int NG = 1>
 struct PfCfg {
-  // NG = 2: the packed (HBM) and activation (L2) rings are latency x depth
-  // bound per SM, so they get the space and A keeps PF_NG2_AS slots
-  static constexpr int kPS = NG == 2 ? PF_NG2_PS : (NMAT == 1 ? 12 : 8);      // packed-weight ring (HBM latency)
-  static constexpr int kAS = NG == 2 ? PF_NG2_AS : (NMAT == 1 ? 6 : 3);       // dequantized A ring
-  static constexpr int kBRegion = NG == 2 ? PF_NG2_B * 1024 : (NMAT == 1 ? 64 * 1024 : 32 * 1024);
+  static constexpr int kPS = (NG == 2 || NMAT == 2) ? PF_PS2 : 16;  // packed-weight ring (HBM latency)
+  static constexpr int kStageCols = NG * NMAT * 32;  // TMEM columns of one A stage
+  static constexpr int kACol0 = 256;
+  static constexpr int kAS = 256 / kStageCols;       // A slots in TMEM
+  static constexpr int kBRegion = PF_B_KB * 1024;
   static constexpr int kBSMax = 16;                      // B slots = region / (ntok_max x 128), <= 16
-  static constexpr int kStageA = NG * NMAT * kPfImg;
   static constexpr int kStageP = NG * NMAT * kPfPackedPerMat;
-  static constexpr int kOffA = 0;                        // 1024-aligned images first
-  static constexpr int kOffB = kOffA + kAS * kStageA;
+  static constexpr int kOffB = 0;                        // 1024-aligned images first
   static constexpr int kOffP = kOffB + kBRegion;
   static constexpr int kOffBar = kOffP + kPS * kStageP;
-  // p_full[PS] p_empty[PS] a_full[AS] a_empty[AS] v_full[AS] b_full[BSMax] b_empty[BSMax] acc_full[2] acc_empty[2]
-  static constexpr int kNumBars = 2 * kPS + 3 * kAS + 2 * kBSMax + 4;
+  // p_full[PS] p_empty[PS] a_full[AS] a_empty[AS] b_full[BSMax] b_empty[BSMax] acc_full[2] acc_empty[2]
+  static constexpr int kNumBars = 2 * kPS + 2 * kAS + 2 * kBSMax + 4;
   static constexpr int kOffTmem = kOffBar + kNumBars * 8;
   static constexpr int kOffStage = (kOffTmem + 16 + 127) & ~127;  // epilogue transpose [4 warps][32][33] f32
   static constexpr int kBytes = kOffStage + kPfEpiWarps * 32 * 33 * 4 + 1024;  // + alignment slack
-  static constexpr int kTmemCols = 2 * NG * NMAT * kPfN;  // double-buffered accumulators
+  static constexpr int kTmemCols = 512;
 };
 
 // One GEMM problem: a weight matrix (or w1|w3 pair) times a block of token rows.
@@ -142,6 +152,72 @@ __device__ __forceinline__ void pf_mma(uint32_t tmem_d, uint64_t da, uint64_t db
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
       ::"r"(tmem_d), "l"(da), "l"(db), "r"(idesc), "r"(accum));
 }
+// A operand from tensor memory (rows = TMEM lanes, k pairs = columns).
+__device__ __forceinline__ void pf_mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc,
+                                          uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}"
+      ::"r"(tmem_d), "r"(tmem_a), "l"(db), "r"(idesc), "r"(accum));
+}
+// Warp-converged forms: the whole warp executes them, one elected lane issues
+// (operands stay in uniform registers -- a lone-lane issuer pays register ->
+// uniform moves and an election loop per MMA).
+__device__ __forceinline__ void pf_mma_ts_w(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc,
+                                            uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}"
+      ::"r"(tmem_d), "r"(tmem_a), "l"(db), "r"(idesc), "r"(accum));
+}
+__device__ __forceinline__ void pf_commit_w(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_w(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t.reg .b64 st;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e mbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+// 16 lanes x 32 columns: thread (g = lane / 4, q = lane % 4) writes lane g
+// (v[4c], v[4c + 1]) and lane g + 8 (v[4c + 2], v[4c + 3]) at columns
+// 8c + 2q, 8c + 2q + 1 (c = 0..3) -- the mma.m16n8k16 A-fragment geometry.
+__device__ __forceinline__ void tmem_st16x256_x4(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.16x256b.x4.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+// 32 lanes x 32 columns: thread t writes lane t, columns 0..31 = v[0..31].
+__device__ __forceinline__ void tmem_st32x32_x32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]),
+      "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]),
+      "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_cta_shared(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_cta_shared(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void pf_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    smem_u32(bar))
@@ -149,6 +225,13 @@ __device__ __forceinline__ void pf_commit(uint64_t* bar) {
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
@@ -223,6 +306,15 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
   constexpr int PS = CF::kPS, AS = CF::kAS;
   const int bslot = a.ntok_max * 128;
   const int BS = min(CF::kBSMax, CF::kBRegion / bslot);
+  // accumulators: per matrix a 32-column-aligned block of ntok_max columns;
+  // two buffers when both fit the 256 accumulator columns
+  const int mstride = (a.ntok_max + 31) & ~31;
+  // one accumulator per (n-tile, matrix); a single-accumulator kernel with
+  // small token tiles splits each stage's k over two accumulators (one per
+  // MMA issuer, summed by the epilogue)
+  const bool ksplit = NG * NMAT == 1 && a.ntok_max <= 64;
+  const int acc_cols = (ksplit ? 2 : NG * NMAT) * mstride;
+  const int nacc = acc_cols <= 128 ? 2 : 1;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-B aligned base (SW128 atoms); pointer arithmetic keeps the shared address space
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -231,12 +323,12 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
   uint64_t* p_empty = p_full + PS;
   uint64_t* a_full = p_empty + PS;
   uint64_t* a_empty = a_full + AS;
-  uint64_t* v_full = a_empty + AS;
-  uint64_t* b_full = v_full + AS;
+  uint64_t* b_full = a_empty + AS;
   uint64_t* b_empty = b_full + CF::kBSMax;
   uint64_t* acc_full = b_empty + CF::kBSMax;  // [2]
   uint64_t* acc_empty = acc_full + 2;  // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + CF::kOffTmem);
+  uint32_t* stages_ready = tmem_slot + 1;  // kPfWaitWarp -> MMA issuers: stages whose A and B are in place
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -246,17 +338,17 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
     }
     for (int s = 0; s < AS; ++s) {
       mbar_init(&a_full[s], kPfGroupWarps);
-      mbar_init(&a_empty[s], 1);
-      mbar_init(&v_full[s], 1);
+      mbar_init(&a_empty[s], 2);  // one commit (or arrive) per MMA issuer
     }
     for (int s = 0; s < BS; ++s) {
       mbar_init(&b_full[s], 1);
-      mbar_init(&b_empty[s], 1);
+      mbar_init(&b_empty[s], 2);
     }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_full[i], 2);
       mbar_init(&acc_empty[i], kPfEpiWarps);
     }
+    *stages_ready = 0;
     fence_barrier_init();
   }
   if (warp == kPfMmaWarp) {
@@ -277,11 +369,14 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
     }
   };
   if (threadIdx.x == 0) pf_dbg(0);
-  auto pf_trace = [&](int stage, int role) {  // CTA 0, first 64 stages: [stage][4 roles]
-    if (a.dbg != nullptr && blockIdx.x == 0 && stage < 64) {
+  // CTA 0, first kPfTraceStages stages of its whole sequence: [stage][8 events]
+  //   0 packed issued  1 group: A slot free  2 group: packed landed  3 group: A ready
+  //   4 MMA: A seen    5 MMA: B seen         6 MMA: committed        7 B issued
+  auto pf_trace = [&](int stage, int ev) {
+    if (a.dbg != nullptr && blockIdx.x == 0 && stage < kPfTraceStages) {
       long long t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      a.dbg[148 * 8 + stage * 4 + role] = t;
+      a.dbg[148 * 8 + stage * 8 + ev] = t;
     }
   };
 
@@ -301,6 +396,22 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
     tpart = part == 1 ? 1 : 0;
   };
 
+#if PF_PROF_MMA  // experiments: MMA-thread cycle split (CTA 0 -> dbg trace row kPfTraceStages - 1)
+  long long pf_prof[4] = {0, 0, 0, 0};
+#define PF_PROF_T(v) const long long v = clock64()
+#define PF_PROF_ACC(c0, c1, c2, c3, c4) \
+  pf_prof[0] += c1 - c0;                \
+  pf_prof[1] += c2 - c1;                \
+  pf_prof[2] += c3 - c2;                \
+  pf_prof[3] += c4 - c3
+#define PF_PROF_OUT()                                                                          \
+  if (a.dbg != nullptr && blockIdx.x == 0)                                                     \
+    for (int i = 0; i < 4; ++i) a.dbg[148 * 8 + (kPfTraceStages - 1) * 8 + i] = pf_prof[i]
+#else
+#define PF_PROF_T(v)
+#define PF_PROF_ACC(c0, c1, c2, c3, c4)
+#define PF_PROF_OUT()
+#endif
   if (warp == kPfProdWarp) {
     // ======================= packed-weight producer =======================
     // A stage's NG x NMAT x 2 copies are issued by as many lanes in parallel: one
@@ -308,7 +419,7 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
     constexpr int kCopies = NG * NMAT * 2;
     if (lane < kCopies) {
       const int ng = lane / (NMAT * 2), mat = (lane / 2) % NMAT, sl = lane & 1;
-      int ps = 0;
+      int ps = 0, gs0 = 0;
       uint32_t pph = 0;
       for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
         int p, nt, tt;
@@ -324,27 +435,28 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
           const int kst = (st + nt * 13) % ks;  // rotated k order per n-tile (spreads L2 hot spots)
           const uint8_t* src = P.w[mat] + ((int64_t)(2 * (NG * nt + ng) + sl) * kts + 2 * kst) * kTileBytes;
           bulk_g2s(sP + ((ng * NMAT + mat) * 2 + sl) * 2 * kTileBytes, src, 2 * kTileBytes, &p_full[ps]);
-          if (item == (int)blockIdx.x && lane == 0) pf_trace(st, 0);
+          if (lane == 0) pf_trace(gs0 + st, 0);
 
           if (++ps == PS) {
             ps = 0;
             pph ^= 1;
           }
         }
+        gs0 += item_stages(P);
       }
       if (lane == 0) pf_dbg(1);
     }
   } else if (warp == kPfBWarp) {
     // ======================= activation / t image producer =======================
     if (lane == 0) {
-      int bs = 0;
+      int bs = 0, gs = 0;
       uint32_t bph = 0;
       for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
         int p, nt, tt;
         pf_item<NG>(a, item, p, nt, tt);
         const PfProblem P = a.problems[p];  // by value: fields live in registers
         const int ks = P.k / kPfK, total = item_stages(P);
-        for (int st = 0; st < total; ++st) {
+        for (int st = 0; st < total; ++st, ++gs) {
           ring_wait(&b_empty[bs], bph ^ 1);
           uint8_t* sB = smem + CF::kOffB + bs * bslot;
           const uint8_t* src;
@@ -358,7 +470,7 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
           }
           mbar_arrive_expect_tx(&b_full[bs], ib);
           bulk_g2s(sB, src, ib, &b_full[bs]);
-          if (item == (int)blockIdx.x) pf_trace(st, 3);
+          pf_trace(gs, 7);
           if (++bs == BS) {
             bs = 0;
             bph ^= 1;
@@ -369,11 +481,19 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
     }
   } else if (warp >= kPfDeqWarp0) {
     // ======================= dequant warps =======================
-    // group grp handles the stages st = grp (mod kPfDeqGroups): two stages are
-    // de-quantized concurrently; within a stage, warp gw does jobs gw, gw + 4, ...
+    // group grp handles the stages st = grp (mod kPfDeqGroups); within a stage,
+    // warp w writes TMEM lane quarter Q = w % 4 (the only lanes its tcgen05.st
+    // can reach): A rows 32 Q .. 32 Q + 31 = slab Q / 2, n subtiles i of half
+    // Q % 2 -- half of every unit of that slab (half_unit_dequant).  Main stage:
+    // packed tiles -> bit-exact binary16 W^T -> tcgen05.st.16x256b, k pair
+    // (q, q + 4) of each 16-k block into columns (2q, 2q + 1) (the activation
+    // images carry the same permutation, pf_image_kernel).  LoRC stage: the
+    // V^T image rows of the quarter (L2-resident) -> tcgen05.st.32x32b.
     const int dw = warp - kPfDeqWarp0;
     const int grp = dw / kPfGroupWarps, gw = dw % kPfGroupWarps;
-    const int g = lane >> 2, q = lane & 3;
+    const int Q = warp & 3, sl = Q >> 1, ih = Q & 1;
+    const int q = lane & 3;
+    const uint32_t lane_q = (uint32_t)(32 * Q) << 16;
     int ps = 0, as = 0, gs = 0;
     uint32_t pph = 0, aph = 0;
     for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
@@ -384,61 +504,73 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
       const DqConsts dq = make_dq_consts(P.mode);
       for (int st = 0; st < total; ++st, ++gs) {
         const bool mine = (gs % kPfDeqGroups) == grp;
-        uint8_t* sA = smem + CF::kOffA + as * CF::kStageA;
         if (mine) {
-          // every warp of the group waits for the A slot (a parity wait on v_full
-          // alone would pass early when this group's first stage reuses a slot
-          // whose previous phase has not completed yet); the first warp then
-          // either fetches a V image into it (LoRC stage) or releases v_full
-          ring_wait(&a_empty[as], aph ^ 1);
-          if (gw == 0 && lane == 0) {
-            if (st >= ks) {
-              int mat, ch, vpart, tpart;
-              lorc_stage(P, st - ks, mat, ch, vpart, tpart);
-              mbar_arrive_expect_tx(&v_full[as], (uint32_t)(NG * kPfImg));
-              for (int ng = 0; ng < NG; ++ng)
-                bulk_g2s(sA + (ng * NMAT + mat) * kPfImg,
-                         P.vimg[mat] + (((int64_t)(NG * nt + ng) * P.rchunks[mat] + ch) * 2 + vpart) * kPfImg, kPfImg,
-                         &v_full[as]);
-            } else {
-              mbar_arrive(&v_full[as]);
-            }
-          }
-          ring_wait(&v_full[as], aph);
+          const uint32_t a_col = tmem + (uint32_t)(CF::kACol0 + as * CF::kStageCols);
+          ring_wait(&a_empty[as], aph ^ 1);  // the MMAs that read this slot are done
+          tc_fence_after();
+          if (gw == 0 && lane == 0) pf_trace(gs, 1);
           if (st < ks) {
             ring_wait(&p_full[ps], pph);
-            if (gw == 0 && lane == 0 && item == (int)blockIdx.x) pf_trace(st, 1);
+            if (gw == 0 && lane == 0) pf_trace(gs, 2);
             const uint8_t* sP = smem + CF::kOffP + ps * CF::kStageP;
-            constexpr int kJobs = 8 * NMAT * NG / kPfGroupWarps;
+            if (!(a.flags & 1)) {
 #pragma unroll
-            for (int jb = 0; jb < ((a.flags & 1) ? 0 : kJobs); ++jb) {
-              const int jid = gw + kPfGroupWarps * jb;
-              const int j = jid & 1, t4 = jid >> 1;
-              const int kt = t4 & 1, sl = (t4 >> 1) & 1, nm = t4 >> 2;  // nm = ng * NMAT + mat
-              const uint8_t* tile = sP + ((nm * 2 + sl) * 2 + kt) * kTileBytes;
-              const uint32_t* pa = reinterpret_cast<const uint32_t*>(tile + kPlaneAOff + lane * 16);
-              const uint32_t* pb = reinterpret_cast<const uint32_t*>(tile + kPlaneBOff + lane * 8);
-              const uint4 mm = *reinterpret_cast<const uint4*>(tile + kMetaOff + q * 32 + 16 * j);
-              const uint32_t S2[2] = {mm.x, mm.z}, O2[2] = {mm.y, mm.w};
-              uint32_t wv[16];
-              unit_dequant(pa[2 * j], pa[2 * j + 1], pb[j], S2, O2, dq, wv);
-              uint8_t* A = sA + nm * kPfImg;
+              for (int nm = 0; nm < NG * NMAT; ++nm) {  // nm = ng * NMAT + mat
+                uint32_t v0[16], v1[16];  // n subtiles 2 ih, 2 ih + 1
 #pragma unroll
-              for (int pp = 0; pp < 16; ++pp) {
-                const int i = pp >> 2, r = pp & 3;
-                const int n = sl * 64 + 16 * i + g + 8 * (r & 1);
-                const int k = kt * 32 + 16 * j + 2 * q + 8 * (r >> 1);
-                const uint32_t off = (uint32_t)n * 128u + (uint32_t)(((k >> 3) ^ (n & 7)) << 4) + (uint32_t)((k & 7) * 2);
-                *reinterpret_cast<uint32_t*>(A + off) = wv[pp];
+                for (int u = 0; u < 4; ++u) {  // unit (kt, j) = 16-k block u of the stage
+                  const int kt = u >> 1, j = u & 1;
+                  const uint8_t* tile = sP + ((nm * 2 + sl) * 2 + kt) * kTileBytes;
+                  const uint2 wa = *reinterpret_cast<const uint2*>(tile + kPlaneAOff + lane * 16 + 8 * j);
+                  const uint32_t wb = *reinterpret_cast<const uint32_t*>(tile + kPlaneBOff + lane * 8 + 4 * j);
+                  const uint4 mm = *reinterpret_cast<const uint4*>(tile + kMetaOff + q * 32 + 16 * j);
+                  const uint32_t S2[2] = {mm.x, mm.z}, O2[2] = {mm.y, mm.w};
+                  uint32_t o[8];
+                  if (ih == 0)
+                    half_unit_dequant<0>(wa.x, wa.y, wb, S2, O2, dq, o);
+                  else
+                    half_unit_dequant<1>(wa.x, wa.y, wb, S2, O2, dq, o);
+                  // o[4 il + r]: row g + 8 (r & 1), k pair q + 4 (r >> 1)
+                  v0[4 * u + 0] = o[0];
+                  v0[4 * u + 1] = o[2];
+                  v0[4 * u + 2] = o[1];
+                  v0[4 * u + 3] = o[3];
+                  v1[4 * u + 0] = o[4];
+                  v1[4 * u + 1] = o[6];
+                  v1[4 * u + 2] = o[5];
+                  v1[4 * u + 3] = o[7];
+                }
+                tmem_st16x256_x4(a_col + lane_q + (uint32_t)(nm * 32), v0);
+                tmem_st16x256_x4(a_col + lane_q + (16u << 16) + (uint32_t)(nm * 32), v1);
               }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&p_empty[ps]);
-            if (!(a.flags & 16)) fence_proxy_async();  // generic smem writes -> tensor-core (async proxy) reads
+          } else {
+            int mat, ch, vpart, tpart;
+            lorc_stage(P, st - ks, mat, ch, vpart, tpart);
+            const int row = 32 * Q + lane;
+#pragma unroll 1
+            for (int ng = 0; ng < NG; ++ng) {
+              const uint8_t* img =
+                  P.vimg[mat] + (((int64_t)(NG * nt + ng) * P.rchunks[mat] + ch) * 2 + vpart) * kPfImg + row * 128;
+              uint32_t v[32];
+#pragma unroll
+              for (int c = 0; c < 8; ++c) {
+                const uint4 x = __ldg(reinterpret_cast<const uint4*>(img + ((c ^ (row & 7)) << 4)));
+                v[4 * c] = x.x;
+                v[4 * c + 1] = x.y;
+                v[4 * c + 2] = x.z;
+                v[4 * c + 3] = x.w;
+              }
+              tmem_st32x32_x32(a_col + lane_q + (uint32_t)((ng * NMAT + mat) * 32), v);
+            }
           }
+          tmem_st_wait();
+          tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&a_full[as]);
-
+          if (gw == 0 && lane == 0) pf_trace(gs, 3);
         }
         if (st < ks && ++ps == PS) {
           ps = 0;
@@ -451,54 +583,21 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
       }
     }
     if (dw == 0 && lane == 0) pf_dbg(3);
-  } else if (warp == kPfMmaWarp) {
-    // ======================= MMA issuer =======================
+  } else if (warp == kPfWaitWarp) {
+    // ======================= ring waiter =======================
     if (lane == 0) {
-      int as = 0, bs = 0;
+      int as = 0, bs = 0, gs = 0;
       uint32_t aph = 0, bph = 0;
-      int acc = 0;
-      uint32_t acc_phase = 0;
       for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
         int p, nt, tt;
         pf_item<NG>(a, item, p, nt, tt);
-        const PfProblem P = a.problems[p];  // by value: fields live in registers
-        const int ks = P.k / kPfK, total = item_stages(P);
-        const uint32_t idesc = pf_idesc(P.ntok);
-        ring_wait(&acc_empty[acc], acc_phase ^ 1);
-        tc_fence_after();
-        const uint32_t d0 = tmem + (uint32_t)(acc * NG * NMAT * kPfN);
-        for (int st = 0; st < total; ++st) {
+        const int total = item_stages(a.problems[p]);
+        for (int st = 0; st < total; ++st, ++gs) {
           ring_wait(&a_full[as], aph);
-
+          pf_trace(gs, 4);
           ring_wait(&b_full[bs], bph);
-          tc_fence_after();
-          const uint32_t aA = smem_u32(smem + CF::kOffA + as * CF::kStageA);
-          const uint32_t aB = smem_u32(smem + CF::kOffB + bs * bslot);
-          int mat0 = 0, mat1 = NMAT;
-          if (st >= ks) {
-            int mat, ch, vpart, tpart;
-            lorc_stage(P, st - ks, mat, ch, vpart, tpart);
-            mat0 = mat;
-            mat1 = mat + 1;
-          }
-          for (int ng = 0; ng < NG; ++ng)
-            for (int mat = mat0; mat < mat1; ++mat) {
-#pragma unroll
-              for (int k16 = 0; k16 < kPfK / 16; ++k16) {
-                const uint64_t da = pf_desc_sw128(aA + (ng * NMAT + mat) * kPfImg + k16 * 32);
-                const uint64_t db = pf_desc_sw128(aB + k16 * 32);
-                if (!(a.flags & 2))
-                  pf_mma(d0 + (uint32_t)((ng * NMAT + mat) * kPfN), da, db, idesc, (st > 0 || k16 > 0) ? 1u : 0u);
-              }
-            }
-          pf_commit(&a_empty[as]);
-          pf_commit(&b_empty[bs]);
-          if ((a.flags & 32) && item == (int)blockIdx.x && st < 64) {  // debug: commit latency
-            pf_trace(st, 1);
-            ring_wait(&a_empty[as], aph);
-            pf_trace(st, 3);
-          }
-          if (item == (int)blockIdx.x) pf_trace(st, 2);
+          pf_trace(gs, 5);
+          st_release_cta_shared(stages_ready, (uint32_t)(gs + 1));
           if (++as == AS) {
             as = 0;
             aph ^= 1;
@@ -508,13 +607,99 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
             bph ^= 1;
           }
         }
-        pf_commit(&acc_full[acc]);
-        if (++acc == 2) {
+      }
+    }
+  } else if (warp == kPfMmaWarp || warp == kPfMmaWarp2) {
+    // ======================= MMA issuers =======================
+    // Two threads issue (a single thread issues at most one tcgen05.mma per
+    // ~55 cycles, tools/micro/mma_rate.cu, while a 128 x 64 x 16 MMA executes
+    // in 32): issuer i owns accumulator i -- matrix i (w1 / w3), n-tile i, or
+    // for one-accumulator kernels with ntok <= 64 the k16 steps i, i + 2 of
+    // every stage.  Both release every A / B slot (commit, or a plain arrive
+    // when the stage has no MMA of theirs) and every accumulator.
+    const int issuer = warp == kPfMmaWarp ? 0 : 1;
+    {  // the whole warp (converged), one elected lane issues
+      const uint64_t dB0 = pf_desc_sw128(smem_u32(smem + CF::kOffB));
+      const bool mma_on = !(a.flags & 2);
+      int as = 0, bs = 0;
+      int acc = 0, gs = 0;
+      uint32_t acc_phase = 0;
+      for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
+        int p, nt, tt;
+        pf_item<NG>(a, item, p, nt, tt);
+        const PfProblem P = a.problems[p];  // by value: fields live in registers
+        const int ks = P.k / kPfK, total = item_stages(P);
+        const uint32_t idesc = pf_idesc(P.ntok);
+        ring_wait(&acc_empty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d0 = tmem + (uint32_t)(acc * acc_cols + issuer * mstride);  // this issuer's accumulator
+        const bool idle = NG * NMAT == 1 && !ksplit && issuer == 1;
+        for (int st = 0; st < total; ++st, ++gs) {
+          PF_PROF_T(c0);
+          // an mbarrier wait costs a thread that issues MMAs ~200 cycles even when
+          // the phase completed long ago (tools/micro/mma_rate.cu); the wait warp
+          // does the ring waits and publishes a stage counter instead
+          while (ld_acquire_cta_shared(stages_ready) <= (uint32_t)gs) {
+          }
+          PF_PROF_T(c1);
+          PF_PROF_T(c2);
+          tc_fence_after();
+          // operand addresses: TMEM A slot, B descriptor of the slot (the 16-B
+          // address field advances by 2 per 16-k step); everything unrolled
+          const uint32_t aA = tmem + (uint32_t)(CF::kACol0 + as * CF::kStageCols);
+          const uint64_t dB = dB0 + (uint64_t)((uint32_t)(bs * bslot) >> 4);
+          bool issued = false;
+          if (!idle && mma_on) {
+            int nm = issuer;  // A block (ng * NMAT + mat) this issuer multiplies
+            uint32_t acc0 = 1u;
+            if (st < ks) {
+              acc0 = st > 0 ? 1u : 0u;
+            } else {
+              int mat, ch, vpart, tpart;
+              lorc_stage(P, st - ks, mat, ch, vpart, tpart);
+              if (NMAT == 2) nm = mat == issuer ? mat : -1;  // the other matrix's issuer sits out
+            }
+            if (NG * NMAT == 1) nm = 0;
+            if (nm >= 0) {
+              const uint32_t aN = aA + (uint32_t)(nm * 32);
+              if (NG * NMAT == 1 && ksplit) {  // k16 steps issuer, issuer + 2
+                pf_mma_ts_w(d0, aN + (uint32_t)(issuer * 8), dB + 2 * issuer, idesc, acc0);
+                pf_mma_ts_w(d0, aN + (uint32_t)(issuer * 8 + 16), dB + 2 * issuer + 4, idesc, 1u);
+              } else {
+#pragma unroll
+                for (int k16 = 0; k16 < kPfK / 16; ++k16)
+                  pf_mma_ts_w(d0, aN + (uint32_t)(k16 * 8), dB + 2 * k16, idesc, k16 > 0 ? 1u : acc0);
+              }
+              issued = true;
+            }
+          }
+          PF_PROF_T(c3);
+          if (issued) {
+            pf_commit_w(&a_empty[as]);
+            pf_commit_w(&b_empty[bs]);
+          } else {
+            mbar_arrive_w(&a_empty[as]);
+            mbar_arrive_w(&b_empty[bs]);
+          }
+          PF_PROF_T(c4);
+          if (issuer == 0 && lane == 0) pf_trace(gs, 6);
+          PF_PROF_ACC(c0, c1, c2, c3, c4);
+          if (++as == AS) as = 0;
+          if (++bs == BS) bs = 0;
+        }
+        if (idle || !mma_on)
+          mbar_arrive_w(&acc_full[acc]);
+        else
+          pf_commit_w(&acc_full[acc]);
+        if (++acc == nacc) {
           acc = 0;
           acc_phase ^= 1;
         }
       }
-      pf_dbg(4);
+      if (issuer == 0 && lane == 0) {
+        PF_PROF_OUT();
+        pf_dbg(4);
+      }
     }
   } else {
     // ======================= epilogue warps 0..3 =======================
@@ -537,23 +722,24 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
       const int ntok = P.ntok;
 #pragma unroll 1
       for (int ng = 0; ng < NG; ++ng) {
-      const uint32_t tbase = tmem + ((uint32_t)(32 * ew) << 16) + (uint32_t)((acc * NG + ng) * NMAT * kPfN);
+      const uint32_t tbase = tmem + ((uint32_t)(32 * ew) << 16) + (uint32_t)(acc * acc_cols + ng * NMAT * mstride);
       const int col0 = (NG * nt + ng) * kPfM + 32 * ew + 8 * (lane & 3);  // this lane's 8 output columns
 #pragma unroll 1
-      for (int c0 = 0; c0 < ntok; c0 += 32) {
-        uint32_t v0[32], v1[32];
-        tmem_ld32(tbase + (uint32_t)c0, v0);
-        if (NMAT == 2) tmem_ld32(tbase + (uint32_t)(kPfN + c0), v1);
+      for (int c0 = 0; c0 < ntok; c0 += 16) {  // 16 tokens per pass (register budget of 640+ threads)
+        uint32_t v0[16], v1[16];
+        tmem_ld16(tbase + (uint32_t)c0, v0);
+        if (NMAT == 2 || ksplit) tmem_ld16(tbase + (uint32_t)(mstride + c0), v1);
         tmem_ld_wait();
 #pragma unroll
-        for (int c = 0; c < 32; ++c) {
+        for (int c = 0; c < 16; ++c) {
           float x = __uint_as_float(v0[c]);
+          if (NMAT == 1 && ksplit) x += __uint_as_float(v1[c]);  // the two k halves
           if (kind == 1) x = pf_silu(x) * (NMAT == 2 ? __uint_as_float(v1[c]) : 0.0f);
           stg[c * 33 + lane] = x;
         }
         __syncwarp();
 #pragma unroll
-        for (int it = 0; it < 4; ++it) {
+        for (int it = 0; it < 2; ++it) {
           const int tr = 8 * it + (lane >> 2);  // token row within the chunk
           const int row = tt * ntok + c0 + tr;
           if (row < rows && c0 + tr < ntok) {
@@ -582,7 +768,7 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[acc]);
-      if (++acc == 2) {
+      if (++acc == nacc) {
         acc = 0;
         acc_phase ^= 1;
       }
@@ -599,29 +785,45 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
 
 // Activation images: rows (binary16 or f32 source, optional row gather) ->
 // [tok_tiles][k/64][ntok rows x 128 B, SW128 K-major], zero rows past `rows`.
+// Within every 16-k block the k pairs are stored in the order 0 4 1 5 2 6 3 7
+// -- the column order in which pf_gemm_kernel's dequant warps write W^T into
+// tensor memory (thread q of a quad owns pairs q and q + 4 of the mma
+// fragment and stores them to adjacent columns 2q, 2q + 1).
+// One 16-k block (8 pairs w[0..7]) of row src_row at column col.
+__device__ __forceinline__ void pf_load_block16(const void* x, int32_t x_dtype, int64_t src_row, int64_t ldx,
+                                                int64_t col, uint32_t (&w)[8]) {
+  if (x_dtype == 0) {
+    const float4* s = reinterpret_cast<const float4*>(static_cast<const float*>(x) + src_row * ldx + col);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float4 f = s[u];
+      w[2 * u] = h2_as_u32(__floats2half2_rn(f.x, f.y));
+      w[2 * u + 1] = h2_as_u32(__floats2half2_rn(f.z, f.w));
+    }
+  } else {
+    const uint4* s = reinterpret_cast<const uint4*>(static_cast<const __half*>(x) + src_row * ldx + col);
+    const uint4 p0 = s[0], p1 = s[1];
+    w[0] = p0.x; w[1] = p0.y; w[2] = p0.z; w[3] = p0.w;
+    w[4] = p1.x; w[5] = p1.y; w[6] = p1.z; w[7] = p1.w;
+  }
+}
+// Stores block b (0..3) of image row r in the permuted order.
+__device__ __forceinline__ void pf_store_block16(uint8_t* dst, int r, int b, const uint32_t (&w)[8]) {
+  *reinterpret_cast<uint4*>(dst + r * 128 + (((2 * b) ^ (r & 7)) << 4)) = make_uint4(w[0], w[4], w[1], w[5]);
+  *reinterpret_cast<uint4*>(dst + r * 128 + (((2 * b + 1) ^ (r & 7)) << 4)) = make_uint4(w[2], w[6], w[3], w[7]);
+}
 __global__ void pf_image_kernel(const void* __restrict__ x, int32_t x_dtype, int64_t ldx,
                                 const int32_t* __restrict__ row_ids, int32_t rows, int32_t k, int32_t ntok,
                                 uint8_t* __restrict__ img) {
   const int ks = k / kPfK;
   const int tile = blockIdx.x / ks, st = blockIdx.x % ks;
   uint8_t* dst = img + (int64_t)blockIdx.x * ntok * 128;
-  for (int c = threadIdx.x; c < ntok * 8; c += blockDim.x) {  // 16-B chunks
-    const int r = c >> 3, ch = c & 7;
+  for (int c = threadIdx.x; c < ntok * 4; c += blockDim.x) {  // 16-k blocks
+    const int r = c >> 2, b = c & 3;
     const int row = tile * ntok + r;
-    uint4 v = make_uint4(0u, 0u, 0u, 0u);
-    if (row < rows) {
-      const int64_t src_row = row_ids ? row_ids[row] : row;
-      const int64_t col = (int64_t)st * kPfK + ch * 8;
-      if (x_dtype == 0) {
-        const float4* s = reinterpret_cast<const float4*>(static_cast<const float*>(x) + src_row * ldx + col);
-        const float4 p0 = s[0], p1 = s[1];
-        v = make_uint4(h2_as_u32(__floats2half2_rn(p0.x, p0.y)), h2_as_u32(__floats2half2_rn(p0.z, p0.w)),
-                       h2_as_u32(__floats2half2_rn(p1.x, p1.y)), h2_as_u32(__floats2half2_rn(p1.z, p1.w)));
-      } else {
-        v = *reinterpret_cast<const uint4*>(static_cast<const __half*>(x) + src_row * ldx + col);
-      }
-    }
-    *reinterpret_cast<uint4*>(dst + r * 128 + ((ch ^ (r & 7)) << 4)) = v;
+    uint32_t w[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+    if (row < rows) pf_load_block16(x, x_dtype, row_ids ? row_ids[row] : row, ldx, (int64_t)st * kPfK + b * 16, w);
+    pf_store_block16(dst, r, b, w);
   }
   pdl_launch_dependents();
 }
@@ -821,30 +1023,19 @@ __device__ __forceinline__ void pf_img_t_unit(const ImgJob* __restrict__ jobs, i
   const int tile = rel / ks, st = rel % ks;
   const int ntok = J.ntok, tid = threadIdx.x;
   uint8_t* dst = J.img + (int64_t)rel * ntok * 128;
-  for (int c = tid; c < ntok * 8; c += blockDim.x) {  // 16-B chunks
-    const int r = c >> 3, ch = c & 7;
+  for (int c = tid; c < ntok * 4; c += blockDim.x) {  // 16-k blocks
+    const int r = c >> 2, b = c & 3;
     const int row = tile * ntok + r;
-    uint4 v = make_uint4(0u, 0u, 0u, 0u);
-    if (row < J.rows) {
-      const int64_t src_row = J.row_ids ? J.row_ids[row] : row;
-      const int64_t col = (int64_t)st * kPfK + ch * 8;
-      if (J.x_dtype == 0) {
-        const float4* sp = reinterpret_cast<const float4*>(static_cast<const float*>(J.x) + src_row * J.ldx + col);
-        const float4 p0 = sp[0], p1 = sp[1];
-        v = make_uint4(h2_as_u32(__floats2half2_rn(p0.x, p0.y)), h2_as_u32(__floats2half2_rn(p0.z, p0.w)),
-                       h2_as_u32(__floats2half2_rn(p1.x, p1.y)), h2_as_u32(__floats2half2_rn(p1.z, p1.w)));
-      } else {
-        v = *reinterpret_cast<const uint4*>(static_cast<const __half*>(J.x) + src_row * J.ldx + col);
-      }
-    }
-    *reinterpret_cast<uint4*>(dst + r * 128 + ((ch ^ (r & 7)) << 4)) = v;
+    uint32_t w[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+    if (row < J.rows)
+      pf_load_block16(J.x, J.x_dtype, J.row_ids ? J.row_ids[row] : row, J.ldx, (int64_t)st * kPfK + b * 16, w);
+    pf_store_block16(dst, r, b, w);
     if (J.n_t > 0) {
-      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < 8; ++u) {
         const float2 f = __half22float2(u32_as_h2(w[u]));
-        sx[r * 65 + ch * 8 + 2 * u] = f.x;
-        sx[r * 65 + ch * 8 + 2 * u + 1] = f.y;
+        sx[r * 65 + b * 16 + 2 * u] = f.x;
+        sx[r * 65 + b * 16 + 2 * u + 1] = f.y;
       }
     }
   }

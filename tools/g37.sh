@@ -1,0 +1,4 @@
+cd "${GRAFT_REPO_ROOT:-/root/repo}"; O=gpurun_out; mkdir -p $O
+for f in 0 1; do MILO_B200_LIB_VARIANT=prof timeout 300 python tools/pf_stage_trace.py --batch 256 --flags $f > $O/pr256_$f.txt 2>&1; done
+timeout 300 python tools/time_prefill.py 256 2048 > $O/tp.txt 2>&1
+timeout 300 python tools/timeline.py --batch 256 > $O/tl256.txt 2>&1
