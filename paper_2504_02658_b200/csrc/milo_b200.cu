@@ -1189,8 +1189,13 @@ cudaError_t launch_t_batch(const std::vector<TProb>& v, int units, uint8_t* tabl
   if (v.empty()) return cudaSuccess;
   cudaError_t e = h2d_async(table, v.data(), v.size() * sizeof(TProb), stream);
   if (e != cudaSuccess) return e;
-  e = launch(pf_t_kernel, dim3(units), dim3(256), 0, stream, false, (const TProb*)table, (int)v.size(),
-             (const int32_t*)nullptr);
+  bool coded = false, real = false;
+  for (const TProb& t : v) (t.ucodes ? coded : real) = true;
+  if (coded) e = launch(pf_t_kernel<0>, dim3(units), dim3(256), 0, stream, false, (const TProb*)table, (int)v.size(),
+                        (const int32_t*)nullptr);
+  if (e == cudaSuccess && real)
+    e = launch(pf_t_kernel<1>, dim3(units), dim3(256), 0, stream, false, (const TProb*)table, (int)v.size(),
+               (const int32_t*)nullptr);
   if (e != cudaSuccess) return e;
   return launch(pf_t_images_kernel, dim3(256, (unsigned)v.size()), dim3(256), 0, stream, false, (const TProb*)table,
                 (int)v.size(), (const int32_t*)nullptr);
@@ -1545,6 +1550,7 @@ struct milo_moe {
   std::mutex stage_mu;  // the staging is per handle; handles may be shared across threads
   __half* gate = nullptr;  // optional router gate, E x d binary16 (milo_moe_set_gate)
   PfExpertStatic* pf_static = nullptr;  // device: per expert, what moe_plan_kernel needs
+  int t_kinds[2] = {0, 0};               // per phase: bit 0 symm-INT3 factors, bit 1 real factors
   int32_t rch_max[3] = {0, 0, 0};       // largest 64-rank chunk count per matrix
   bool hd_ok = true;                    // hdec_kernel eligible (int3 / no compensators, 64-multiple shapes)
   HdExp* hd_exp = nullptr;              // device: hdec_kernel's per-expert static view
@@ -1711,6 +1717,7 @@ extern "C" milo_status milo_moe_create(const milo_expert_desc* experts, int32_t 
           M.gpr = c->gpr;
           M.rch = c->rch;
           moe->rch_max[j] = std::max(moe->rch_max[j], c->rch);
+          moe->t_kinds[j == 2 ? 1 : 0] |= c->ucodes ? 1 : 2;
         }
       }
     if (err == cudaSuccess) err = cudaMalloc(&moe->pf_static, ps.size() * sizeof(PfExpertStatic));
@@ -2242,8 +2249,12 @@ milo_status moe_prefill_dev(milo_moe* moe, const void* x, int64_t m, int32_t x_d
     // activation images (+ gathered rows) and LoRC t = x U -> hi / lo images
     CUDA_TRY(launch(pf_img_t_kernel, dim3((unsigned)(sms * 8)), dim3(256), kImgTSmem, stream, false,
                     (const ImgJob*)pa.jobs[ph], 0, cnt));
-    CUDA_TRY(launch(pf_t_kernel, dim3((unsigned)(sms * 8)), dim3(256), 0, stream, false, (const TProb*)pa.tps[ph], 0,
-                    cnt + 2));
+    if (moe->t_kinds[ph] & 1)
+      CUDA_TRY(launch(pf_t_kernel<0>, dim3((unsigned)(sms * 8)), dim3(256), 0, stream, false, (const TProb*)pa.tps[ph],
+                      0, cnt + 2));
+    if (moe->t_kinds[ph] & 2)
+      CUDA_TRY(launch(pf_t_kernel<1>, dim3((unsigned)(sms * 8)), dim3(256), 0, stream, false, (const TProb*)pa.tps[ph],
+                      0, cnt + 2));
     CUDA_TRY(launch(pf_t_images_kernel, dim3(64, (unsigned)std::max<int64_t>(1, G * (ph == 0 ? 2 : 1))), dim3(256),
                     0, stream, false, (const TProb*)pa.tps[ph], 0, cnt + 2));
     // the grouped tcgen05 GEMM (persistent grid; items from the plan)

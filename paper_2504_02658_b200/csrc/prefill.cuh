@@ -962,20 +962,203 @@ __device__ __forceinline__ void pf_t_unit(const TProb* __restrict__ probs, int n
   }
 }
 
+// The same unit for symm-INT3 factors on the tensor cores (mma.sync
+// m16n8k16, fp32 accumulation): U[k][j] = s'[k] (c[k][j] - 4) with
+// s' = scale x 2/7 per (k, 64-rank group) (lowrank.cpp:122-134), so
+//   t = half(x) U = (half(x) (.) s') C,   C = c - 4 exact in binary16,
+// and the fp32 row-scaled activations p = half(x) s' enter as binary16 hi + lo
+// halves (p - hi(p) is exact in fp32; hi + lo carries 22 of its 24 bits).  The
+// products with C are exact and accumulate in fp32 -- the reference's fp32
+// product up to summation order and the 2^-22 split residual.
+struct TTcSmem {
+  __half xh[kTRows][72];  // p hi, rows of the tile x 64 k (+8 pad: conflict-free fragment loads)
+  __half xl[kTRows][72];  // p lo
+  __half ct[64][72];      // C^T: 64 ranks x 64 k
+};
+__device__ __forceinline__ void t_tc_load(const TProb& P, int kb, int ch, int tid, const int64_t xrow, float (&xv)[8],
+                                          float (&sv)[8], uint4& cv) {
+  const int k8 = (tid & 7) * 8;  // x: row tid / 8, k k8 .. k8 + 7
+  if (xrow >= 0) {
+    if (P.x_dtype == 0) {
+      const float4* xp = reinterpret_cast<const float4*>(static_cast<const float*>(P.x) + xrow + kb + k8);
+      const float4 a = xp[0], b = xp[1];
+      const float f[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int i = 0; i < 8; ++i) xv[i] = __half2float(__float2half_rn(f[i]));
+    } else {
+      const uint4 h = *reinterpret_cast<const uint4*>(static_cast<const __half*>(P.x) + xrow + kb + k8);
+      const uint32_t w[4] = {h.x, h.y, h.z, h.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 f = __half22float2(u32_as_h2(w[i]));
+        xv[2 * i] = f.x;
+        xv[2 * i + 1] = f.y;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) xv[i] = 0.0f;
+  }
+  if (P.gpr == 1) {
+    const float4* sp = reinterpret_cast<const float4*>(P.uscales + kb + k8);
+    const float4 a = __ldg(sp), b = __ldg(sp + 1);
+    sv[0] = a.x; sv[1] = a.y; sv[2] = a.z; sv[3] = a.w;
+    sv[4] = b.x; sv[5] = b.y; sv[6] = b.z; sv[7] = b.w;
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) sv[i] = P.uscales[(int64_t)(kb + k8 + i) * P.gpr + ch];
+  }
+  if (P.rchunks == 1) {
+    // the block's codes are one contiguous run of 64 x rank bytes (16-B aligned:
+    // 64 rank is): thread tid loads bytes 16 tid .. 16 tid + 15 of it
+    const int nb = 64 * P.rank;
+    cv = 16 * tid < nb ? __ldg(reinterpret_cast<const uint4*>(P.ucodes + (int64_t)kb * P.rank + 16 * tid))
+                       : make_uint4(0u, 0u, 0u, 0u);
+  } else {
+    // codes: k row tid / 4, ranks ch * 64 + 16 (tid % 4) .. + 15 (past the rank: code 4 -> 0)
+    const int kk = tid >> 2, j0 = ch * 64 + (tid & 3) * 16;
+    const uint8_t* cp = P.ucodes + (int64_t)(kb + kk) * P.rank + j0;
+    uint32_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      uint32_t v = 0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int j = j0 + 4 * i + b;
+        const uint32_t c = j < P.rank ? cp[4 * i + b] : 4u;
+        v |= c << (8 * b);
+      }
+      w[i] = v;
+    }
+    cv = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+__device__ __forceinline__ void pf_t_tc_unit(const TProb& P, int u, TTcSmem& sm) {
+  const int tiles = (P.rows + kTRows - 1) / kTRows;
+  const int ksi = u % P.ks;
+  u /= P.ks;
+  const int ch = u % P.rchunks, tile = u / P.rchunks;
+  if (tile >= tiles) return;
+  const int kper = ((P.k / 64 + P.ks - 1) / P.ks) * 64;
+  const int k0 = ksi * kper, k1 = min(P.k, k0 + kper);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, q = lane & 3;
+  const int slab = warp & 1, rq = warp >> 1;  // rows 16 slab .., ranks 16 rq ..
+  const int lrow = tid >> 3, row = tile * kTRows + lrow;
+  const int64_t xrow = row < P.rows ? (P.row_ids ? (int64_t)P.row_ids[row] : (int64_t)row) * P.ldx : int64_t(-1);
+  float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+  float xv[8], sv[8];
+  uint4 cv;
+  if (P.rchunks == 1)  // ranks past the rank stay 0 (the contiguous-run path writes only j < rank)
+    for (int e = tid; e < (64 - P.rank) * 72; e += blockDim.x) sm.ct[P.rank + e / 72][e % 72] = __float2half_rn(0.0f);
+  if (k0 < k1) t_tc_load(P, k0, ch, tid, xrow, xv, sv, cv);
+  for (int kb = k0; kb < k1; kb += 64) {
+    {  // registers -> shared: p = x s' as hi / lo; C^T
+      uint32_t hv[4], lv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float p0 = xv[2 * i] * (sv[2 * i] * (2.0f / 7.0f)), p1 = xv[2 * i + 1] * (sv[2 * i + 1] * (2.0f / 7.0f));
+        const __half h0 = __float2half_rn(p0), h1 = __float2half_rn(p1);
+        hv[i] = h2_as_u32(__halves2half2(h0, h1));
+        lv[i] = h2_as_u32(__floats2half2_rn(p0 - __half2float(h0), p1 - __half2float(h1)));
+      }
+      const int k8 = (tid & 7) * 8;
+      *reinterpret_cast<uint4*>(&sm.xh[lrow][k8]) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
+      *reinterpret_cast<uint4*>(&sm.xl[lrow][k8]) = make_uint4(lv[0], lv[1], lv[2], lv[3]);
+      const uint32_t w[4] = {cv.x, cv.y, cv.z, cv.w};
+      if (P.rchunks == 1) {  // byte e = 16 tid + i of the run: k row e / rank, rank e % rank
+        const int e0 = 16 * tid;
+        int kk = e0 / P.rank, j = e0 - kk * P.rank;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          if (kk < 64) sm.ct[j][kk] = __float2half_rn((float)((w[i >> 2] >> (8 * (i & 3))) & 0xFFu) - 4.0f);
+          if (++j == P.rank) {
+            j = 0;
+            ++kk;
+          }
+        }
+      } else {
+        const int kk = tid >> 2, jl = (tid & 3) * 16;
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          sm.ct[jl + i][kk] = __float2half_rn((float)((w[i >> 2] >> (8 * (i & 3))) & 0xFFu) - 4.0f);
+      }
+    }
+    __syncthreads();
+    if (kb + 64 < k1) t_tc_load(P, kb + 64, ch, tid, xrow, xv, sv, cv);  // next block in flight
+#pragma unroll
+    for (int k16 = 0; k16 < 4; ++k16) {
+      const int kc = 16 * k16 + 2 * q, r0 = 16 * slab + g;
+      uint32_t ah[4], al[4];
+      ah[0] = *reinterpret_cast<const uint32_t*>(&sm.xh[r0][kc]);
+      ah[1] = *reinterpret_cast<const uint32_t*>(&sm.xh[r0 + 8][kc]);
+      ah[2] = *reinterpret_cast<const uint32_t*>(&sm.xh[r0][kc + 8]);
+      ah[3] = *reinterpret_cast<const uint32_t*>(&sm.xh[r0 + 8][kc + 8]);
+      al[0] = *reinterpret_cast<const uint32_t*>(&sm.xl[r0][kc]);
+      al[1] = *reinterpret_cast<const uint32_t*>(&sm.xl[r0 + 8][kc]);
+      al[2] = *reinterpret_cast<const uint32_t*>(&sm.xl[r0][kc + 8]);
+      al[3] = *reinterpret_cast<const uint32_t*>(&sm.xl[r0 + 8][kc + 8]);
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        const int n = 16 * rq + 8 * nt + g;
+        const uint32_t b0 = *reinterpret_cast<const uint32_t*>(&sm.ct[n][kc]);
+        const uint32_t b1 = *reinterpret_cast<const uint32_t*>(&sm.ct[n][kc + 8]);
+        mma_16816(acc[nt], ah, b0, b1);
+        mma_16816(acc[nt], al, b0, b1);
+      }
+    }
+    __syncthreads();
+  }
+  const int r64 = P.rchunks * 64;
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt) {
+    const int col = ch * 64 + 16 * rq + 8 * nt + 2 * q;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = tile * kTRows + 16 * slab + g + 8 * h;
+      if (r < P.rows)
+        *reinterpret_cast<float2*>(&P.part[((int64_t)ksi * P.rows + r) * r64 + col]) =
+            make_float2(acc[nt][2 * h], acc[nt][2 * h + 1]);
+    }
+  }
+}
+
 // dev_counts (nullable): {n_probs, units} from moe_plan_kernel; the CTAs then
-// loop over the planned units (grid-stride), else CTA = unit.
-__global__ void __launch_bounds__(256) pf_t_kernel(const TProb* __restrict__ probs, int n_probs,
-                                                  const int32_t* __restrict__ dev_counts) {
-  __shared__ __align__(16) float sx[kTRows][68];  // rows 16 B aligned: float4 reads of 4 k
-  __shared__ float su[64][65];
+// loop over the planned units (grid-stride), else CTA = unit.  Symm-INT3
+// factors take the tensor-core unit, real-valued ones the CUDA-core unit.
+struct TCoreSmem {  // pf_t_unit's operands
+  float sx[kTRows][68];  // rows 16 B aligned: float4 reads of 4 k
+  float su[64][65];
+};
+// KIND 0: the units of symm-INT3 factors (tensor cores); KIND 1: real-valued
+// factors (CUDA cores).  Launch both when a table mixes them.
+template <int KIND>
+__device__ __forceinline__ void pf_t_any_unit(const TProb* __restrict__ probs, int n_probs, int unit, uint8_t* sm) {
+  int lo = 0, hi = n_probs - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (probs[mid].unit0 <= unit) lo = mid; else hi = mid - 1;
+  }
+  if ((probs[lo].ucodes != nullptr) != (KIND == 0)) return;
+  if (KIND == 0) {
+    pf_t_tc_unit(probs[lo], unit - probs[lo].unit0, *reinterpret_cast<TTcSmem*>(sm));
+  } else {
+    TCoreSmem& c = *reinterpret_cast<TCoreSmem*>(sm);
+    pf_t_unit(probs, n_probs, unit, c.sx, c.su);
+  }
+}
+template <int KIND>
+__global__ void __launch_bounds__(256, KIND == 0 ? 4 : 1) pf_t_kernel(const TProb* __restrict__ probs, int n_probs,
+                                                                    const int32_t* __restrict__ dev_counts) {
+  constexpr int kSm = KIND == 0 ? sizeof(TTcSmem) : sizeof(TCoreSmem);
+  __shared__ __align__(16) uint8_t sm[kSm];
   if (dev_counts == nullptr) {
-    pf_t_unit(probs, n_probs, blockIdx.x, sx, su);
+    pf_t_any_unit<KIND>(probs, n_probs, blockIdx.x, sm);
     return;
   }
   n_probs = dev_counts[0];
   const int units = dev_counts[1];
   for (int u = blockIdx.x; u < units; u += gridDim.x) {
-    pf_t_unit(probs, n_probs, u, sx, su);
+    pf_t_any_unit<KIND>(probs, n_probs, u, sm);
     __syncthreads();
   }
 }
