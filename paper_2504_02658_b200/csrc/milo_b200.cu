@@ -1327,7 +1327,8 @@ extern "C" milo_status milo_gemm_w3a16(const milo_weight* w, const milo_comp* co
   const int m_pad = 8 * nt;
   const int64_t k = (int64_t)w->rows, n = (int64_t)w->cols;
   const bool pf_comp_ok = !(comp && comp->rank > 0) || comp->vimg != nullptr;
-  if (!legacy_path() && m >= prefill_min_rows() && n % kPfM == 0 && pf_comp_ok) {
+  // (the prefill kernel's producers move 128 k per ring slot)
+  if (!legacy_path() && m >= prefill_min_rows() && n % kPfM == 0 && k % (2 * kPfK) == 0 && pf_comp_ok) {
     // tcgen05 path: activation images (binary16, SW128) then the grouped GEMM
     const int ntok = pf_ntok(m);
     const int64_t tiles = (m + ntok - 1) / ntok, ks = k / kPfK;
@@ -1603,7 +1604,7 @@ extern "C" milo_status milo_moe_create(const milo_expert_desc* experts, int32_t 
     moe->hc.push_back({c[0], c[1], c[2]});
     for (int j = 0; j < 3; ++j) {
       const bool comp_ok = !(c[j] && c[j]->rank > 0) || c[j]->vimg != nullptr;
-      if (w[j]->cols % kPfM != 0 || w[j]->rows % kPfK != 0 || !comp_ok) moe->prefill_ok = false;
+      if (w[j]->cols % kPfM != 0 || w[j]->rows % (2 * kPfK) != 0 || !comp_ok) moe->prefill_ok = false;
     }
     for (int j = 0; j < 3; ++j) {
       const bool has_c = c[j] && c[j]->rank > 0;

@@ -33,13 +33,19 @@ namespace milo_dev {
 #define PF_NG2_GROUPS 3
 #endif
 #ifndef PF_PS2
-#define PF_PS2 10  // packed ring stages of the two-matrix / two-n-tile variants
+#define PF_PS2 5  // packed ring slots (128 k each) of the two-matrix / two-n-tile variants
 #endif
-#ifndef PF_PROF_MMA
-#define PF_PROF_MMA 0
+#ifndef PF_PROF
+#define PF_PROF 0  // experiments: per-role cycle split of CTA 0 (tools/pf_stage_trace.py)
+#endif
+#ifndef PF_ISSUERS
+#define PF_ISSUERS 2  // MMA-issuing threads (experiments: 1)
+#endif
+#ifndef PF_MIN_AS
+#define PF_MIN_AS 6
 #endif
 #ifndef PF_B_KB
-#define PF_B_KB 96  // activation / t image ring (KB)
+#define PF_B_KB 128  // activation / t image ring (KB)
 #endif
 constexpr int kPfM = 128;              // output columns per tile (UMMA M)
 constexpr int kPfN = 128;              // tokens per tile (UMMA N, TMEM columns)
@@ -80,21 +86,23 @@ struct PfRoles {
 // packed-weight ring and the activation / t image ring.
 template <int NMAT, int NG = 1>
 struct PfCfg {
-  static constexpr int kPS = (NG == 2 || NMAT == 2) ? PF_PS2 : 16;  // packed-weight ring (HBM latency)
+  static constexpr int kPS = (NG == 2 || NMAT == 2) ? PF_PS2 : 10;  // packed-weight ring (HBM latency)
   static constexpr int kStageCols = NG * NMAT * 32;  // TMEM columns of one A stage
-  static constexpr int kACol0 = 256;
-  static constexpr int kAS = 256 / kStageCols;       // A slots in TMEM
+  static constexpr int kASMax = 384 / kStageCols;    // A slots in TMEM (the accumulators take >= 128 columns)
   static constexpr int kBRegion = PF_B_KB * 1024;
   static constexpr int kBSMax = 16;                      // B slots = region / (ntok_max x 128), <= 16
-  static constexpr int kStageP = NG * NMAT * kPfPackedPerMat;
+  // the producers move 128 k per ring slot (two 64-k stages): a bulk copy costs
+  // its issuing thread ~400-650 cycles whatever its size, so fewer, larger copies
+  static constexpr int kStageP = 2 * NG * NMAT * kPfPackedPerMat;  // [nm][slab][4 k-tiles]
   static constexpr int kOffB = 0;                        // 1024-aligned images first
   static constexpr int kOffP = kOffB + kBRegion;
   static constexpr int kOffBar = kOffP + kPS * kStageP;
   // p_full[PS] p_empty[PS] a_full[AS] a_empty[AS] b_full[BSMax] b_empty[BSMax] acc_full[2] acc_empty[2]
-  static constexpr int kNumBars = 2 * kPS + 2 * kAS + 2 * kBSMax + 4;
+  // (B slots: two 64-k activation images of a main-stage pair, or one t image)
+  static constexpr int kNumBars = 2 * kPS + 2 * kASMax + 2 * kBSMax + 4;
   static constexpr int kOffTmem = kOffBar + kNumBars * 8;
   static constexpr int kOffStage = (kOffTmem + 16 + 127) & ~127;  // epilogue transpose [4 warps][32][33] f32
-  static constexpr int kBytes = kOffStage + kPfEpiWarps * 32 * 33 * 4 + 1024;  // + alignment slack
+  static constexpr int kBytes = kOffStage + kPfEpiWarps * 16 * 33 * 4 + 1024;  // + alignment slack
   static constexpr int kTmemCols = 512;
 };
 
@@ -277,6 +285,40 @@ __device__ __forceinline__ void pf_item(const PfArgs& a, int item, int& p, int& 
   tt = rel - nt * tts;
 }
 
+// One main stage of one dequant warp: for each of the stage's NM matrices /
+// n-tiles, the half IH of the 4 units of slab tiles (kt = 0, 1) -> binary16
+// W^T rows of TMEM lanes taddr .. + 31 (16x256b stores, n subtiles 2 IH, 2 IH + 1).
+template <int IH, int NM>
+__device__ __forceinline__ void pf_dequant_stage(const uint8_t* sP, int lane, const DqConsts& dq, uint32_t taddr) {
+  const int q = lane & 3;
+#pragma unroll
+  for (int nm = 0; nm < NM; ++nm) {  // tiles of (nm, slab, kt) at ((nm * 2 + slab) * 2 + kt) * 896
+    uint32_t v0[16], v1[16];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {  // unit (kt, j) = 16-k block u of the stage
+      const int kt = u >> 1, j = u & 1;
+      const uint8_t* tile = sP + (nm * 8 + kt) * kTileBytes;  // [nm][slab][4 k-tiles]
+      const uint2 wa = *reinterpret_cast<const uint2*>(tile + kPlaneAOff + lane * 16 + 8 * j);
+      const uint32_t wb = *reinterpret_cast<const uint32_t*>(tile + kPlaneBOff + lane * 8 + 4 * j);
+      const uint4 mm = *reinterpret_cast<const uint4*>(tile + kMetaOff + q * 32 + 16 * j);
+      const uint32_t S2[2] = {mm.x, mm.z}, O2[2] = {mm.y, mm.w};
+      uint32_t o[8];
+      half_unit_dequant<IH>(wa.x, wa.y, wb, S2, O2, dq, o);
+      // o[4 il + r]: row g + 8 (r & 1), k pair q + 4 (r >> 1)
+      v0[4 * u + 0] = o[0];
+      v0[4 * u + 1] = o[2];
+      v0[4 * u + 2] = o[1];
+      v0[4 * u + 3] = o[3];
+      v1[4 * u + 0] = o[4];
+      v1[4 * u + 1] = o[6];
+      v1[4 * u + 2] = o[5];
+      v1[4 * u + 3] = o[7];
+    }
+    tmem_st16x256_x4(taddr + (uint32_t)(nm * 32), v0);
+    tmem_st16x256_x4(taddr + (16u << 16) + (uint32_t)(nm * 32), v1);
+  }
+}
+
 // ---------------------------------------------------------------- the kernel
 // Persistent: CTA c handles items c, c + grid, ...  Three rings decouple the
 // roles: packed weights (deep, HBM latency), dequantized A, activation images.
@@ -301,10 +343,10 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
   }
 
   constexpr int kPfDeqGroups = PfRoles<NMAT, NG>::kGroups;
-  static_assert(kPfDeqGroups <= PfCfg<NMAT, NG>::kAS, "dequant groups must not outnumber A slots");
+  static_assert(kPfDeqGroups <= 4, "dequant groups must not outnumber A slots (>= 4)");
   using CF = PfCfg<NMAT, NG>;
-  constexpr int PS = CF::kPS, AS = CF::kAS;
-  const int bslot = a.ntok_max * 128;
+  constexpr int PS = CF::kPS;
+  const int bslot = 2 * a.ntok_max * 128;
   const int BS = min(CF::kBSMax, CF::kBRegion / bslot);
   // accumulators: per matrix a 32-column-aligned block of ntok_max columns;
   // two buffers when both fit the 256 accumulator columns
@@ -312,9 +354,14 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
   // one accumulator per (n-tile, matrix); a single-accumulator kernel with
   // small token tiles splits each stage's k over two accumulators (one per
   // MMA issuer, summed by the epilogue)
-  const bool ksplit = NG * NMAT == 1 && a.ntok_max <= 64;
+  const bool ksplit = PF_ISSUERS == 2 && NG * NMAT == 1 && a.ntok_max <= 64;
   const int acc_cols = (ksplit ? 2 : NG * NMAT) * mstride;
-  const int nacc = acc_cols <= 128 ? 2 : 1;
+  // TMEM columns: accumulators (double-buffered when that leaves >= PF_MIN_AS
+  // A slots), then the A slots.  The A ring's depth covers the dequant ->
+  // MMA -> release loop latency (~4 stages measured at 64 tokens).
+  const int nacc = (acc_cols <= 128 && (512 - 2 * acc_cols) / CF::kStageCols >= PF_MIN_AS) ? 2 : 1;
+  const int a_col0 = nacc * acc_cols;
+  const int AS = min(CF::kASMax, (512 - a_col0) / CF::kStageCols);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-B aligned base (SW128 atoms); pointer arithmetic keeps the shared address space
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -322,8 +369,8 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
   uint64_t* p_full = bars;
   uint64_t* p_empty = p_full + PS;
   uint64_t* a_full = p_empty + PS;
-  uint64_t* a_empty = a_full + AS;
-  uint64_t* b_full = a_empty + AS;
+  uint64_t* a_empty = a_full + CF::kASMax;
+  uint64_t* b_full = a_empty + CF::kASMax;
   uint64_t* b_empty = b_full + CF::kBSMax;
   uint64_t* acc_full = b_empty + CF::kBSMax;  // [2]
   uint64_t* acc_empty = acc_full + 2;  // [2]
@@ -334,7 +381,7 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
   if (threadIdx.x == 0) {
     for (int s = 0; s < PS; ++s) {
       mbar_init(&p_full[s], 1);
-      mbar_init(&p_empty[s], kPfGroupWarps);
+      mbar_init(&p_empty[s], 2 * kPfGroupWarps);  // the two groups of the slot's two stages
     }
     for (int s = 0; s < AS; ++s) {
       mbar_init(&a_full[s], kPfGroupWarps);
@@ -396,27 +443,27 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
     tpart = part == 1 ? 1 : 0;
   };
 
-#if PF_PROF_MMA  // experiments: MMA-thread cycle split (CTA 0 -> dbg trace row kPfTraceStages - 1)
+#if PF_PROF  // per-role cycle split, CTA 0 -> dbg trace row kPfTraceStages - 1 - role
   long long pf_prof[4] = {0, 0, 0, 0};
-#define PF_PROF_T(v) const long long v = clock64()
-#define PF_PROF_ACC(c0, c1, c2, c3, c4) \
-  pf_prof[0] += c1 - c0;                \
-  pf_prof[1] += c2 - c1;                \
-  pf_prof[2] += c3 - c2;                \
-  pf_prof[3] += c4 - c3
-#define PF_PROF_OUT()                                                                          \
-  if (a.dbg != nullptr && blockIdx.x == 0)                                                     \
-    for (int i = 0; i < 4; ++i) a.dbg[148 * 8 + (kPfTraceStages - 1) * 8 + i] = pf_prof[i]
+  long long pf_t0 = clock64();
+#define PF_LAP(i)                    \
+  do {                               \
+    const long long t_ = clock64();  \
+    pf_prof[i] += t_ - pf_t0;        \
+    pf_t0 = t_;                      \
+  } while (0)
+#define PF_PROF_OUT(role)                                                                         \
+  if (a.dbg != nullptr && blockIdx.x == 0)                                                        \
+    for (int i = 0; i < 4; ++i) a.dbg[148 * 8 + (kPfTraceStages - 1 - (role)) * 8 + i] = pf_prof[i]
 #else
-#define PF_PROF_T(v)
-#define PF_PROF_ACC(c0, c1, c2, c3, c4)
-#define PF_PROF_OUT()
+#define PF_LAP(i)
+#define PF_PROF_OUT(role)
 #endif
   if (warp == kPfProdWarp) {
     // ======================= packed-weight producer =======================
     // A stage's NG x NMAT x 2 copies are issued by as many lanes in parallel: one
     // thread serialises its bulk copies at ~300 cycles each (tools/micro/bulk_issue.cu).
-    constexpr int kCopies = NG * NMAT * 2;
+    constexpr int kCopies = NG * NMAT * 2;  // one 4-k-tile run of one slab each
     if (lane < kCopies) {
       const int ng = lane / (NMAT * 2), mat = (lane / 2) % NMAT, sl = lane & 1;
       int ps = 0, gs0 = 0;
@@ -425,18 +472,18 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
         int p, nt, tt;
         pf_item<NG>(a, item, p, nt, tt);
         const PfProblem P = a.problems[p];  // by value: fields live in registers
-        const int ks = P.k / kPfK, kts = P.k / kTileK;
-        for (int st = 0; st < ks; ++st) {
+        const int ks2 = P.k / (2 * kPfK), kts = P.k / kTileK;
+        for (int sp = 0; sp < ks2; ++sp) {
           ring_wait(&p_empty[ps], pph ^ 1);
-
+          PF_LAP(0);
           uint8_t* sP = smem + CF::kOffP + ps * CF::kStageP;
           if (lane == 0) mbar_arrive_expect_tx(&p_full[ps], (uint32_t)CF::kStageP);
           __syncwarp((1u << kCopies) - 1u);
-          const int kst = (st + nt * 13) % ks;  // rotated k order per n-tile (spreads L2 hot spots)
-          const uint8_t* src = P.w[mat] + ((int64_t)(2 * (NG * nt + ng) + sl) * kts + 2 * kst) * kTileBytes;
-          bulk_g2s(sP + ((ng * NMAT + mat) * 2 + sl) * 2 * kTileBytes, src, 2 * kTileBytes, &p_full[ps]);
-          if (lane == 0) pf_trace(gs0 + st, 0);
-
+          const int kp = (sp + nt * 13) % ks2;  // rotated k order per n-tile (spreads L2 hot spots)
+          const uint8_t* src = P.w[mat] + ((int64_t)(2 * (NG * nt + ng) + sl) * kts + 4 * kp) * kTileBytes;
+          bulk_g2s(sP + ((ng * NMAT + mat) * 2 + sl) * 4 * kTileBytes, src, 4 * kTileBytes, &p_full[ps]);
+          if (lane == 0) pf_trace(gs0 + 2 * sp, 0);
+          PF_LAP(1);
           if (++ps == PS) {
             ps = 0;
             pph ^= 1;
@@ -444,10 +491,15 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
         }
         gs0 += item_stages(P);
       }
-      if (lane == 0) pf_dbg(1);
+      if (lane == 0) {
+        PF_PROF_OUT(3);
+        pf_dbg(1);
+      }
     }
   } else if (warp == kPfBWarp) {
     // ======================= activation / t image producer =======================
+    // one copy per main-stage pair (the two 64-k images of a token tile are
+    // adjacent), one per LoRC stage
     if (lane == 0) {
       int bs = 0, gs = 0;
       uint32_t bph = 0;
@@ -456,27 +508,34 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
         pf_item<NG>(a, item, p, nt, tt);
         const PfProblem P = a.problems[p];  // by value: fields live in registers
         const int ks = P.k / kPfK, total = item_stages(P);
+        const uint32_t ib = (uint32_t)P.ntok * 128u;  // one token-tile image
         for (int st = 0; st < total; ++st, ++gs) {
+          if (st < ks && (st & 1)) continue;  // second stage of a pair: already in the slot
           ring_wait(&b_empty[bs], bph ^ 1);
+          PF_LAP(0);
           uint8_t* sB = smem + CF::kOffB + bs * bslot;
           const uint8_t* src;
-          const uint32_t ib = (uint32_t)P.ntok * 128u;  // one token-tile image
+          uint32_t bytes = ib;
           if (st < ks) {
-            src = P.act + ((int64_t)tt * ks + (st + nt * 13) % ks) * ib;  // same rotation as the weights
+            const int kp = (st / 2 + nt * 13) % (ks / 2);  // same rotation as the weights
+            src = P.act + ((int64_t)tt * ks + 2 * kp) * ib;
+            bytes = 2 * ib;
           } else {
             int mat, ch, vpart, tpart;
             lorc_stage(P, st - ks, mat, ch, vpart, tpart);
             src = P.timg[mat] + (((int64_t)tt * P.rchunks[mat] + ch) * 2 + tpart) * ib;
           }
-          mbar_arrive_expect_tx(&b_full[bs], ib);
-          bulk_g2s(sB, src, ib, &b_full[bs]);
+          mbar_arrive_expect_tx(&b_full[bs], bytes);
+          bulk_g2s(sB, src, bytes, &b_full[bs]);
           pf_trace(gs, 7);
+          PF_LAP(1);
           if (++bs == BS) {
             bs = 0;
             bph ^= 1;
           }
         }
       }
+      PF_PROF_OUT(2);
       pf_dbg(2);
     }
   } else if (warp >= kPfDeqWarp0) {
@@ -505,44 +564,23 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
       for (int st = 0; st < total; ++st, ++gs) {
         const bool mine = (gs % kPfDeqGroups) == grp;
         if (mine) {
-          const uint32_t a_col = tmem + (uint32_t)(CF::kACol0 + as * CF::kStageCols);
+          const uint32_t a_col = tmem + (uint32_t)(a_col0 + as * CF::kStageCols);
+          PF_LAP(3);  // (not this group's stages)
           ring_wait(&a_empty[as], aph ^ 1);  // the MMAs that read this slot are done
+          PF_LAP(0);
           tc_fence_after();
           if (gw == 0 && lane == 0) pf_trace(gs, 1);
           if (st < ks) {
             ring_wait(&p_full[ps], pph);
+            PF_LAP(1);
             if (gw == 0 && lane == 0) pf_trace(gs, 2);
-            const uint8_t* sP = smem + CF::kOffP + ps * CF::kStageP;
-            if (!(a.flags & 1)) {
-#pragma unroll
-              for (int nm = 0; nm < NG * NMAT; ++nm) {  // nm = ng * NMAT + mat
-                uint32_t v0[16], v1[16];  // n subtiles 2 ih, 2 ih + 1
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {  // unit (kt, j) = 16-k block u of the stage
-                  const int kt = u >> 1, j = u & 1;
-                  const uint8_t* tile = sP + ((nm * 2 + sl) * 2 + kt) * kTileBytes;
-                  const uint2 wa = *reinterpret_cast<const uint2*>(tile + kPlaneAOff + lane * 16 + 8 * j);
-                  const uint32_t wb = *reinterpret_cast<const uint32_t*>(tile + kPlaneBOff + lane * 8 + 4 * j);
-                  const uint4 mm = *reinterpret_cast<const uint4*>(tile + kMetaOff + q * 32 + 16 * j);
-                  const uint32_t S2[2] = {mm.x, mm.z}, O2[2] = {mm.y, mm.w};
-                  uint32_t o[8];
-                  if (ih == 0)
-                    half_unit_dequant<0>(wa.x, wa.y, wb, S2, O2, dq, o);
-                  else
-                    half_unit_dequant<1>(wa.x, wa.y, wb, S2, O2, dq, o);
-                  // o[4 il + r]: row g + 8 (r & 1), k pair q + 4 (r >> 1)
-                  v0[4 * u + 0] = o[0];
-                  v0[4 * u + 1] = o[2];
-                  v0[4 * u + 2] = o[1];
-                  v0[4 * u + 3] = o[3];
-                  v1[4 * u + 0] = o[4];
-                  v1[4 * u + 1] = o[6];
-                  v1[4 * u + 2] = o[5];
-                  v1[4 * u + 3] = o[7];
-                }
-                tmem_st16x256_x4(a_col + lane_q + (uint32_t)(nm * 32), v0);
-                tmem_st16x256_x4(a_col + lane_q + (16u << 16) + (uint32_t)(nm * 32), v1);
-              }
+            // this stage's k-tiles: 2 (st & 1), + 1 of the slot's [nm][slab][4] runs
+            const uint8_t* sP = smem + CF::kOffP + ps * CF::kStageP + (sl * 4 + (st & 1) * 2) * kTileBytes;
+            if (!(a.flags & 1)) {  // branch-free stage bodies per half (the units interleave)
+              if (ih == 0)
+                pf_dequant_stage<0, NG * NMAT>(sP, lane, dq, a_col + lane_q);
+              else
+                pf_dequant_stage<1, NG * NMAT>(sP, lane, dq, a_col + lane_q);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&p_empty[ps]);
@@ -566,13 +604,14 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
               tmem_st32x32_x32(a_col + lane_q + (uint32_t)((ng * NMAT + mat) * 32), v);
             }
           }
+          PF_LAP(2);
           tmem_st_wait();
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&a_full[as]);
           if (gw == 0 && lane == 0) pf_trace(gs, 3);
         }
-        if (st < ks && ++ps == PS) {
+        if (st < ks && (st & 1) && ++ps == PS) {  // a slot holds a stage pair
           ps = 0;
           pph ^= 1;
         }
@@ -582,7 +621,10 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
         }
       }
     }
-    if (dw == 0 && lane == 0) pf_dbg(3);
+    if (dw == 0 && lane == 0) {
+      PF_PROF_OUT(4);
+      pf_dbg(3);
+    }
   } else if (warp == kPfWaitWarp) {
     // ======================= ring waiter =======================
     if (lane == 0) {
@@ -591,23 +633,28 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
       for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
         int p, nt, tt;
         pf_item<NG>(a, item, p, nt, tt);
-        const int total = item_stages(a.problems[p]);
+        const int total = item_stages(a.problems[p]), ks = a.problems[p].k / kPfK;
         for (int st = 0; st < total; ++st, ++gs) {
           ring_wait(&a_full[as], aph);
+          PF_LAP(0);
           pf_trace(gs, 4);
-          ring_wait(&b_full[bs], bph);
+          const bool pair2 = st < ks && (st & 1);  // B slot of a pair: loaded with the first stage
+          if (!pair2) ring_wait(&b_full[bs], bph);
+          PF_LAP(1);
           pf_trace(gs, 5);
           st_release_cta_shared(stages_ready, (uint32_t)(gs + 1));
+          PF_LAP(2);
           if (++as == AS) {
             as = 0;
             aph ^= 1;
           }
-          if (++bs == BS) {
+          if (!(st < ks && !(st & 1)) && ++bs == BS) {  // slot done after its last stage
             bs = 0;
             bph ^= 1;
           }
         }
       }
+      PF_PROF_OUT(1);
     }
   } else if (warp == kPfMmaWarp || warp == kPfMmaWarp2) {
     // ======================= MMA issuers =======================
@@ -622,6 +669,7 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
       const uint64_t dB0 = pf_desc_sw128(smem_u32(smem + CF::kOffB));
       const bool mma_on = !(a.flags & 2);
       int as = 0, bs = 0;
+      bool slot_issued = false;
       int acc = 0, gs = 0;
       uint32_t acc_phase = 0;
       for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
@@ -632,60 +680,67 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
         const uint32_t idesc = pf_idesc(P.ntok);
         ring_wait(&acc_empty[acc], acc_phase ^ 1);
         tc_fence_after();
-        const uint32_t d0 = tmem + (uint32_t)(acc * acc_cols + issuer * mstride);  // this issuer's accumulator
-        const bool idle = NG * NMAT == 1 && !ksplit && issuer == 1;
+        const uint32_t d0 = tmem + (uint32_t)(acc * acc_cols);  // accumulator buffer
+        const bool idle = (PF_ISSUERS == 1 || (NG * NMAT == 1 && !ksplit)) && issuer == 1;
         for (int st = 0; st < total; ++st, ++gs) {
-          PF_PROF_T(c0);
           // an mbarrier wait costs a thread that issues MMAs ~200 cycles even when
           // the phase completed long ago (tools/micro/mma_rate.cu); the wait warp
           // does the ring waits and publishes a stage counter instead
           while (ld_acquire_cta_shared(stages_ready) <= (uint32_t)gs) {
           }
-          PF_PROF_T(c1);
-          PF_PROF_T(c2);
+          PF_LAP(0);
           tc_fence_after();
           // operand addresses: TMEM A slot, B descriptor of the slot (the 16-B
           // address field advances by 2 per 16-k step); everything unrolled
-          const uint32_t aA = tmem + (uint32_t)(CF::kACol0 + as * CF::kStageCols);
-          const uint64_t dB = dB0 + (uint64_t)((uint32_t)(bs * bslot) >> 4);
+          const uint32_t aA = tmem + (uint32_t)(a_col0 + as * CF::kStageCols);
+          // B: the slot's first or second image (main-stage pair) or its t image
+          const bool pair2 = st < ks && (st & 1), pair1 = st < ks && !(st & 1);
+          const uint64_t dB = dB0 + (uint64_t)((uint32_t)(bs * bslot + (pair2 ? P.ntok * 128 : 0)) >> 4);
           bool issued = false;
           if (!idle && mma_on) {
-            int nm = issuer;  // A block (ng * NMAT + mat) this issuer multiplies
             uint32_t acc0 = 1u;
+            int lmat = -1;  // LoRC stage: its matrix
             if (st < ks) {
               acc0 = st > 0 ? 1u : 0u;
             } else {
-              int mat, ch, vpart, tpart;
-              lorc_stage(P, st - ks, mat, ch, vpart, tpart);
-              if (NMAT == 2) nm = mat == issuer ? mat : -1;  // the other matrix's issuer sits out
+              int ch, vpart, tpart;
+              lorc_stage(P, st - ks, lmat, ch, vpart, tpart);
             }
-            if (NG * NMAT == 1) nm = 0;
-            if (nm >= 0) {
-              const uint32_t aN = aA + (uint32_t)(nm * 32);
-              if (NG * NMAT == 1 && ksplit) {  // k16 steps issuer, issuer + 2
-                pf_mma_ts_w(d0, aN + (uint32_t)(issuer * 8), dB + 2 * issuer, idesc, acc0);
-                pf_mma_ts_w(d0, aN + (uint32_t)(issuer * 8 + 16), dB + 2 * issuer + 4, idesc, 1u);
-              } else {
+            if (NG * NMAT == 1 && ksplit) {  // k16 steps issuer, issuer + 2 into accumulator issuer
+              const uint32_t dI = d0 + (uint32_t)(issuer * mstride);
+              pf_mma_ts_w(dI, aA + (uint32_t)(issuer * 8), dB + 2 * issuer, idesc, acc0);
+              pf_mma_ts_w(dI, aA + (uint32_t)(issuer * 8 + 16), dB + 2 * issuer + 4, idesc, 1u);
+              issued = true;
+            } else {
+#pragma unroll
+              for (int nm = 0; nm < NG * NMAT; ++nm) {  // A block (ng * NMAT + mat) = accumulator nm
+                if (PF_ISSUERS == 2 && nm % 2 != issuer) continue;
+                if (lmat >= 0 && nm % NMAT != lmat) continue;  // LoRC: that matrix's blocks only
 #pragma unroll
                 for (int k16 = 0; k16 < kPfK / 16; ++k16)
-                  pf_mma_ts_w(d0, aN + (uint32_t)(k16 * 8), dB + 2 * k16, idesc, k16 > 0 ? 1u : acc0);
+                  pf_mma_ts_w(d0 + (uint32_t)(nm * mstride), aA + (uint32_t)(nm * 32 + k16 * 8), dB + 2 * k16, idesc,
+                              k16 > 0 ? 1u : acc0);
+                issued = true;
               }
-              issued = true;
             }
           }
-          PF_PROF_T(c3);
-          if (issued) {
+          PF_LAP(1);
+          if (issued)
             pf_commit_w(&a_empty[as]);
-            pf_commit_w(&b_empty[bs]);
-          } else {
+          else
             mbar_arrive_w(&a_empty[as]);
-            mbar_arrive_w(&b_empty[bs]);
+          slot_issued |= issued;
+          if (!pair1) {  // the B slot's last stage: release it (a commit covers both stages of a pair)
+            if (slot_issued)
+              pf_commit_w(&b_empty[bs]);
+            else
+              mbar_arrive_w(&b_empty[bs]);
+            slot_issued = false;
+            if (++bs == BS) bs = 0;
           }
-          PF_PROF_T(c4);
+          PF_LAP(2);
           if (issuer == 0 && lane == 0) pf_trace(gs, 6);
-          PF_PROF_ACC(c0, c1, c2, c3, c4);
           if (++as == AS) as = 0;
-          if (++bs == BS) bs = 0;
         }
         if (idle || !mma_on)
           mbar_arrive_w(&acc_full[acc]);
@@ -697,7 +752,7 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
         }
       }
       if (issuer == 0 && lane == 0) {
-        PF_PROF_OUT();
+        PF_PROF_OUT(0);
         pf_dbg(4);
       }
     }
@@ -718,7 +773,7 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
       const int rows = P.rows, kind = P.kind, odt = P.out_dtype;
       const int64_t ldo = P.ldo;
       const int32_t* rmap = P.row_map;
-      float* stg = reinterpret_cast<float*>(smem + CF::kOffStage) + ew * 32 * 33;
+      float* stg = reinterpret_cast<float*>(smem + CF::kOffStage) + ew * 16 * 33;
       const int ntok = P.ntok;
 #pragma unroll 1
       for (int ng = 0; ng < NG; ++ng) {

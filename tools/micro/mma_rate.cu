@@ -193,6 +193,27 @@ __global__ void __launch_bounds__(32 * (1 + NOISE), 1) noisy_rate(int n, int sta
       done = 1;
       if (blockIdx.x == 0) out[0] = t1 - t0;
     }
+  } else if (seed == 7) {  // tcgen05.st traffic: each noise warp rewrites 32 columns of its lane quarter
+    const uint32_t q = (uint32_t)(warp & 3) * 32;
+    uint32_t v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = threadIdx.x * 16 + i;
+    long long t0 = clock64(), iters = 0;
+    while (!done) {
+      ++iters;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint32_t col = 384u + (uint32_t)(((warp >> 2) * 8 + i) & 3) * 32;
+        asm volatile(
+            "tcgen05.st.sync.aligned.16x256b.x4.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+                tmem + (q << 16) + col),
+            "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+            "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+            : "memory");
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 32) out[1] = (clock64() - t0) / (iters > 0 ? iters : 1);
   } else {
     __half2 a = __float2half2_rn((float)(seed & 7)), b = __float2half2_rn(0.5f), c = __float2half2_rn(0.25f);
     uint32_t w = seed ^ threadIdx.x;
@@ -211,14 +232,16 @@ __global__ void __launch_bounds__(32 * (1 + NOISE), 1) noisy_rate(int n, int sta
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 template <int NOISE>
-void run_noisy(long long* d) {
+void run_noisy(long long* d, uint32_t seed = 3) {
   long long h[2];
   const int stages = 2048;
-  for (int rep = 0; rep < 2; ++rep) noisy_rate<NOISE><<<148, 32 * (1 + NOISE)>>>(64, stages, d, 3);
+  for (int rep = 0; rep < 2; ++rep) noisy_rate<NOISE><<<148, 32 * (1 + NOISE)>>>(64, stages, d, seed);
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) printf("error %s\n", cudaGetErrorString(e));
   cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
-  printf("4 MMAs (ts N=64) + commit with %2d busy ALU warps: %7.1f cyc/stage\n", NOISE, (double)h[0] / stages);
+  printf("4 MMAs (ts N=64) + commit with %2d busy %s warps: %7.1f cyc/stage; %s\n", NOISE, seed == 7 ? "TMEM-store" : "ALU",
+         (double)h[0] / stages, seed == 7 ? "" : "");
+  if (seed == 7) printf("   per store warp: 8 x 16x256b.x4 stores + wait::st = %lld cycles\n", h[1]);
 }
 
 template <int PER, int WAIT>
@@ -243,10 +266,10 @@ int main() {
   cudaFuncSetAttribute(mma_rate<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int iters = 4096;
   run_noisy<0>(d);
-  run_noisy<3>(d);
-  run_noisy<7>(d);
-  run_noisy<12>(d);
-  run_noisy<19>(d);
+  run_noisy<1>(d, 7);
+  run_noisy<4>(d, 7);
+  run_noisy<8>(d, 7);
+  run_noisy<12>(d, 7);
   run_stage<4, 0>(d, 64);
   run_stage<4, 1>(d, 64);
   run_stage<4, 2>(d, 64);

@@ -81,8 +81,12 @@ for ph in range(2):
                             (7, 5, "B issued -> MMA saw B"), (1, 3, "slot free -> A ready")]:
             g = t[:, b_] - t[:, a_]
             print(f"  {lbl:36s} med {np.median(g):7.3f}  p90 {np.percentile(g, 90):7.3f} us")
-    raw = dd[148 * 8 + (TS - 1) * 8:148 * 8 + (TS - 1) * 8 + 4]
-    if os.environ.get("MILO_B200_LIB_VARIANT") and raw.sum() > 0:  # PF_PROF_MMA build: MMA-thread cycles
-        tot = raw.sum()
-        print("  MMA thread cycles: " + ", ".join(f"{n} {v / tot * 100:.0f}%" for n, v in
-              zip(["wait A", "wait B", "issue", "commit"], raw)) + f" (total {tot / 1e6:.2f} Mcyc)")
+    if os.environ.get("MILO_B200_LIB_VARIANT"):  # PF_PROF build: per-role cycle split of CTA 0
+        roles = [("MMA issuer 0", ["wait stage", "MMAs", "commits"]), ("ring waiter", ["wait A", "wait B", "publish"]),
+                 ("B producer", ["wait slot", "copy"]), ("packed producer", ["wait slot", "copies"]),
+                 ("dequant w0", ["wait A slot", "wait packed", "dequant+st", "tail/idle"])]
+        for r, (nm, parts) in enumerate(roles):
+            raw = dd[148 * 8 + (TS - 1 - r) * 8:148 * 8 + (TS - 1 - r) * 8 + 4]
+            tot = raw.sum()
+            if tot > 0:
+                print(f"  {nm:16s} {tot / 1e6:6.3f} Mcyc: " + ", ".join(f"{p_} {v / tot * 100:.0f}%" for p_, v in zip(parts, raw)))
