@@ -2235,6 +2235,8 @@ milo_status moe_prefill_dev(milo_moe* moe, const void* x, int64_t m, int32_t x_d
   }
   pa.h = reinterpret_cast<__half*>(b + o_h);
   pa.Y = reinterpret_cast<float*>(b + o_y);
+  // (programmatic launches of this chain measured no faster: the early CTAs of
+  // each dependent grid hold SM slots while the previous grid drains)
   CUDA_TRY(launch(moe_plan_kernel, dim3(1), dim3(1024), 0, stream, false, pa));
   static thread_local int configured_dev = -1;
   int dev = 0;

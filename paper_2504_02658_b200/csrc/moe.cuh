@@ -81,6 +81,7 @@ __device__ __forceinline__ void topk_warp(const float* __restrict__ l, int64_t t
 __global__ void router_topk_kernel(const float* __restrict__ logits, int64_t m, int E, int K,
                                    int score_mode, int32_t* __restrict__ ids,
                                    float* __restrict__ wts) {
+  pdl_wait();  // logits may come from the preceding grid
   const int warps = blockDim.x >> 5;
   const int64_t t = (int64_t)blockIdx.x * warps + (threadIdx.x >> 5);
   if (t >= m) return;

@@ -1204,6 +1204,7 @@ __device__ __forceinline__ void pf_t_any_unit(const TProb* __restrict__ probs, i
 template <int KIND>
 __global__ void __launch_bounds__(256, KIND == 0 ? 4 : 1) pf_t_kernel(const TProb* __restrict__ probs, int n_probs,
                                                                     const int32_t* __restrict__ dev_counts) {
+  pdl_wait();  // inputs come from the preceding grid (programmatic dependent launch)
   constexpr int kSm = KIND == 0 ? sizeof(TTcSmem) : sizeof(TCoreSmem);
   __shared__ __align__(16) uint8_t sm[kSm];
   if (dev_counts == nullptr) {
@@ -1323,6 +1324,7 @@ __device__ __forceinline__ void pf_img_t_unit(const ImgJob* __restrict__ jobs, i
 // then loop over the planned blocks (grid-stride), else CTA = block.
 __global__ void __launch_bounds__(256) pf_img_t_kernel(const ImgJob* __restrict__ jobs, int n_jobs,
                                                       const int32_t* __restrict__ dev_counts) {
+  pdl_wait();  // inputs come from the preceding grid (programmatic dependent launch)
   if (dev_counts == nullptr) {
     pf_img_t_unit(jobs, n_jobs, blockIdx.x);
     return;
@@ -1338,6 +1340,7 @@ __global__ void __launch_bounds__(256) pf_img_t_kernel(const ImgJob* __restrict_
 // Sums the k-split partials in split order and writes the hi / lo images.
 __global__ void pf_t_images_kernel(const TProb* __restrict__ probs, int n_probs,
                                    const int32_t* __restrict__ dev_counts) {
+  pdl_wait();  // inputs come from the preceding grid (programmatic dependent launch)
   if (dev_counts != nullptr) n_probs = dev_counts[0];
   for (int pi = blockIdx.y; pi < n_probs; pi += gridDim.y) {
   const TProb& P = probs[pi];
@@ -1422,6 +1425,7 @@ __device__ __forceinline__ int pf_t_splits_dev(int64_t rows, int64_t k, int rch,
 constexpr int kPlanMaxGroups = 256;  // >= E + S (kRouteMaxE)
 
 __global__ void __launch_bounds__(1024) moe_plan_kernel(PfPlanArgs a) {
+  pdl_wait();  // inputs come from the preceding grid (programmatic dependent launch)
   __shared__ int32_t s_cnt[kPlanMaxGroups];   // rows per expert (routed, shared)
   __shared__ int32_t s_off[kPlanMaxGroups];   // grouped row offset
   __shared__ int32_t s_gexp[kPlanMaxGroups];  // group -> expert
