@@ -2237,7 +2237,19 @@ milo_status moe_prefill_dev(milo_moe* moe, const void* x, int64_t m, int32_t x_d
   pa.Y = reinterpret_cast<float*>(b + o_y);
   // (programmatic launches of this chain measured no faster: the early CTAs of
   // each dependent grid hold SM slots while the previous grid drains)
-  CUDA_TRY(launch(moe_plan_kernel, dim3(1), dim3(1024), 0, stream, false, pa));
+  pa.dbg = g_dbg ? g_dbg + 2 * kPfDbgLongs : nullptr;  // after the two GEMM phases' regions
+  const size_t ids_smem = (size_t)m * K * 4;
+  pa.ids_cached = ids_smem <= kPlanIdsSmem ? 1 : 0;
+  {
+    static thread_local int plan_dev = -1;
+    int dv = 0;
+    cudaGetDevice(&dv);
+    if (plan_dev != dv) {
+      CUDA_TRY(cudaFuncSetAttribute(moe_plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPlanIdsSmem));
+      plan_dev = dv;
+    }
+  }
+  CUDA_TRY(launch(moe_plan_kernel, dim3(1), dim3(1024), pa.ids_cached ? ids_smem : 0, stream, false, pa));
   static thread_local int configured_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);

@@ -1394,6 +1394,8 @@ struct PfExpertStatic {
 //   [0] n_jobs  [1] img blocks  [2] n_tprobs  [3] t units  [4] n_problems  [5] n_items  [6] ntok_max
 struct PfPlanArgs {
   const int32_t* ids;             // m x K routing (-1 = unused)
+  int32_t ids_cached;             // the ids fit the launch's dynamic shared memory (m K int32)
+  long long* dbg;                 // optional: globaltimer after each planning step (debug)
   int64_t m;
   int32_t K, E, S, sms;
   const PfExpertStatic* ex;       // E routed then S shared
@@ -1417,15 +1419,24 @@ struct PfPlanArgs {
 };
 
 __device__ __forceinline__ int pf_ntok_dev(int64_t rows) { return (int)min((int64_t)kPfN, (rows + 15) / 16 * 16); }
-__device__ __forceinline__ int pf_t_splits_dev(int64_t rows, int64_t k, int rch, int sms) {
-  const int row_tiles = (int)((rows + kTRows - 1) / kTRows);
-  return max(1, min((int)(k / 256), (kTCtasPerSm * sms) / max(1, row_tiles * rch)));
+__device__ __forceinline__ int pf_t_splits_dev(int rows, int k, int rch, int sms) {  // 32-bit: one thread per group
+  const int row_tiles = (rows + kTRows - 1) / kTRows;
+  return max(1, min(k / 256, (kTCtasPerSm * sms) / max(1, row_tiles * rch)));
 }
 
 constexpr int kPlanMaxGroups = 256;  // >= E + S (kRouteMaxE)
+constexpr int kPlanIdsSmem = 160 * 1024;  // routing ids cached in shared memory up to this size
 
 __global__ void __launch_bounds__(1024) moe_plan_kernel(PfPlanArgs a) {
   pdl_wait();  // inputs come from the preceding grid (programmatic dependent launch)
+  auto stamp = [&](int i) {
+    if (a.dbg != nullptr && threadIdx.x == 0) {
+      long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      a.dbg[i] = t;
+    }
+  };
+  stamp(0);
   __shared__ int32_t s_cnt[kPlanMaxGroups];   // rows per expert (routed, shared)
   __shared__ int32_t s_off[kPlanMaxGroups];   // grouped row offset
   __shared__ int32_t s_gexp[kPlanMaxGroups];  // group -> expert
@@ -1437,6 +1448,15 @@ __global__ void __launch_bounds__(1024) moe_plan_kernel(PfPlanArgs a) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nwarps = blockDim.x >> 5;
   const int E = a.E, S = a.S, K = a.K;
   const int64_t m = a.m, mK = m * K;
+  // the routing ids in shared memory when they fit: the per-expert ballot scans
+  // below read them E + S times (global round trips dominated the plan)
+  extern __shared__ int32_t s_ids[];
+  const int32_t* ids = a.ids;
+  if (a.ids_cached) {
+    for (int64_t i = tid; i < mK; i += blockDim.x) s_ids[i] = a.ids[i];
+    ids = s_ids;
+  }
+  __syncthreads();
   for (int i = tid; i < (E + S) * 3; i += blockDim.x) {  // one parallel pass over the static table
     const PfMatStatic& M = a.ex[i / 3].m[i % 3];
     s_shape[i / 3][i % 3][0] = M.k;
@@ -1444,13 +1464,15 @@ __global__ void __launch_bounds__(1024) moe_plan_kernel(PfPlanArgs a) {
     s_shape[i / 3][i % 3][2] = M.rank;
     s_shape[i / 3][i % 3][3] = M.rch;
   }
+  stamp(1);
   // 1. rows per expert: one warp per expert scans the entries with ballots
   for (int e = warp; e < E + S; e += nwarps) {
     int64_t c = 0;
     if (e < E) {
-      for (int64_t base = 0; base < mK; base += 32) {
-        const int64_t i = base + lane;
-        const bool hit = i < mK && a.ids[i] == e;
+      const int n = (int)mK;
+      for (int base = 0; base < n; base += 32) {
+        const int i = base + lane;
+        const bool hit = i < n && ids[i] == e;
         c += __popc(__ballot_sync(0xffffffffu, hit));
       }
     } else {
@@ -1459,83 +1481,143 @@ __global__ void __launch_bounds__(1024) moe_plan_kernel(PfPlanArgs a) {
     if (lane == 0) s_cnt[e] = (int32_t)c;
   }
   __syncthreads();
-  // 2. groups (non-empty experts, expert order) and every per-group offset (serial: <= 512 groups)
-  if (tid == 0) {
-    int ng = 0;
-    int64_t off = 0, oimg[2] = {0, 0}, ot[3] = {0, 0, 0}, op[3] = {0, 0, 0};
-    int32_t blk[2] = {0, 0}, unit[3] = {0, 0, 0}, item[2] = {0, 0}, ntmax = 16;
-    int32_t ntp[2] = {0, 0};
-    for (int e = 0; e < E + S; ++e) {
-      const int64_t rows = s_cnt[e];
-      if (rows == 0) continue;
-      const int g = ng++;
-      s_gexp[g] = e;
-      s_off[g] = (int32_t)off;
-      const int nt = pf_ntok_dev(rows);
-      ntmax = max(ntmax, nt);
-      const int64_t tiles = (rows + nt - 1) / nt;
+  stamp(2);
+  // 2. groups (non-empty experts, expert order) and every per-group offset: thread e
+  //    sizes expert e's group, block-wide exclusive scans place them (a one-thread
+  //    loop over the groups cost 70-100 us at 66-128 experts)
+  {
+    constexpr int kQ = 18;  // scanned quantities
+    int64_t v[kQ];
+#pragma unroll
+    for (int i = 0; i < kQ; ++i) v[i] = 0;
+    const int e = tid;
+    const int rows = e < E + S ? s_cnt[e] : 0;
+    const int nt = rows > 0 ? pf_ntok_dev(rows) : 0;
+    const int tiles = rows > 0 ? (rows + nt - 1) / nt : 0;
+    int ks_j[3] = {0, 0, 0};
+    if (rows > 0) {
+      v[0] = 1;     // group index
+      v[1] = rows;  // grouped row offset
       // images: phase 1 over d, phase 2 over this expert's f (regions sized with f_max)
-      s_o[0][g] = oimg[0];
-      oimg[0] += (tiles * (a.d / kPfK) * nt * 128 + 255) & ~int64_t(255);
-      s_o[1][g] = oimg[1];
-      oimg[1] += (tiles * (a.f_max / kPfK) * nt * 128 + 255) & ~int64_t(255);
-      s_blk[0][g] = blk[0];
-      blk[0] += (int32_t)(tiles * (a.d / kPfK));
-      s_blk[1][g] = blk[1];
-      blk[1] += (int32_t)(tiles * (s_shape[e][2][0] / kPfK));
-      s_tp[0][g] = ntp[0];
-      s_tp[1][g] = ntp[1];
+      v[2] = ((int64_t)tiles * (a.d / kPfK) * nt * 128 + 255) & ~int64_t(255);
+      v[3] = ((int64_t)tiles * (a.f_max / kPfK) * nt * 128 + 255) & ~int64_t(255);
+      v[4] = (int64_t)tiles * (a.d / kPfK);
+      v[5] = (int64_t)tiles * (s_shape[e][2][0] / kPfK);
       for (int j = 0; j < 3; ++j) {
         const int mk = s_shape[e][j][0], rank = s_shape[e][j][2], rch = s_shape[e][j][3];
-        s_o[2 + j][g] = ot[j];
-        s_o[5 + j][g] = op[j];
-        s_unit[j][g] = 0;
         if (rank <= 0) continue;
-        ot[j] += (tiles * rch * 2 * nt * 128 + 255) & ~int64_t(255);
+        v[6 + j] = ((int64_t)tiles * rch * 2 * nt * 128 + 255) & ~int64_t(255);
         const int ks = pf_t_splits_dev(rows, mk, rch, a.sms);
-        op[j] += ((int64_t)max(mk / kPfK, ks) * rows * rch * 64 * 4 + 255) & ~int64_t(255);
-        const int ph = j == 2 ? 1 : 0;
-        s_unit[j][g] = unit[ph];  // unit0 of this t problem (phase-wide prefix)
-        unit[ph] += (int32_t)((rows + kTRows - 1) / kTRows) * rch * ks;
-        ++ntp[ph];
+        ks_j[j] = ks;
+        v[9 + j] = ((int64_t)max(mk / kPfK, ks) * rows * rch * 64 * 4 + 255) & ~int64_t(255);
+        v[12 + (j == 2 ? 1 : 0)] += (int64_t)((rows + kTRows - 1) / kTRows) * rch * ks;  // t units per phase
+        v[14 + (j == 2 ? 1 : 0)] += 1;                                                  // t problems per phase
       }
-      s_item[0][g] = item[0];
-      item[0] += (int32_t)((s_shape[e][0][1] / kPfM) * tiles);
-      s_item[1][g] = item[1];
-      item[1] += (int32_t)((s_shape[e][2][1] / kPfM) * tiles);
-      off += rows;
+      v[16] = (int64_t)(s_shape[e][0][1] / kPfM) * tiles;
+      v[17] = (int64_t)(s_shape[e][2][1] / kPfM) * tiles;
     }
-    s_ng = ng;
-    s_item[0][ng] = item[0];
-    s_item[1][ng] = item[1];
-    for (int ph = 0; ph < 2; ++ph) {
-      int32_t* c = a.counts + 16 * ph;
-      c[0] = ng;
-      c[1] = blk[ph];
-      c[2] = ntp[ph];
-      c[3] = unit[ph];
-      c[4] = ng;
-      c[5] = item[ph];
-      c[6] = ntmax;
+    // warp inclusive scans, then the warps' totals
+    __shared__ int64_t s_wtot[32][kQ];
+    __shared__ int32_t s_ntmax;
+    if (tid == 0) s_ntmax = 16;
+    int64_t inc[kQ];
+#pragma unroll
+    for (int i = 0; i < kQ; ++i) {
+      int64_t x = v[i];
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int64_t y = __shfl_up_sync(0xffffffffu, x, d);
+        if (lane >= d) x += y;
+      }
+      inc[i] = x;
+      if (lane == 31) s_wtot[warp][i] = x;
+    }
+    __syncthreads();
+    if (nt > 0) atomicMax(&s_ntmax, nt);
+    if (warp == 0) {
+#pragma unroll
+      for (int i = 0; i < kQ; ++i) {
+        const int64_t t = lane < nwarps ? s_wtot[lane][i] : 0;
+        int64_t x = t;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const int64_t y = __shfl_up_sync(0xffffffffu, x, d);
+          if (lane >= d) x += y;
+        }
+        if (lane < nwarps) s_wtot[lane][i] = x - t;  // exclusive warp offsets
+      }
+    }
+    __syncthreads();
+    int64_t ex[kQ];
+#pragma unroll
+    for (int i = 0; i < kQ; ++i) ex[i] = s_wtot[warp][i] + inc[i] - v[i];
+    if (rows > 0) {
+      const int g = (int)ex[0];
+      s_gexp[g] = e;
+      s_off[g] = (int32_t)ex[1];
+      s_o[0][g] = ex[2];
+      s_o[1][g] = ex[3];
+      s_blk[0][g] = (int32_t)ex[4];
+      s_blk[1][g] = (int32_t)ex[5];
+      s_tp[0][g] = (int32_t)ex[14];
+      s_tp[1][g] = (int32_t)ex[15];
+      int64_t u01 = ex[12];  // w1 then w3 within the group (phase-wide prefix)
+      for (int j = 0; j < 3; ++j) {
+        s_o[2 + j][g] = ex[6 + j];
+        s_o[5 + j][g] = ex[9 + j];
+        s_unit[j][g] = 0;
+        if (s_shape[e][j][2] <= 0) continue;
+        const int64_t units = (int64_t)((rows + kTRows - 1) / kTRows) * s_shape[e][j][3] * ks_j[j];
+        if (j < 2) {
+          s_unit[j][g] = (int32_t)u01;
+          u01 += units;
+        } else {
+          s_unit[j][g] = (int32_t)ex[13];
+        }
+      }
+      s_item[0][g] = (int32_t)ex[16];
+      s_item[1][g] = (int32_t)ex[17];
+    }
+    if (tid == blockDim.x - 1) {  // totals: the last thread's inclusive values
+      const int ng = (int)(ex[0] + v[0]);
+      s_ng = ng;
+      s_item[0][ng] = (int32_t)(ex[16] + v[16]);
+      s_item[1][ng] = (int32_t)(ex[17] + v[17]);
+    }
+    __syncthreads();
+    if (tid == blockDim.x - 1) {
+      const int ng = s_ng;
+      for (int ph = 0; ph < 2; ++ph) {
+        int32_t* c = a.counts + 16 * ph;
+        c[0] = ng;
+        c[1] = (int32_t)(ex[4 + ph] + v[4 + ph]);
+        c[2] = (int32_t)(ex[14 + ph] + v[14 + ph]);
+        c[3] = (int32_t)(ex[12 + ph] + v[12 + ph]);
+        c[4] = ng;
+        c[5] = (int32_t)(ex[16 + ph] + v[16 + ph]);
+        c[6] = s_ntmax;
+      }
     }
   }
   __syncthreads();
   const int ng = s_ng;
+  stamp(3);
   // 3. grouped rows: token (x row) and Y slot, entries of an expert in (t, k) order
   for (int g = warp; g < ng; g += nwarps) {
     const int e = s_gexp[g];
     int32_t* tok = a.tok + s_off[g];
     int32_t* slot = a.slot + s_off[g];
-    if (e < E) {
-      int64_t pos = 0;
-      for (int64_t base = 0; base < mK; base += 32) {
-        const int64_t i = base + lane;
-        const bool hit = i < mK && a.ids[i] == e;
+    if (e < E) {  // (32-bit indices: mK < 2^31; a 64-bit division per hit cost ~10 us)
+      const int n = (int)mK;
+      int pos = 0;
+      for (int base = 0; base < n; base += 32) {
+        const int i = base + lane;
+        const bool hit = i < n && ids[i] == e;
         const unsigned b = __ballot_sync(0xffffffffu, hit);
         if (hit) {
-          const int64_t p = pos + __popc(b & ((1u << lane) - 1u));
-          tok[p] = (int32_t)(i / K);
-          slot[p] = (int32_t)i;
+          const int p = pos + __popc(b & ((1u << lane) - 1u));
+          tok[p] = i / K;
+          slot[p] = i;
         }
         pos += __popc(b);
       }
@@ -1546,6 +1628,8 @@ __global__ void __launch_bounds__(1024) moe_plan_kernel(PfPlanArgs a) {
       }
     }
   }
+  __syncthreads();
+  stamp(4);
   // 4. per-group tables (thread per group)
   for (int g = tid; g < ng; g += blockDim.x) {
     const int e = s_gexp[g];
@@ -1658,6 +1742,8 @@ __global__ void __launch_bounds__(1024) moe_plan_kernel(PfPlanArgs a) {
     a.starts[0][ng] = s_item[0][ng];
     a.starts[1][ng] = s_item[1][ng];
   }
+  __syncthreads();
+  stamp(5);
 }
 
 }  // namespace milo_dev

@@ -1,0 +1,4 @@
+cd "${GRAFT_REPO_ROOT:-/root/repo}"; O=gpurun_out; mkdir -p $O
+timeout 900 python -m pytest tests/test_gpu_moe.py tests/test_gpu_real_configs.py -x -q > $O/pt_moe.txt 2>&1
+tail -2 $O/pt_moe.txt
+timeout 300 python tools/timeline.py --batch 256 > $O/tl256.txt 2>&1
