@@ -1069,6 +1069,11 @@ __device__ __forceinline__ void t_tc_load(const TProb& P, int kb, int ch, int ti
     const int nb = 64 * P.rank;
     cv = 16 * tid < nb ? __ldg(reinterpret_cast<const uint4*>(P.ucodes + (int64_t)kb * P.rank + 16 * tid))
                        : make_uint4(0u, 0u, 0u, 0u);
+  } else if (P.rank % 16 == 0) {
+    // codes: k row tid / 4, ranks ch * 64 + 16 (tid % 4) .. + 15: one aligned 16-B load
+    const int kk = tid >> 2, j0 = ch * 64 + (tid & 3) * 16;
+    cv = j0 < P.rank ? __ldg(reinterpret_cast<const uint4*>(P.ucodes + (int64_t)(kb + kk) * P.rank + j0))
+                     : make_uint4(0x04040404u, 0x04040404u, 0x04040404u, 0x04040404u);
   } else {
     // codes: k row tid / 4, ranks ch * 64 + 16 (tid % 4) .. + 15 (past the rank: code 4 -> 0)
     const int kk = tid >> 2, j0 = ch * 64 + (tid & 3) * 16;
