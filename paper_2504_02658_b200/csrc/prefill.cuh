@@ -29,8 +29,8 @@
 
 namespace milo_dev {
 
-#ifndef PF_NG2_GROUPS
-#define PF_NG2_GROUPS 3
+#ifndef PF_GROUPS
+#define PF_GROUPS 3  // dequant groups (4 warps each)
 #endif
 #ifndef PF_PS2
 #define PF_PS2 5  // packed ring slots (128 k each) of the two-matrix / two-n-tile variants
@@ -70,7 +70,7 @@ constexpr int kPfDbgLongs = 148 * 8 + kPfTraceStages * 8;  // dbg region of one 
 // if the slot's barrier is at most one phase behind (st - 2 AS consumed).
 template <int NMAT, int NG = 1>
 struct PfRoles {
-  static constexpr int kGroups = NG == 2 ? PF_NG2_GROUPS : 3;  // stages de-quantized concurrently
+  static constexpr int kGroups = PF_GROUPS;  // stages de-quantized concurrently
   static constexpr int kDeqWarps = kGroups * kPfGroupWarps;
   static constexpr int kThreads = 32 * (kPfDeqWarp0 + kDeqWarps);
 };
