@@ -909,7 +909,7 @@ struct TProb {
 };
 
 #ifndef PF_T_CTAS
-#define PF_T_CTAS 1
+#define PF_T_CTAS 2  // t-kernel k splits target ~2 units per SM (4 CTAs per SM resident)
 #endif
 constexpr int kTRows = 32;  // rows per t-kernel CTA
 constexpr int kTCtasPerSm = PF_T_CTAS;
