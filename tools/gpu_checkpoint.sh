@@ -2,7 +2,7 @@
 # Round-2 checkpoint: full GPU suite, smoke, bench (3 configs), timelines, launch list,
 # ncu full captures of the MoE prefill kernels at batch 256.
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
-O=gpurun_out/r02c; mkdir -p $O
+O=gpurun_out/${CHECKPOINT:-r02c}; mkdir -p $O
 nvidia-smi -L > $O/gpu.txt 2>&1
 timeout 1200 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
