@@ -19,7 +19,7 @@ pytestmark = pytest.mark.gpu
 TOL_MOE = 1e-4
 
 
-def _experts(oracle, gpu, E, d, f, ranks, seed, mode=1):
+def _experts(oracle, gpu, E, d, f, ranks, seed, mode=1, storage=None):
     from tests.helpers import random_comp, random_quantized
     o_ex, g_ex = [], []
     for e in range(E):
@@ -27,7 +27,8 @@ def _experts(oracle, gpu, E, d, f, ranks, seed, mode=1):
         for j, (k, n) in enumerate([(d, f), (d, f), (f, d)]):
             P, _ = random_quantized(oracle, k, n, seed=seed + 31 * e + j, mode=mode)
             r = ranks[e][j]
-            c = random_comp(oracle, k, n, r, seed=seed + 977 * e + j) if r else None
+            st = 1 if storage is None else storage[e][j]
+            c = random_comp(oracle, k, n, r, seed=seed + 977 * e + j, storage=st) if r else None
             ws.append(P)
             cs.append(c)
             gw.append(gpu.Weight(P))
@@ -339,3 +340,26 @@ def test_router_gemm_bit_exact_and_forward_x(gpu, oracle, m, x16):
     out, gids, gw = layer.forward_x(xt, return_routing=True)
     assert np.array_equal(gids.cpu().numpy(), ids)
     assert rel_err(out.cpu().numpy(), want) <= 2.5e-4
+
+
+@pytest.mark.parametrize("m", [96, 200])
+def test_prefill_mixed_compensators(gpu, oracle, m):
+    """The tcgen05 prefill path with every LoRC t variant in one layer: symm-INT3
+    factors of one rank chunk (contiguous code runs), of several chunks with
+    rank % 16 == 0 (16-byte code rows) and != 0 (byte loads), real-valued factors
+    (the CUDA-core t kernel), and a rank-0 matrix; the shared expert's t on all
+    tokens.  f = 256: k % 128 == 0 on both phases."""
+    import torch
+    E, K, d, f = 4, 2, 256, 256
+    ranks = [[8, 70, 96], [32, 0, 64], [80, 16, 40], [128, 24, 4]]
+    storage = [[1, 1, 1], [0, 1, 0], [1, 0, 1], [1, 1, 0]]
+    o_ex, g_ex = _experts(oracle, gpu, E, d, f, ranks, 900, storage=storage)
+    o_sh, g_sh = _experts(oracle, gpu, 1, d, f, [[96, 70, 8]], 1900, storage=[[1, 0, 1]])
+    layer = gpu.MoELayer(g_ex, g_sh, top_k=K)
+    rng = np.random.default_rng(m)
+    x = rng.normal(0, 1, (m, d)).astype(np.float32)
+    logits = rng.normal(0, 1, (m, E)).astype(np.float32)
+    ids, w = oracle.router_topk(logits, K, 0)
+    want = oracle.moe_forward(o_ex, o_sh, x, ids, w)
+    got = layer.forward(torch.from_numpy(x).cuda(), torch.from_numpy(logits).cuda()).cpu().numpy()
+    assert rel_err(got, want) <= TOL_MOE
