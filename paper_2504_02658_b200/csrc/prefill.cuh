@@ -41,6 +41,9 @@ namespace milo_dev {
 #ifndef PF_ISSUERS
 #define PF_ISSUERS 2  // MMA-issuing threads (experiments: 1)
 #endif
+#ifndef PF_KSPLIT
+#define PF_KSPLIT 0  // one-accumulator items with <= 64 tokens: k16 steps split over both issuers (measured ~5 us slower on the w2 phase)
+#endif
 #ifndef PF_MIN_AS
 #define PF_MIN_AS 6
 #endif
@@ -354,7 +357,7 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
   // one accumulator per (n-tile, matrix); a single-accumulator kernel with
   // small token tiles splits each stage's k over two accumulators (one per
   // MMA issuer, summed by the epilogue)
-  const bool ksplit = PF_ISSUERS == 2 && NG * NMAT == 1 && a.ntok_max <= 64;
+  const bool ksplit = PF_KSPLIT && PF_ISSUERS == 2 && NG * NMAT == 1 && a.ntok_max <= 64;
   const int acc_cols = (ksplit ? 2 : NG * NMAT) * mstride;
   // TMEM columns: accumulators (double-buffered when that leaves >= PF_MIN_AS
   // A slots), then the A slots.  The A ring's depth covers the dequant ->
