@@ -30,7 +30,7 @@
 namespace milo_dev {
 
 #ifndef PF_GROUPS
-#define PF_GROUPS 3  // dequant groups (4 warps each)
+#define PF_GROUPS 2  // dequant groups (4 warps each; 2 measured faster than 3 or 4: 96 registers at 17 warps)
 #endif
 #ifndef PF_PS2
 #define PF_PS2 5  // packed ring slots (128 k each) of the two-matrix / two-n-tile variants
