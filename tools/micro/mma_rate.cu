@@ -244,6 +244,70 @@ void run_noisy(long long* d, uint32_t seed = 3) {
   if (seed == 7) printf("   per store warp: 8 x 16x256b.x4 stores + wait::st = %lld cycles\n", h[1]);
 }
 
+// The prefill kernel's issuer form: the whole warp runs the loop, elect.sync inside
+// the asm picks the issuing lane (operands in uniform registers); per stage: PER
+// MMAs and one commit, optionally a poll of a shared-memory counter (always ready).
+template <int PER, int POLL>
+__global__ void __launch_bounds__(128, 1) warp_rate(int n, int stages, long long* out) {
+  __shared__ uint32_t tslot;
+  __shared__ __align__(8) uint64_t ring[8];
+  __shared__ __align__(1024) uint8_t bsm[16384];
+  __shared__ uint32_t ready;
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 8; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&ring[i])));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+    ready = 1u << 30;
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tslot;
+  if (warp == 0) {
+    const uint32_t id = idesc(n);
+    const uint64_t db = desc_sw128(smem_u32(bsm));
+    long long t0 = clock64();
+    for (int s = 0; s < stages; ++s) {
+      if (POLL) {
+        uint32_t v;
+        do {
+          asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(&ready)) : "memory");
+        } while (v <= (uint32_t)s);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+      }
+#pragma unroll
+      for (int j = 0; j < PER; ++j)
+        asm volatile("{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                     "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem),
+                     "r"(tmem + 256u + (uint32_t)((j & 3) * 8)), "l"(db + 2 * (j & 3)), "r"(id), "r"(1));
+      asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+                   "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+                       smem_u32(&ring[s & 7]))
+                   : "memory");
+    }
+    long long t1 = clock64();
+    if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = t1 - t0;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+template <int PER, int POLL>
+void run_warp(long long* d, int n) {
+  long long h[2];
+  const int stages = 2048;
+  for (int rep = 0; rep < 2; ++rep) warp_rate<PER, POLL><<<148, 128>>>(n, stages, d);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) printf("error %s\n", cudaGetErrorString(e));
+  cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+  printf("warp-converged elect issuer: %d MMAs (ts N=%d) + commit%s: %7.1f cyc/stage\n", PER, n,
+         POLL ? " + counter poll + fence" : "", (double)h[0] / stages);
+}
+
 template <int PER, int WAIT>
 void run_stage(long long* d, int n) {
   long long h[2];
@@ -265,6 +329,12 @@ int main() {
   cudaFuncSetAttribute(mma_rate<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(mma_rate<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int iters = 4096;
+  run_stage<4, 0>(d, 64);
+  run_warp<4, 0>(d, 64);
+  run_warp<4, 1>(d, 64);
+  run_stage<8, 0>(d, 64);
+  run_warp<8, 0>(d, 64);
+  return 0;
   run_noisy<0>(d);
   run_noisy<1>(d, 7);
   run_noisy<4>(d, 7);
