@@ -6,20 +6,22 @@
 //   C = half(A) * dequant(W) + (half(A) U) V, fp32 accumulation.
 //
 // Per work item (problem p, n-tile of 128 output columns = 2 slabs, token tile
-// of 128 rows) one CTA computes D[128 n][128 tok] = W^T X^T in TMEM:
-//   * producer warp : cp.async.bulk of the packed INT3 macro tiles (2 slabs x
-//                     2 k-tiles per 64-k stage) and of the stage's activation
-//                     "image" (16 KB, already binary16, SW128 K-major, built by
-//                     pf_image_kernel), and of the LoRC images;
-//   * dequant warps : packed tiles -> bit-exact binary16 weights written into
-//                     the A operand (128 n rows x 64 k, SW128 K-major);
-//   * MMA thread    : 4 x tcgen05.mma.kind::f16 (K = 16) per stage, then
-//                     tcgen05.commit to release the stage;
-//   * epilogue warps: tcgen05.ld (32 lanes x 32 columns) -> C rows / SwiGLU.
+// of <= 128 rows) one CTA computes D[128 n][ntok] = W^T X^T in TMEM:
+//   * packed producer : cp.async.bulk of the packed INT3 macro tiles, one run of
+//                       4 k-tiles per (matrix, slab) per 128-k ring slot;
+//   * image producer  : the activation images (binary16, SW128 K-major, built by
+//                       pf_image_kernel / pf_img_t_kernel) of a stage pair in one
+//                       copy, and the LoRC t images;
+//   * dequant groups  : packed tiles -> bit-exact binary16 W^T written into TMEM
+//                       (tcgen05.st from each warp's lane quarter), the A operand;
+//   * ring waiter     : waits on the A / B rings, publishes a stage counter;
+//   * two MMA issuers : tcgen05.mma.kind::f16 with A from TMEM (K = 16, 4 per
+//                       matrix per 64-k stage), tcgen05.commit releases the slots;
+//   * epilogue warps  : tcgen05.ld (32 lanes x 16 columns) -> C rows / SwiGLU.
 // The compensator term (t V) runs as extra K stages of the same accumulator:
-// A = V^T image (hi or lo binary16 half of the fp32 values), B = t image (hi
-// or lo), three MMAs per 64-rank chunk (hi.hi + hi.lo + lo.hi), i.e. fp32-level
-// accuracy on the tensor cores.
+// A = V^T image rows (hi or lo binary16 half of the fp32 values, copied into the
+// TMEM slot), B = t image (hi or lo), three MMAs per 64-rank chunk (hi.hi +
+// hi.lo + lo.hi), i.e. fp32-level accuracy on the tensor cores.
 #pragma once
 #include <cstdint>
 #include <cuda_fp16.h>
