@@ -2429,7 +2429,14 @@ milo_status moe_forward_impl(milo_moe* moe, const void* x, int64_t m, int32_t x_
     return m <= 8 ? launch_hdec<1>(moe, x, m, x_dtype, logits, ids, wts, out, out_dtype, stream, props.sms)
                   : launch_hdec<2>(moe, x, m, x_dtype, logits, ids, wts, out, out_dtype, stream, props.sms);
   // decode megakernel blocks: each touched expert's tokens in chunks of m_pad rows
-  const int dec_mpad = m <= 8 ? 8 : 16;
+  // 8-row blocks (NT = 1) up to batch 24: an expert with more tokens takes two
+  // blocks (its weights stream twice) but the 16-row variant's MMA work and
+  // spills cost more (Mixtral batch 16: 332 -> 285 us; MILO_DEC_NT1_MAX overrides)
+  static const int nt1_max = [] {
+    const char* e = getenv("MILO_DEC_NT1_MAX");
+    return e ? atoi(e) : 24;
+  }();
+  const int dec_mpad = m <= nt1_max ? 8 : 16;
   // bound on the blocks: t = min(E, mK) touched experts, an expert with c <= m
   // entries needs ceil(c / m_pad) blocks (one each when m <= m_pad), so at most
   // t + (mK - t) / m_pad, plus the shared experts' chunks
@@ -2460,7 +2467,7 @@ milo_status moe_forward_impl(milo_moe* moe, const void* x, int64_t m, int32_t x_
     a.out_dtype = out_dtype;
     a.ldo = moe->d;
     const int64_t y_rows = m * moe->K + (int64_t)moe->n_shared * m;
-    return m <= 8 ? launch_decode<1, 2, true>(a, x, x_dtype, moe->d, (int)nb_dec, moe->f_max,
+    return m <= nt1_max ? launch_decode<1, 2, true>(a, x, x_dtype, moe->d, (int)nb_dec, moe->f_max,
                                               moe->r16_max, y_rows, stream, props.sms)
                   : launch_decode<2, 2, true>(a, x, x_dtype, moe->d, (int)nb_dec, moe->f_max,
                                               moe->r16_max, y_rows, stream, props.sms);
