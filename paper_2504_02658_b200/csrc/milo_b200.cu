@@ -1164,7 +1164,7 @@ struct ImgTPlan {
     int dev = 0;
     cudaGetDevice(&dev);
     if (configured_dev != dev) {
-      cudaError_t e = cudaFuncSetAttribute(pf_img_t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kImgTSmem);
+      cudaError_t e = cudaFuncSetAttribute(pf_img_t_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kImgTSmem);
       if (e != cudaSuccess) return e;
       configured_dev = dev;
     }
@@ -1175,8 +1175,10 @@ struct ImgTPlan {
       e = h2d_async(table + jb, tps.data(), tps.size() * sizeof(TProb), stream);
       if (e != cudaSuccess) return e;
     }
-    e = launch(pf_img_t_kernel, dim3((unsigned)blocks), dim3(256), kImgTSmem, stream, false,
-               (const ImgJob*)table, (int)jobs.size(), (const int32_t*)nullptr);
+    e = fuse_t ? launch(pf_img_t_kernel<true>, dim3((unsigned)blocks), dim3(256), kImgTSmem, stream, false,
+                        (const ImgJob*)table, (int)jobs.size(), (const int32_t*)nullptr)
+               : launch(pf_img_t_kernel<false>, dim3((unsigned)blocks), dim3(256), 0, stream, false,
+                        (const ImgJob*)table, (int)jobs.size(), (const int32_t*)nullptr);
     if (e != cudaSuccess || tps.empty()) return e;
     return launch(pf_t_images_kernel, dim3(256, (unsigned)tps.size()), dim3(256), 0, stream, false,
                   (const TProb*)(table + jb), (int)tps.size(), (const int32_t*)nullptr);
@@ -2254,7 +2256,7 @@ milo_status moe_prefill_dev(milo_moe* moe, const void* x, int64_t m, int32_t x_d
   int dev = 0;
   cudaGetDevice(&dev);
   if (configured_dev != dev) {
-    CUDA_TRY(cudaFuncSetAttribute(pf_img_t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kImgTSmem));
+    CUDA_TRY(cudaFuncSetAttribute(pf_img_t_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kImgTSmem));
     CUDA_TRY(set_smem(pf_gemm_kernel<2, 1>, PfCfg<2, 1>::kBytes));
     CUDA_TRY(set_smem(pf_gemm_kernel<1, 1>, PfCfg<1, 1>::kBytes));
     configured_dev = dev;
@@ -2262,7 +2264,7 @@ milo_status moe_prefill_dev(milo_moe* moe, const void* x, int64_t m, int32_t x_d
   for (int ph = 0; ph < 2; ++ph) {
     const int32_t* cnt = pa.counts + 16 * ph;
     // activation images (+ gathered rows) and LoRC t = x U -> hi / lo images
-    CUDA_TRY(launch(pf_img_t_kernel, dim3((unsigned)(sms * 8)), dim3(256), kImgTSmem, stream, false,
+    CUDA_TRY(launch(pf_img_t_kernel<false>, dim3((unsigned)(sms * 8)), dim3(256), 0, stream, false,
                     (const ImgJob*)pa.jobs[ph], 0, cnt));
     if (moe->t_kinds[ph] & 1)
       CUDA_TRY(launch(pf_t_kernel<0>, dim3((unsigned)(sms * 8)), dim3(256), 0, stream, false, (const TProb*)pa.tps[ph],

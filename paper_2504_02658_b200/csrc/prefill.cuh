@@ -1257,6 +1257,7 @@ struct ImgJob {
 };
 constexpr int kImgTSmem = (kPfN * 65 + 64 * 65) * 4;
 
+template <bool WITH_T>
 __device__ __forceinline__ void pf_img_t_unit(const ImgJob* __restrict__ jobs, int n_jobs, int blk) {
   extern __shared__ float imgt_sm[];
   float* sx = imgt_sm;             // [ntok][65]
@@ -1279,7 +1280,7 @@ __device__ __forceinline__ void pf_img_t_unit(const ImgJob* __restrict__ jobs, i
     if (row < J.rows)
       pf_load_block16(J.x, J.x_dtype, J.row_ids ? J.row_ids[row] : row, J.ldx, (int64_t)st * kPfK + b * 16, w);
     pf_store_block16(dst, r, b, w);
-    if (J.n_t > 0) {
+    if (WITH_T && J.n_t > 0) {
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const float2 f = __half22float2(u32_as_h2(w[u]));
@@ -1288,7 +1289,7 @@ __device__ __forceinline__ void pf_img_t_unit(const ImgJob* __restrict__ jobs, i
       }
     }
   }
-  if (J.n_t == 0) return;
+  if (!WITH_T || J.n_t == 0) return;
   const int j = tid & 63, rg = tid >> 6;  // rank column, row group (rows rg, rg + 4, ...)
   const int nr4 = ntok / 4;               // rows per thread (ntok is a multiple of 16)
   for (int ti = 0; ti < J.n_t; ++ti) {
@@ -1332,17 +1333,20 @@ __device__ __forceinline__ void pf_img_t_unit(const ImgJob* __restrict__ jobs, i
 
 // dev_counts (nullable): {n_jobs, blocks} written by moe_plan_kernel; the CTAs
 // then loop over the planned blocks (grid-stride), else CTA = block.
+// WITH_T = false: images only (the MoE prefill plan computes t separately) -- a
+// small register footprint, so many CTAs per SM (the t variant holds ~170).
+template <bool WITH_T>
 __global__ void __launch_bounds__(256) pf_img_t_kernel(const ImgJob* __restrict__ jobs, int n_jobs,
                                                       const int32_t* __restrict__ dev_counts) {
   pdl_wait();  // inputs come from the preceding grid (programmatic dependent launch)
   if (dev_counts == nullptr) {
-    pf_img_t_unit(jobs, n_jobs, blockIdx.x);
+    pf_img_t_unit<WITH_T>(jobs, n_jobs, blockIdx.x);
     return;
   }
   n_jobs = dev_counts[0];
   const int blocks = dev_counts[1];
   for (int b = blockIdx.x; b < blocks; b += gridDim.x) {
-    pf_img_t_unit(jobs, n_jobs, b);
+    pf_img_t_unit<WITH_T>(jobs, n_jobs, b);
     __syncthreads();
   }
 }
