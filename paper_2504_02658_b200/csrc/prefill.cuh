@@ -1361,12 +1361,16 @@ __global__ void pf_t_images_kernel(const TProb* __restrict__ probs, int n_probs,
   const int r64 = P.rchunks * 64;
   const int ntok = P.ntok;
   const int tiles = (P.rows + ntok - 1) / ntok;
-  const int64_t total = (int64_t)tiles * ntok * r64;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int row = (int)(e / r64), c = (int)(e % r64);
+  const int total = tiles * ntok * r64;  // 32-bit index math (64-bit divisions are software routines)
+  const int64_t sstride = (int64_t)P.rows * r64;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    const int row = (e >> 6) / P.rchunks, c = e - row * r64;
     float t = 0.0f;
-    if (row < P.rows)
-      for (int s = 0; s < P.ks; ++s) t += P.part[((int64_t)s * P.rows + row) * r64 + c];
+    if (row < P.rows) {
+      const float* pp = P.part + (int64_t)row * r64 + c;
+#pragma unroll 4
+      for (int s = 0; s < P.ks; ++s) t += pp[s * sstride];
+    }
     const __half h = __float2half_rn(t);
     const __half l = __float2half_rn(t - __half2float(h));
     const int tile = row / ntok, r = row % ntok, ch = c / 64, jj = c % 64;
