@@ -2240,7 +2240,8 @@ milo_status moe_prefill_dev(milo_moe* moe, const void* x, int64_t m, int32_t x_d
   // (programmatic launches of this chain measured no faster: the early CTAs of
   // each dependent grid hold SM slots while the previous grid drains)
   pa.dbg = g_dbg ? g_dbg + 2 * kPfDbgLongs : nullptr;  // after the two GEMM phases' regions
-  const size_t ids_smem = (size_t)m * K * 4;
+  // cached ids + the per-warp expert histograms of the window scans
+  const size_t ids_smem = (((size_t)m * K + 3) & ~size_t(3)) * 4 + (size_t)32 * kPlanMaxGroups * 4;
   pa.ids_cached = ids_smem <= kPlanIdsSmem ? 1 : 0;
   {
     static thread_local int plan_dev = -1;

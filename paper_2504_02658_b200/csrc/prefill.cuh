@@ -1458,6 +1458,7 @@ __global__ void __launch_bounds__(1024) moe_plan_kernel(PfPlanArgs a) {
   __shared__ int32_t s_cnt[kPlanMaxGroups];   // rows per expert (routed, shared)
   __shared__ int32_t s_off[kPlanMaxGroups];   // grouped row offset
   __shared__ int32_t s_gexp[kPlanMaxGroups];  // group -> expert
+  __shared__ int32_t s_gofe[kPlanMaxGroups];  // expert -> group
   __shared__ int64_t s_o[8][kPlanMaxGroups];  // per group: img1, img2, timg0..2, part0..2 byte offsets
   __shared__ int32_t s_blk[2][kPlanMaxGroups], s_unit[3][kPlanMaxGroups], s_item[2][kPlanMaxGroups + 1];
   __shared__ int32_t s_ng;
@@ -1483,8 +1484,38 @@ __global__ void __launch_bounds__(1024) moe_plan_kernel(PfPlanArgs a) {
     s_shape[i / 3][i % 3][3] = M.rch;
   }
   stamp(1);
-  // 1. rows per expert: one warp per expert scans the entries with ballots
-  for (int e = warp; e < E + S; e += nwarps) {
+  // 1. rows per expert.  Cached ids: warp w counts the experts of its contiguous
+  //    chunk of entries (__match_any_sync per 32-entry window) into hist[w][e],
+  //    then thread e turns the counts into per-warp offsets (step 3 reuses them)
+  //    and its total.  Otherwise one warp per expert scans every entry.
+  const int n_ent = (int)mK;
+  const int chunk = ((n_ent + nwarps * 32 - 1) / (nwarps * 32)) * 32;
+  int32_t* hist = s_ids + ((n_ent + 3) & ~3);  // [nwarps][kPlanMaxGroups] (cached path)
+  if (a.ids_cached) {
+    for (int i = tid; i < nwarps * kPlanMaxGroups; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    const int b0 = warp * chunk, b1 = min(n_ent, b0 + chunk);
+    for (int base = b0; base < b1; base += 32) {
+      const int i = base + lane;
+      const int e = i < b1 ? ids[i] : -1;
+      const unsigned peers = __match_any_sync(0xffffffffu, e);
+      if (e >= 0 && e < E && lane == __ffs(peers) - 1) hist[warp * kPlanMaxGroups + e] += __popc(peers);
+      __syncwarp();
+    }
+    __syncthreads();
+    if (tid < E) {
+      int run = 0;
+      for (int w = 0; w < nwarps; ++w) {
+        const int c = hist[w * kPlanMaxGroups + tid];
+        hist[w * kPlanMaxGroups + tid] = run;
+        run += c;
+      }
+      s_cnt[tid] = run;
+    } else if (tid < E + S) {
+      s_cnt[tid] = (int32_t)m;
+    }
+  }
+  for (int e = warp; !a.ids_cached && e < E + S; e += nwarps) {
     int64_t c = 0;
     if (e < E) {
       const int n = (int)mK;
@@ -1505,7 +1536,8 @@ __global__ void __launch_bounds__(1024) moe_plan_kernel(PfPlanArgs a) {
   //    loop over the groups cost 70-100 us at 66-128 experts)
   {
     constexpr int kQ = 18;  // scanned quantities
-    int64_t v[kQ];
+    // 32-bit scans: byte offsets in 256-byte units (every region is 256-aligned)
+    int32_t v[kQ];
 #pragma unroll
     for (int i = 0; i < kQ; ++i) v[i] = 0;
     const int e = tid;
@@ -1517,34 +1549,34 @@ __global__ void __launch_bounds__(1024) moe_plan_kernel(PfPlanArgs a) {
       v[0] = 1;     // group index
       v[1] = rows;  // grouped row offset
       // images: phase 1 over d, phase 2 over this expert's f (regions sized with f_max)
-      v[2] = ((int64_t)tiles * (a.d / kPfK) * nt * 128 + 255) & ~int64_t(255);
-      v[3] = ((int64_t)tiles * (a.f_max / kPfK) * nt * 128 + 255) & ~int64_t(255);
-      v[4] = (int64_t)tiles * (a.d / kPfK);
-      v[5] = (int64_t)tiles * (s_shape[e][2][0] / kPfK);
+      v[2] = (int32_t)(((int64_t)tiles * (a.d / kPfK) * nt * 128 + 255) >> 8);
+      v[3] = (int32_t)(((int64_t)tiles * (a.f_max / kPfK) * nt * 128 + 255) >> 8);
+      v[4] = tiles * (int)(a.d / kPfK);
+      v[5] = tiles * (s_shape[e][2][0] / kPfK);
       for (int j = 0; j < 3; ++j) {
         const int mk = s_shape[e][j][0], rank = s_shape[e][j][2], rch = s_shape[e][j][3];
         if (rank <= 0) continue;
-        v[6 + j] = ((int64_t)tiles * rch * 2 * nt * 128 + 255) & ~int64_t(255);
+        v[6 + j] = (int32_t)(((int64_t)tiles * rch * 2 * nt * 128 + 255) >> 8);
         const int ks = pf_t_splits_dev(rows, mk, rch, a.sms);
         ks_j[j] = ks;
-        v[9 + j] = ((int64_t)max(mk / kPfK, ks) * rows * rch * 64 * 4 + 255) & ~int64_t(255);
-        v[12 + (j == 2 ? 1 : 0)] += (int64_t)((rows + kTRows - 1) / kTRows) * rch * ks;  // t units per phase
+        v[9 + j] = (int32_t)(((int64_t)max(mk / kPfK, ks) * rows * rch * 64 * 4 + 255) >> 8);
+        v[12 + (j == 2 ? 1 : 0)] += ((rows + kTRows - 1) / kTRows) * rch * ks;  // t units per phase
         v[14 + (j == 2 ? 1 : 0)] += 1;                                                  // t problems per phase
       }
-      v[16] = (int64_t)(s_shape[e][0][1] / kPfM) * tiles;
-      v[17] = (int64_t)(s_shape[e][2][1] / kPfM) * tiles;
+      v[16] = (s_shape[e][0][1] / kPfM) * tiles;
+      v[17] = (s_shape[e][2][1] / kPfM) * tiles;
     }
     // warp inclusive scans, then the warps' totals
-    __shared__ int64_t s_wtot[32][kQ];
+    __shared__ int32_t s_wtot[32][kQ];
     __shared__ int32_t s_ntmax;
     if (tid == 0) s_ntmax = 16;
-    int64_t inc[kQ];
+    int32_t inc[kQ];
 #pragma unroll
     for (int i = 0; i < kQ; ++i) {
-      int64_t x = v[i];
+      int32_t x = v[i];
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
-        const int64_t y = __shfl_up_sync(0xffffffffu, x, d);
+        const int32_t y = __shfl_up_sync(0xffffffffu, x, d);
         if (lane >= d) x += y;
       }
       inc[i] = x;
@@ -1555,37 +1587,38 @@ __global__ void __launch_bounds__(1024) moe_plan_kernel(PfPlanArgs a) {
     if (warp == 0) {
 #pragma unroll
       for (int i = 0; i < kQ; ++i) {
-        const int64_t t = lane < nwarps ? s_wtot[lane][i] : 0;
-        int64_t x = t;
+        const int32_t t = lane < nwarps ? s_wtot[lane][i] : 0;
+        int32_t x = t;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
-          const int64_t y = __shfl_up_sync(0xffffffffu, x, d);
+          const int32_t y = __shfl_up_sync(0xffffffffu, x, d);
           if (lane >= d) x += y;
         }
         if (lane < nwarps) s_wtot[lane][i] = x - t;  // exclusive warp offsets
       }
     }
     __syncthreads();
-    int64_t ex[kQ];
+    int32_t ex[kQ];
 #pragma unroll
     for (int i = 0; i < kQ; ++i) ex[i] = s_wtot[warp][i] + inc[i] - v[i];
     if (rows > 0) {
       const int g = (int)ex[0];
       s_gexp[g] = e;
+      s_gofe[e] = g;
       s_off[g] = (int32_t)ex[1];
-      s_o[0][g] = ex[2];
-      s_o[1][g] = ex[3];
+      s_o[0][g] = (int64_t)ex[2] << 8;
+      s_o[1][g] = (int64_t)ex[3] << 8;
       s_blk[0][g] = (int32_t)ex[4];
       s_blk[1][g] = (int32_t)ex[5];
       s_tp[0][g] = (int32_t)ex[14];
       s_tp[1][g] = (int32_t)ex[15];
-      int64_t u01 = ex[12];  // w1 then w3 within the group (phase-wide prefix)
+      int32_t u01 = ex[12];  // w1 then w3 within the group (phase-wide prefix)
       for (int j = 0; j < 3; ++j) {
-        s_o[2 + j][g] = ex[6 + j];
-        s_o[5 + j][g] = ex[9 + j];
+        s_o[2 + j][g] = (int64_t)ex[6 + j] << 8;
+        s_o[5 + j][g] = (int64_t)ex[9 + j] << 8;
         s_unit[j][g] = 0;
         if (s_shape[e][j][2] <= 0) continue;
-        const int64_t units = (int64_t)((rows + kTRows - 1) / kTRows) * s_shape[e][j][3] * ks_j[j];
+        const int32_t units = ((rows + kTRows - 1) / kTRows) * s_shape[e][j][3] * ks_j[j];
         if (j < 2) {
           s_unit[j][g] = (int32_t)u01;
           u01 += units;
@@ -1621,10 +1654,28 @@ __global__ void __launch_bounds__(1024) moe_plan_kernel(PfPlanArgs a) {
   const int ng = s_ng;
   stamp(3);
   // 3. grouped rows: token (x row) and Y slot, entries of an expert in (t, k) order
+  if (a.ids_cached) {  // the same windows as step 1: offset = group + earlier warps + rank in the window
+    const int b0 = warp * chunk, b1 = min(n_ent, b0 + chunk);
+    for (int base = b0; base < b1; base += 32) {
+      const int i = base + lane;
+      const int e = i < b1 ? ids[i] : -1;
+      const unsigned peers = __match_any_sync(0xffffffffu, e);
+      if (e >= 0 && e < E) {
+        int32_t* h = hist + warp * kPlanMaxGroups + e;
+        const int p = s_off[s_gofe[e]] + *h + __popc(peers & ((1u << lane) - 1u));
+        a.tok[p] = i / K;
+        a.slot[p] = i;
+      }
+      __syncwarp();
+      if (e >= 0 && e < E && lane == __ffs(peers) - 1) hist[warp * kPlanMaxGroups + e] += __popc(peers);
+      __syncwarp();
+    }
+  }
   for (int g = warp; g < ng; g += nwarps) {
     const int e = s_gexp[g];
     int32_t* tok = a.tok + s_off[g];
     int32_t* slot = a.slot + s_off[g];
+    if (e < E && a.ids_cached) continue;  // done above
     if (e < E) {  // (32-bit indices: mK < 2^31; a 64-bit division per hit cost ~10 us)
       const int n = (int)mK;
       int pos = 0;
