@@ -45,6 +45,7 @@
 
 #include "gemv.cuh"
 #include "layout.cuh"
+#include "moe.cuh"
 #include "ptx.cuh"
 
 namespace milo_dev {
@@ -567,74 +568,6 @@ __device__ __forceinline__ void add_tv(float (&acc)[4][NT][4], const DecMat& M, 
           acc[i][nt][2 * h] += sv[2 * i + h] * D[i][nt][2 * h];
           acc[i][nt][2 * h + 1] += sv[2 * i + h] * D[i][nt][2 * h + 1];
         }
-  }
-}
-
-// Top-k of one token's logits by one warp (descending, ties -> lower id) and
-// its routing weights (score_mode 0: softmax over the top-k, Mixtral; 1:
-// softmax over all experts, DeepSeek).  E <= 256: 8 logits per lane.
-__device__ __forceinline__ void topk_regs(const float* __restrict__ l, int E, int K, int score_mode,
-                                          int32_t* ids, float* wts, int lane) {
-  float v[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int e = lane + 32 * i;
-    v[i] = e < E ? __ldg(l + e) : -INFINITY;
-  }
-  float mx_all = -INFINITY;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) mx_all = fmaxf(mx_all, v[i]);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mx_all = fmaxf(mx_all, __shfl_xor_sync(0xffffffffu, mx_all, o));
-  uint32_t used = 0u;  // bit i: v[i] of this lane taken
-  // the selected (value, id) of step k stay on lane k (K <= 16 < 32): no local arrays
-  float my_v = -INFINITY;
-  int my_e = -1;
-  for (int k = 0; k < K; ++k) {
-    float best = -INFINITY;
-    int bid = 0x7fffffff;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int e = lane + 32 * i;
-      if (e < E && !(used >> i & 1u) && (bid == 0x7fffffff || v[i] > best)) {
-        best = v[i];
-        bid = e;
-      }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const float ov = __shfl_xor_sync(0xffffffffu, best, o);
-      const int oid = __shfl_xor_sync(0xffffffffu, bid, o);
-      if (oid != 0x7fffffff && (bid == 0x7fffffff || ov > best || (ov == best && oid < bid))) {
-        best = ov;
-        bid = oid;
-      }
-    }
-    if ((bid & 31) == lane) used |= 1u << (bid >> 5);
-    if (lane == k) {
-      my_v = best;
-      my_e = bid;
-    }
-  }
-  // weights: lane k < K owns selection k (Mixtral: softmax over the top-k;
-  // DeepSeek: softmax over all experts)
-  const float top0 = __shfl_sync(0xffffffffu, my_v, 0);
-  float num, denom;
-  if (score_mode == 0) {
-    num = lane < K ? expf(my_v - top0) : 0.0f;
-    denom = num;
-  } else {
-    num = lane < K ? expf(my_v - mx_all) : 0.0f;
-    denom = 0.0f;
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-      if (lane + 32 * i < E) denom += expf(v[i] - mx_all);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) denom += __shfl_xor_sync(0xffffffffu, denom, o);
-  if (lane < K) {
-    ids[lane] = my_e;
-    wts[lane] = num / denom;
   }
 }
 

@@ -25,21 +25,34 @@ namespace milo_dev {
 // ---------------------------------------------------------------------------
 // router
 // ---------------------------------------------------------------------------
-// One warp: top-K of one token's logits (descending, ties -> lower id) and
-// its routing weights; lane 0 writes ids/wts[t*K ...].
-__device__ __forceinline__ void topk_warp(const float* __restrict__ l, int64_t t, int E, int K,
-                                          int score_mode, int32_t* __restrict__ ids,
-                                          float* __restrict__ wts, int lane) {
-  int sel[16];
+// Top-k of one token's logits by one warp (descending, ties -> lower id) and
+// its routing weights (score_mode 0: softmax over the top-k, Mixtral; 1:
+// softmax over all experts, DeepSeek).  E <= 256: 8 logits per lane.
+__device__ __forceinline__ void topk_regs(const float* __restrict__ l, int E, int K, int score_mode,
+                                          int32_t* ids, float* wts, int lane) {
+  float v[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int e = lane + 32 * i;
+    v[i] = e < E ? __ldg(l + e) : -INFINITY;
+  }
+  float mx_all = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) mx_all = fmaxf(mx_all, v[i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx_all = fmaxf(mx_all, __shfl_xor_sync(0xffffffffu, mx_all, o));
+  uint32_t used = 0u;  // bit i: v[i] of this lane taken
+  // the selected (value, id) of step k stay on lane k (K <= 16 < 32): no local arrays
+  float my_v = -INFINITY;
+  int my_e = -1;
   for (int k = 0; k < K; ++k) {
     float best = -INFINITY;
     int bid = 0x7fffffff;
-    for (int e = lane; e < E; e += 32) {
-      bool used = false;
-      for (int q = 0; q < k; ++q) used |= (sel[q] == e);
-      const float v = l[e];
-      if (!used && (v > best || (v == best && e < bid) || bid == 0x7fffffff)) {
-        best = v;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int e = lane + 32 * i;
+      if (e < E && !(used >> i & 1u) && (bid == 0x7fffffff || v[i] > best)) {
+        best = v[i];
         bid = e;
       }
     }
@@ -52,30 +65,39 @@ __device__ __forceinline__ void topk_warp(const float* __restrict__ l, int64_t t
         bid = oid;
       }
     }
-    sel[k] = bid;
-  }
-  if (lane == 0) {
-    float w[16];
-    if (score_mode == 0) {
-      const float mx = l[sel[0]];
-      float sum = 0.0f;
-      for (int k = 0; k < K; ++k) {
-        w[k] = expf(l[sel[k]] - mx);
-        sum += w[k];
-      }
-      for (int k = 0; k < K; ++k) w[k] = w[k] / sum;
-    } else {
-      float mx = l[0];
-      for (int e = 1; e < E; ++e) mx = l[e] > mx ? l[e] : mx;
-      float sum = 0.0f;
-      for (int e = 0; e < E; ++e) sum += expf(l[e] - mx);
-      for (int k = 0; k < K; ++k) w[k] = expf(l[sel[k]] - mx) / sum;
-    }
-    for (int k = 0; k < K; ++k) {
-      ids[t * K + k] = sel[k];
-      wts[t * K + k] = w[k];
+    if ((bid & 31) == lane) used |= 1u << (bid >> 5);
+    if (lane == k) {
+      my_v = best;
+      my_e = bid;
     }
   }
+  // weights: lane k < K owns selection k (Mixtral: softmax over the top-k;
+  // DeepSeek: softmax over all experts)
+  const float top0 = __shfl_sync(0xffffffffu, my_v, 0);
+  float num, denom;
+  if (score_mode == 0) {
+    num = lane < K ? expf(my_v - top0) : 0.0f;
+    denom = num;
+  } else {
+    num = lane < K ? expf(my_v - mx_all) : 0.0f;
+    denom = 0.0f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (lane + 32 * i < E) denom += expf(v[i] - mx_all);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) denom += __shfl_xor_sync(0xffffffffu, denom, o);
+  if (lane < K) {
+    ids[lane] = my_e;
+    wts[lane] = num / denom;
+  }
+}
+
+// One warp per token (the prefill router): topk_regs into ids / wts[t K ...].
+__device__ __forceinline__ void topk_warp(const float* __restrict__ l, int64_t t, int E, int K,
+                                          int score_mode, int32_t* __restrict__ ids,
+                                          float* __restrict__ wts, int lane) {
+  topk_regs(l, E, K, score_mode, ids + t * K, wts + t * K, lane);
 }
 
 __global__ void router_topk_kernel(const float* __restrict__ logits, int64_t m, int E, int K,
