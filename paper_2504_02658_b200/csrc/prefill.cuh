@@ -770,7 +770,9 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
       int p, nt, tt;
       pf_item<NG>(a, item, p, nt, tt);
       const PfProblem P = a.problems[p];  // by value: fields live in registers
+      PF_LAP(2);
       ring_wait(&acc_full[acc], acc_phase);
+      PF_LAP(0);
       tc_fence_after();
       if (threadIdx.x == 0) pf_dbg(6);
       // TMEM -> registers (thread = output column, 32 tokens per load) -> SwiGLU /
@@ -828,11 +830,13 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[acc]);
+      PF_LAP(1);
       if (++acc == nacc) {
         acc = 0;
         acc_phase ^= 1;
       }
     }
+    if (warp == 0 && lane == 0) PF_PROF_OUT(5);
   }
   if (threadIdx.x == 0) pf_dbg(5);
   __syncthreads();

@@ -84,7 +84,8 @@ for ph in range(2):
     if os.environ.get("MILO_B200_LIB_VARIANT"):  # PF_PROF build: per-role cycle split of CTA 0
         roles = [("MMA issuer 0", ["wait stage", "MMAs", "commits"]), ("ring waiter", ["wait A", "wait B", "publish"]),
                  ("B producer", ["wait slot", "copy"]), ("packed producer", ["wait slot", "copies"]),
-                 ("dequant w0", ["wait A slot", "wait packed", "dequant+st", "tail/idle"])]
+                 ("dequant w0", ["wait A slot", "wait packed", "dequant+st", "tail/idle"]),
+                 ("epilogue w0", ["wait acc", "drain", "item setup"])]
         for r, (nm, parts) in enumerate(roles):
             raw = dd[148 * 8 + (TS - 1 - r) * 8:148 * 8 + (TS - 1 - r) * 8 + 4]
             tot = raw.sum()
