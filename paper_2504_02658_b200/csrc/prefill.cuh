@@ -58,7 +58,10 @@ constexpr int kPfK = 64;               // k per stage (128 B of binary16 per ope
 constexpr int kPfImg = kPfN * kPfK * 2;  // 16 KB: one operand image (128 rows x 128 B)
 constexpr int kPfPackedPerMat = 2 * 2 * kTileBytes;  // 2 slabs x 2 k-tiles = 3584 B
 constexpr int kPfGroupWarps = 4;       // warps per dequant group = the 4 TMEM lane quarters
-constexpr int kPfEpiWarps = 4;         // warps 0..3: TMEM lanes 32 w .. 32 w + 31
+#ifndef PF_EPI_HALVES
+#define PF_EPI_HALVES 2  // epilogue warps per TMEM lane quarter (the second four follow the dequant groups)
+#endif
+constexpr int kPfEpiWarps = 4 * PF_EPI_HALVES;  // warps 0..3 (+ the last 4): TMEM lanes 32 (w % 4) ..
 constexpr int kPfProdWarp = 4;         // packed-weight producer
 constexpr int kPfMmaWarp = 5;
 constexpr int kPfBWarp = 6;            // activation / t image producer
@@ -77,7 +80,7 @@ template <int NMAT, int NG = 1>
 struct PfRoles {
   static constexpr int kGroups = PF_GROUPS;  // stages de-quantized concurrently
   static constexpr int kDeqWarps = kGroups * kPfGroupWarps;
-  static constexpr int kThreads = 32 * (kPfDeqWarp0 + kDeqWarps);
+  static constexpr int kThreads = 32 * (kPfDeqWarp0 + kDeqWarps + 4 * (PF_EPI_HALVES - 1));
 };
 
 // The de-quantized weights (the MMA's A operand, W^T) live in TENSOR memory:
@@ -543,7 +546,7 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
       PF_PROF_OUT(2);
       pf_dbg(2);
     }
-  } else if (warp >= kPfDeqWarp0) {
+  } else if (warp >= kPfDeqWarp0 && warp < kPfDeqWarp0 + PfRoles<NMAT, NG>::kDeqWarps) {
     // ======================= dequant warps =======================
     // group grp handles the stages st = grp (mod kPfDeqGroups); within a stage,
     // warp w writes TMEM lane quarter Q = w % 4 (the only lanes its tcgen05.st
@@ -762,8 +765,10 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
       }
     }
   } else {
-    // ======================= epilogue warps 0..3 =======================
-    const int ew = warp;  // TMEM lanes 32 ew .. 32 ew + 31 = A rows (output columns)
+    // ======================= epilogue warps =======================
+    // quarter ew: TMEM lanes 32 ew .. 32 ew + 31 = A rows (output columns); with two
+    // warps per quarter they take alternate 16-token passes
+    const int ew = warp & 3, eh = warp < 4 ? 0 : 1;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
@@ -780,14 +785,14 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
       const int rows = P.rows, kind = P.kind, odt = P.out_dtype;
       const int64_t ldo = P.ldo;
       const int32_t* rmap = P.row_map;
-      float* stg = reinterpret_cast<float*>(smem + CF::kOffStage) + ew * 16 * 33;
+      float* stg = reinterpret_cast<float*>(smem + CF::kOffStage) + (ew + 4 * eh) * 16 * 33;
       const int ntok = P.ntok;
 #pragma unroll 1
       for (int ng = 0; ng < NG; ++ng) {
       const uint32_t tbase = tmem + ((uint32_t)(32 * ew) << 16) + (uint32_t)(acc * acc_cols + ng * NMAT * mstride);
       const int col0 = (NG * nt + ng) * kPfM + 32 * ew + 8 * (lane & 3);  // this lane's 8 output columns
 #pragma unroll 1
-      for (int c0 = 0; c0 < ntok; c0 += 16) {  // 16 tokens per pass (register budget of 640+ threads)
+      for (int c0 = 16 * eh; c0 < ntok; c0 += 16 * PF_EPI_HALVES) {  // 16 tokens per pass
         uint32_t v0[16], v1[16];
         tmem_ld16(tbase + (uint32_t)c0, v0);
         if (NMAT == 2 || ksplit) tmem_ld16(tbase + (uint32_t)(mstride + c0), v1);
