@@ -2240,6 +2240,12 @@ milo_status moe_prefill_dev(milo_moe* moe, const void* x, int64_t m, int32_t x_d
   // (programmatic launches of this chain measured no faster: the early CTAs of
   // each dependent grid hold SM slots while the previous grid drains)
   pa.dbg = g_dbg ? g_dbg + 2 * kPfDbgLongs : nullptr;  // after the two GEMM phases' regions
+  // w2 items of two n-tiles (one activation image feeds two MMAs; half the items)
+  static const int ng2_env = [] {
+    const char* e = getenv("MILO_PF_NG2");
+    return e ? atoi(e) : 1;
+  }();
+  pa.ng2 = (ng2_env && d % (2 * kPfM) == 0) ? 1 : 0;
   // cached ids + the per-warp expert histograms of the window scans
   const size_t ids_smem = (((size_t)m * K + 3) & ~size_t(3)) * 4 + (size_t)32 * kPlanMaxGroups * 4;
   pa.ids_cached = ids_smem <= kPlanIdsSmem ? 1 : 0;
@@ -2260,6 +2266,7 @@ milo_status moe_prefill_dev(milo_moe* moe, const void* x, int64_t m, int32_t x_d
     CUDA_TRY(cudaFuncSetAttribute(pf_img_t_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kImgTSmem));
     CUDA_TRY(set_smem(pf_gemm_kernel<2, 1>, PfCfg<2, 1>::kBytes));
     CUDA_TRY(set_smem(pf_gemm_kernel<1, 1>, PfCfg<1, 1>::kBytes));
+    CUDA_TRY(set_smem(pf_gemm_kernel<1, 2>, PfCfg<1, 2>::kBytes));
     configured_dev = dev;
   }
   for (int ph = 0; ph < 2; ++ph) {
@@ -2290,8 +2297,12 @@ milo_status moe_prefill_dev(milo_moe* moe, const void* x, int64_t m, int32_t x_d
                       false, a));
     } else {
       ProfScope ps(kProfGemv2, stream);
-      CUDA_TRY(launch(pf_gemm_kernel<1, 1>, dim3(sms), dim3(PfRoles<1, 1>::kThreads), PfCfg<1, 1>::kBytes, stream,
-                      false, a));
+      if (pa.ng2)
+        CUDA_TRY(launch(pf_gemm_kernel<1, 2>, dim3(sms), dim3(PfRoles<1, 2>::kThreads), PfCfg<1, 2>::kBytes, stream,
+                        false, a));
+      else
+        CUDA_TRY(launch(pf_gemm_kernel<1, 1>, dim3(sms), dim3(PfRoles<1, 1>::kThreads), PfCfg<1, 1>::kBytes, stream,
+                        false, a));
     }
   }
   const int64_t total = m * (d / 4);

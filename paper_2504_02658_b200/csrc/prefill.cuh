@@ -1422,6 +1422,7 @@ struct PfExpertStatic {
 struct PfPlanArgs {
   const int32_t* ids;             // m x K routing (-1 = unused)
   int32_t ids_cached;             // the ids fit the launch's dynamic shared memory (m K int32)
+  int32_t ng2;                    // phase-2 (w2) items cover two 128-column n-tiles (pf_gemm_kernel<1, 2>)
   long long* dbg;                 // optional: globaltimer after each planning step (debug)
   int64_t m;
   int32_t K, E, S, sms;
@@ -1573,7 +1574,7 @@ __global__ void __launch_bounds__(1024) moe_plan_kernel(PfPlanArgs a) {
         v[14 + (j == 2 ? 1 : 0)] += 1;                                                  // t problems per phase
       }
       v[16] = (s_shape[e][0][1] / kPfM) * tiles;
-      v[17] = (s_shape[e][2][1] / kPfM) * tiles;
+      v[17] = (s_shape[e][2][1] / (kPfM * (a.ng2 ? 2 : 1))) * tiles;
     }
     // warp inclusive scans, then the warps' totals
     __shared__ int32_t s_wtot[32][kQ];
