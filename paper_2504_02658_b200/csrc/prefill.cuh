@@ -43,11 +43,8 @@ namespace milo_dev {
 #ifndef PF_ISSUERS
 #define PF_ISSUERS 2  // MMA-issuing threads (experiments: 1)
 #endif
-#ifndef PF_KSPLIT
-#define PF_KSPLIT 0  // one-accumulator items with <= 64 tokens: k16 steps split over both issuers (measured ~5 us slower on the w2 phase)
-#endif
 #ifndef PF_MIN_AS
-#define PF_MIN_AS 6
+#define PF_MIN_AS 3
 #endif
 #ifndef PF_B_KB
 #define PF_B_KB 128  // activation / t image ring (KB)
@@ -95,7 +92,7 @@ struct PfRoles {
 template <int NMAT, int NG = 1>
 struct PfCfg {
   static constexpr int kPS = (NG == 2 || NMAT == 2) ? PF_PS2 : 10;  // packed-weight ring (HBM latency)
-  static constexpr int kStageCols = NG * NMAT * 32;  // TMEM columns of one A stage
+  static constexpr int kStageCols = NG * NMAT * 64;  // TMEM columns of one A stage (128 k)
   static constexpr int kASMax = 384 / kStageCols;    // A slots in TMEM (the accumulators take >= 128 columns)
   static constexpr int kBRegion = PF_B_KB * 1024;
   static constexpr int kBSMax = 16;                      // B slots = region / (ntok_max x 128), <= 16
@@ -322,8 +319,8 @@ __device__ __forceinline__ void pf_dequant_stage(const uint8_t* sP, int lane, co
       v1[4 * u + 2] = o[5];
       v1[4 * u + 3] = o[7];
     }
-    tmem_st16x256_x4(taddr + (uint32_t)(nm * 32), v0);
-    tmem_st16x256_x4(taddr + (16u << 16) + (uint32_t)(nm * 32), v1);
+    tmem_st16x256_x4(taddr + (uint32_t)(nm * 64), v0);  // A block nm: 64 columns (128 k)
+    tmem_st16x256_x4(taddr + (16u << 16) + (uint32_t)(nm * 64), v1);
   }
 }
 
@@ -362,7 +359,7 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
   // one accumulator per (n-tile, matrix); a single-accumulator kernel with
   // small token tiles splits each stage's k over two accumulators (one per
   // MMA issuer, summed by the epilogue)
-  const bool ksplit = PF_KSPLIT && PF_ISSUERS == 2 && NG * NMAT == 1 && a.ntok_max <= 64;
+  const bool ksplit = false;  // (a two-issuer k split of one-matrix items measured slower)
   const int acc_cols = (ksplit ? 2 : NG * NMAT) * mstride;
   // TMEM columns: accumulators (double-buffered when that leaves >= PF_MIN_AS
   // A slots), then the A slots.  The A ring's depth covers the dequant ->
@@ -389,7 +386,7 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
   if (threadIdx.x == 0) {
     for (int s = 0; s < PS; ++s) {
       mbar_init(&p_full[s], 1);
-      mbar_init(&p_empty[s], 2 * kPfGroupWarps);  // the two groups of the slot's two stages
+      mbar_init(&p_empty[s], kPfGroupWarps);  // the group of the slot's stage
     }
     for (int s = 0; s < AS; ++s) {
       mbar_init(&a_full[s], kPfGroupWarps);
@@ -435,8 +432,10 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
     }
   };
 
+  // stages: main stages of 128 k (P.k % 128 == 0), then 3 LoRC stages per 64-rank
+  // chunk per matrix (K = 64 each)
   auto item_stages = [&](const PfProblem& P) {
-    return P.k / kPfK + 3 * (P.rchunks[0] + (NMAT == 2 ? P.rchunks[1] : 0));
+    return P.k / (2 * kPfK) + 3 * (P.rchunks[0] + (NMAT == 2 ? P.rchunks[1] : 0));
   };
   // LoRC stage l (0-based after the main stages) -> matrix, chunk, V part, t part
   auto lorc_stage = [&](const PfProblem& P, int l, int& mat, int& ch, int& vpart, int& tpart) {
@@ -490,7 +489,7 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
           const int kp = (sp + nt * 13) % ks2;  // rotated k order per n-tile (spreads L2 hot spots)
           const uint8_t* src = P.w[mat] + ((int64_t)(2 * (NG * nt + ng) + sl) * kts + 4 * kp) * kTileBytes;
           bulk_g2s(sP + ((ng * NMAT + mat) * 2 + sl) * 4 * kTileBytes, src, 4 * kTileBytes, &p_full[ps]);
-          if (lane == 0) pf_trace(gs0 + 2 * sp, 0);
+          if (lane == 0) pf_trace(gs0 + sp, 0);
           PF_LAP(1);
           if (++ps == PS) {
             ps = 0;
@@ -515,18 +514,17 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
         int p, nt, tt;
         pf_item<NG>(a, item, p, nt, tt);
         const PfProblem P = a.problems[p];  // by value: fields live in registers
-        const int ks = P.k / kPfK, total = item_stages(P);
-        const uint32_t ib = (uint32_t)P.ntok * 128u;  // one token-tile image
+        const int ks = P.k / (2 * kPfK), total = item_stages(P);
+        const uint32_t ib = (uint32_t)P.ntok * 128u;  // one token-tile image (64 k)
         for (int st = 0; st < total; ++st, ++gs) {
-          if (st < ks && (st & 1)) continue;  // second stage of a pair: already in the slot
           ring_wait(&b_empty[bs], bph ^ 1);
           PF_LAP(0);
           uint8_t* sB = smem + CF::kOffB + bs * bslot;
           const uint8_t* src;
           uint32_t bytes = ib;
-          if (st < ks) {
-            const int kp = (st / 2 + nt * 13) % (ks / 2);  // same rotation as the weights
-            src = P.act + ((int64_t)tt * ks + 2 * kp) * ib;
+          if (st < ks) {  // the two adjacent 64-k images of the stage
+            const int kp = (st + nt * 13) % ks;  // same rotation as the weights
+            src = P.act + ((int64_t)tt * 2 * ks + 2 * kp) * ib;
             bytes = 2 * ib;
           } else {
             int mat, ch, vpart, tpart;
@@ -567,7 +565,7 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
       int p, nt, tt;
       pf_item<NG>(a, item, p, nt, tt);
       const PfProblem P = a.problems[p];  // by value: fields live in registers
-      const int ks = P.k / kPfK, total = item_stages(P);
+      const int ks = P.k / (2 * kPfK), total = item_stages(P);
       const DqConsts dq = make_dq_consts(P.mode);
       for (int st = 0; st < total; ++st, ++gs) {
         const bool mine = (gs % kPfDeqGroups) == grp;
@@ -582,13 +580,17 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
             ring_wait(&p_full[ps], pph);
             PF_LAP(1);
             if (gw == 0 && lane == 0) pf_trace(gs, 2);
-            // this stage's k-tiles: 2 (st & 1), + 1 of the slot's [nm][slab][4] runs
-            const uint8_t* sP = smem + CF::kOffP + ps * CF::kStageP + (sl * 4 + (st & 1) * 2) * kTileBytes;
+            // the slot's [nm][slab][4 k-tiles] runs: k-tiles 0, 1 -> A columns nm * 64 + [0, 32),
+            // k-tiles 2, 3 -> nm * 64 + [32, 64)
+            const uint8_t* sP = smem + CF::kOffP + ps * CF::kStageP + sl * 4 * kTileBytes;
             if (!(a.flags & 1)) {  // branch-free stage bodies per half (the units interleave)
-              if (ih == 0)
-                pf_dequant_stage<0, NG * NMAT>(sP, lane, dq, a_col + lane_q);
-              else
-                pf_dequant_stage<1, NG * NMAT>(sP, lane, dq, a_col + lane_q);
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                if (ih == 0)
+                  pf_dequant_stage<0, NG * NMAT>(sP + h * 2 * kTileBytes, lane, dq, a_col + lane_q + 32 * h);
+                else
+                  pf_dequant_stage<1, NG * NMAT>(sP + h * 2 * kTileBytes, lane, dq, a_col + lane_q + 32 * h);
+              }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&p_empty[ps]);
@@ -609,7 +611,7 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
                 v[4 * c + 2] = x.z;
                 v[4 * c + 3] = x.w;
               }
-              tmem_st32x32_x32(a_col + lane_q + (uint32_t)((ng * NMAT + mat) * 32), v);
+              tmem_st32x32_x32(a_col + lane_q + (uint32_t)((ng * NMAT + mat) * 64), v);
             }
           }
           PF_LAP(2);
@@ -619,7 +621,7 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
           if (lane == 0) mbar_arrive(&a_full[as]);
           if (gw == 0 && lane == 0) pf_trace(gs, 3);
         }
-        if (st < ks && (st & 1) && ++ps == PS) {  // a slot holds a stage pair
+        if (st < ks && ++ps == PS) {
           ps = 0;
           pph ^= 1;
         }
@@ -641,13 +643,12 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
       for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
         int p, nt, tt;
         pf_item<NG>(a, item, p, nt, tt);
-        const int total = item_stages(a.problems[p]), ks = a.problems[p].k / kPfK;
+        const int total = item_stages(a.problems[p]);
         for (int st = 0; st < total; ++st, ++gs) {
           ring_wait(&a_full[as], aph);
           PF_LAP(0);
           pf_trace(gs, 4);
-          const bool pair2 = st < ks && (st & 1);  // B slot of a pair: loaded with the first stage
-          if (!pair2) ring_wait(&b_full[bs], bph);
+          ring_wait(&b_full[bs], bph);
           PF_LAP(1);
           pf_trace(gs, 5);
           st_release_cta_shared(stages_ready, (uint32_t)(gs + 1));
@@ -656,7 +657,7 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
             as = 0;
             aph ^= 1;
           }
-          if (!(st < ks && !(st & 1)) && ++bs == BS) {  // slot done after its last stage
+          if (++bs == BS) {
             bs = 0;
             bph ^= 1;
           }
@@ -677,15 +678,15 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
       const uint64_t dB0 = pf_desc_sw128(smem_u32(smem + CF::kOffB));
       const bool mma_on = !(a.flags & 2);
       int as = 0, bs = 0;
-      bool slot_issued = false;
       int acc = 0, gs = 0;
       uint32_t acc_phase = 0;
       for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
         int p, nt, tt;
         pf_item<NG>(a, item, p, nt, tt);
         const PfProblem P = a.problems[p];  // by value: fields live in registers
-        const int ks = P.k / kPfK, total = item_stages(P);
+        const int ks = P.k / (2 * kPfK), total = item_stages(P);
         const uint32_t idesc = pf_idesc(P.ntok);
+        const uint32_t ib16 = ((uint32_t)P.ntok * 128u) >> 4;  // one image, in descriptor units
         ring_wait(&acc_empty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d0 = tmem + (uint32_t)(acc * acc_cols);  // accumulator buffer
@@ -701,9 +702,8 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
           // operand addresses: TMEM A slot, B descriptor of the slot (the 16-B
           // address field advances by 2 per 16-k step); everything unrolled
           const uint32_t aA = tmem + (uint32_t)(a_col0 + as * CF::kStageCols);
-          // B: the slot's first or second image (main-stage pair) or its t image
-          const bool pair2 = st < ks && (st & 1), pair1 = st < ks && !(st & 1);
-          const uint64_t dB = dB0 + (uint64_t)((uint32_t)(bs * bslot + (pair2 ? P.ntok * 128 : 0)) >> 4);
+          // B: the slot's two 64-k images (main stage) or its t image
+          const uint64_t dB = dB0 + (uint64_t)((uint32_t)(bs * bslot) >> 4);
           bool issued = false;
           if (!idle && mma_on) {
             uint32_t acc0 = 1u;
@@ -714,38 +714,32 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
               int ch, vpart, tpart;
               lorc_stage(P, st - ks, lmat, ch, vpart, tpart);
             }
-            if (NG * NMAT == 1 && ksplit) {  // k16 steps issuer, issuer + 2 into accumulator issuer
-              const uint32_t dI = d0 + (uint32_t)(issuer * mstride);
-              pf_mma_ts_w(dI, aA + (uint32_t)(issuer * 8), dB + 2 * issuer, idesc, acc0);
-              pf_mma_ts_w(dI, aA + (uint32_t)(issuer * 8 + 16), dB + 2 * issuer + 4, idesc, 1u);
-              issued = true;
-            } else {
 #pragma unroll
-              for (int nm = 0; nm < NG * NMAT; ++nm) {  // A block (ng * NMAT + mat) = accumulator nm
-                if (PF_ISSUERS == 2 && nm % 2 != issuer) continue;
-                if (lmat >= 0 && nm % NMAT != lmat) continue;  // LoRC: that matrix's blocks only
+            for (int nm = 0; nm < NG * NMAT; ++nm) {  // A block (ng * NMAT + mat) = accumulator nm
+              if (PF_ISSUERS == 2 && nm % 2 != issuer) continue;
+              if (lmat >= 0 && nm % NMAT != lmat) continue;  // LoRC: that matrix's blocks only
+              const uint32_t dN = d0 + (uint32_t)(nm * mstride), aN = aA + (uint32_t)(nm * 64);
+              if (st < ks) {  // 8 k16 steps: image 0 then image 1 of the slot
 #pragma unroll
-                for (int k16 = 0; k16 < kPfK / 16; ++k16)
-                  pf_mma_ts_w(d0 + (uint32_t)(nm * mstride), aA + (uint32_t)(nm * 32 + k16 * 8), dB + 2 * k16, idesc,
+                for (int k16 = 0; k16 < 8; ++k16)
+                  pf_mma_ts_w(dN, aN + (uint32_t)(k16 * 8), dB + (k16 < 4 ? 2 * k16 : ib16 + 2 * (k16 - 4)), idesc,
                               k16 > 0 ? 1u : acc0);
-                issued = true;
+              } else {  // LoRC: 4 k16 steps over a 64-rank chunk
+#pragma unroll
+                for (int k16 = 0; k16 < 4; ++k16) pf_mma_ts_w(dN, aN + (uint32_t)(k16 * 8), dB + 2 * k16, idesc, 1u);
               }
+              issued = true;
             }
           }
           PF_LAP(1);
-          if (issued)
+          if (issued) {
             pf_commit_w(&a_empty[as]);
-          else
+            pf_commit_w(&b_empty[bs]);
+          } else {
             mbar_arrive_w(&a_empty[as]);
-          slot_issued |= issued;
-          if (!pair1) {  // the B slot's last stage: release it (a commit covers both stages of a pair)
-            if (slot_issued)
-              pf_commit_w(&b_empty[bs]);
-            else
-              mbar_arrive_w(&b_empty[bs]);
-            slot_issued = false;
-            if (++bs == BS) bs = 0;
+            mbar_arrive_w(&b_empty[bs]);
           }
+          if (++bs == BS) bs = 0;
           PF_LAP(2);
           if (issuer == 0 && lane == 0) pf_trace(gs, 6);
           if (++as == AS) as = 0;
