@@ -367,6 +367,9 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
   const int nacc = (acc_cols <= 128 && (512 - 2 * acc_cols) / CF::kStageCols >= PF_MIN_AS) ? 2 : 1;
   const int a_col0 = nacc * acc_cols;
   const int AS = min(CF::kASMax, (512 - a_col0) / CF::kStageCols);
+  // parity waits on the A ring are unambiguous only with at least as many slots as
+  // dequant groups (a smaller ring would deadlock): fail loudly instead
+  if (AS < kPfDeqGroups) __trap();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-B aligned base (SW128 atoms); pointer arithmetic keeps the shared address space
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
