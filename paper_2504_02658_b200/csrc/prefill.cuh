@@ -44,7 +44,7 @@ namespace milo_dev {
 #define PF_ISSUERS 2  // MMA-issuing threads (experiments: 1)
 #endif
 #ifndef PF_MIN_AS
-#define PF_MIN_AS 3
+#define PF_MIN_AS 3  // A slots below which the accumulators are single-buffered
 #endif
 #ifndef PF_B_KB
 #define PF_B_KB 128  // activation / t image ring (KB)
@@ -362,8 +362,8 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
   const bool ksplit = false;  // (a two-issuer k split of one-matrix items measured slower)
   const int acc_cols = (ksplit ? 2 : NG * NMAT) * mstride;
   // TMEM columns: accumulators (double-buffered when that leaves >= PF_MIN_AS
-  // A slots), then the A slots.  The A ring's depth covers the dequant ->
-  // MMA -> release loop latency (~4 stages measured at 64 tokens).
+  // A slots), then the A slots (128-k stages: 3 slots for two matrices at 64
+  // tokens with one accumulator buffer; double buffering with 2 measured equal).
   const int nacc = (acc_cols <= 128 && (512 - 2 * acc_cols) / CF::kStageCols >= PF_MIN_AS) ? 2 : 1;
   const int a_col0 = nacc * acc_cols;
   const int AS = min(CF::kASMax, (512 - a_col0) / CF::kStageCols);
