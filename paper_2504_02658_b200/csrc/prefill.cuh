@@ -43,6 +43,16 @@ namespace milo_dev {
 #ifndef PF_ISSUERS
 #define PF_ISSUERS 2  // MMA-issuing threads (experiments: 1)
 #endif
+#ifndef PF_VPREFETCH
+#define PF_VPREFETCH 0  // 1: packed producer prefetches the item's V^T images to L2 at item start
+#endif
+#ifndef PF_LMERGE_MIN
+// token tiles >= this run one merged LoRC stage per chunk (else 3).  Off by default:
+// merged (32) measured DeepSeek batch 256 -30 us but Arctic +300 us, and with it
+// compiled out the kernel is ~5% fewer instructions, which alone took Arctic phase 2
+// 906 -> 822 us (the roles' loops share the SM's instruction cache; K3)
+#define PF_LMERGE_MIN (1 << 20)
+#endif
 #ifndef PF_MIN_AS
 #define PF_MIN_AS 3  // A slots below which the accumulators are single-buffered
 #endif
@@ -435,22 +445,28 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
     }
   };
 
-  // stages: main stages of 128 k (P.k % 128 == 0), then 3 LoRC stages per 64-rank
-  // chunk per matrix (K = 64 each)
+  // stages: main stages of 128 k (P.k % 128 == 0), then the LoRC stages per 64-rank
+  // chunk per matrix.  Merged (token tiles >= PF_LMERGE_MIN): one stage, V^T hi | lo
+  // in the A slot, t hi | lo in the B slot, three MMA passes (hi.hi + hi.lo + lo.hi).
+  // Else three stages of one pass each (V_hi.t_hi, V_hi.t_lo, V_lo.t_hi): for small
+  // tiles the stage is latency-bound and splitting it spreads it over both groups.
+  auto lmerged = [&](const PfProblem& P) { return PF_LMERGE_MIN <= kPfN && P.ntok >= PF_LMERGE_MIN; };
   auto item_stages = [&](const PfProblem& P) {
-    return P.k / (2 * kPfK) + 3 * (P.rchunks[0] + (NMAT == 2 ? P.rchunks[1] : 0));
+    return P.k / (2 * kPfK) + (lmerged(P) ? 1 : 3) * (P.rchunks[0] + (NMAT == 2 ? P.rchunks[1] : 0));
   };
   // LoRC stage l (0-based after the main stages) -> matrix, chunk, V part, t part
+  // (part -1: both, merged stage)
   auto lorc_stage = [&](const PfProblem& P, int l, int& mat, int& ch, int& vpart, int& tpart) {
+    const int per = lmerged(P) ? 1 : 3;
     mat = 0;
-    if (l >= 3 * P.rchunks[0]) {
-      l -= 3 * P.rchunks[0];
+    if (l >= per * P.rchunks[0]) {
+      l -= per * P.rchunks[0];
       mat = 1;
     }
-    ch = l / 3;
-    const int part = l % 3;  // 0: V_hi.t_hi, 1: V_hi.t_lo, 2: V_lo.t_hi
-    vpart = part == 2 ? 1 : 0;
-    tpart = part == 1 ? 1 : 0;
+    ch = l / per;
+    const int part = l % per;  // 0: V_hi.t_hi, 1: V_hi.t_lo, 2: V_lo.t_hi
+    vpart = per == 1 ? -1 : (part == 2 ? 1 : 0);
+    tpart = per == 1 ? -1 : (part == 1 ? 1 : 0);
   };
 
 #if PF_PROF  // per-role cycle split, CTA 0 -> dbg trace row kPfTraceStages - 1 - role
@@ -483,6 +499,13 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
         pf_item<NG>(a, item, p, nt, tt);
         const PfProblem P = a.problems[p];  // by value: fields live in registers
         const int ks2 = P.k / (2 * kPfK), kts = P.k / kTileK;
+        // the item's V^T images (its LoRC stages come last) -> L2 now: one contiguous
+        // run of rchunks x (hi, lo) images per (n-tile, matrix)
+        if (PF_VPREFETCH && lane < NG * NMAT && P.rchunks[lane % NMAT] > 0) {
+          const int pm = lane % NMAT, png = lane / NMAT;
+          const uint32_t run = (uint32_t)P.rchunks[pm] * 2u * kPfImg;
+          prefetch_l2(P.vimg[pm] + (int64_t)(NG * nt + png) * run, run);
+        }
         for (int sp = 0; sp < ks2; ++sp) {
           ring_wait(&p_empty[ps], pph ^ 1);
           PF_LAP(0);
@@ -529,10 +552,11 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
             const int kp = (st + nt * 13) % ks;  // same rotation as the weights
             src = P.act + ((int64_t)tt * 2 * ks + 2 * kp) * ib;
             bytes = 2 * ib;
-          } else {
+          } else {  // t hi / lo image of the chunk (merged: both, adjacent)
             int mat, ch, vpart, tpart;
             lorc_stage(P, st - ks, mat, ch, vpart, tpart);
-            src = P.timg[mat] + (((int64_t)tt * P.rchunks[mat] + ch) * 2 + tpart) * ib;
+            src = P.timg[mat] + (((int64_t)tt * P.rchunks[mat] + ch) * 2 + (tpart > 0 ? 1 : 0)) * ib;
+            bytes = tpart < 0 ? 2 * ib : ib;
           }
           mbar_arrive_expect_tx(&b_full[bs], bytes);
           bulk_g2s(sB, src, bytes, &b_full[bs]);
@@ -598,11 +622,12 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
             __syncwarp();
             if (lane == 0) mbar_arrive(&p_empty[ps]);
           } else {
-            int mat, ch, vpart, tpart;
-            lorc_stage(P, st - ks, mat, ch, vpart, tpart);
-            const int row = 32 * Q + lane;
+            int mat, ch, vp, tp;
+            lorc_stage(P, st - ks, mat, ch, vp, tp);
+            const int row = 32 * Q + lane, nv = vp < 0 ? 2 : 1;
 #pragma unroll 1
-            for (int ng = 0; ng < NG; ++ng) {
+            for (int ngv = 0; ngv < nv * NG; ++ngv) {  // (n-tile, V part): merged V hi -> columns [0, 32), lo -> [32, 64)
+              const int ng = ngv / nv, vpart = vp < 0 ? (ngv & 1) : vp;
               const uint8_t* img =
                   P.vimg[mat] + (((int64_t)(NG * nt + ng) * P.rchunks[mat] + ch) * 2 + vpart) * kPfImg + row * 128;
               uint32_t v[32];
@@ -614,7 +639,7 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
                 v[4 * c + 2] = x.z;
                 v[4 * c + 3] = x.w;
               }
-              tmem_st32x32_x32(a_col + lane_q + (uint32_t)((ng * NMAT + mat) * 64), v);
+              tmem_st32x32_x32(a_col + lane_q + (uint32_t)((ng * NMAT + mat) * 64 + (vp < 0 ? 32 * vpart : 0)), v);
             }
           }
           PF_LAP(2);
@@ -710,12 +735,12 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
           bool issued = false;
           if (!idle && mma_on) {
             uint32_t acc0 = 1u;
-            int lmat = -1;  // LoRC stage: its matrix
+            int lmat = -1, ltp = -1;  // LoRC stage: its matrix, t part (-1 merged)
             if (st < ks) {
               acc0 = st > 0 ? 1u : 0u;
             } else {
-              int ch, vpart, tpart;
-              lorc_stage(P, st - ks, lmat, ch, vpart, tpart);
+              int ch, vp;
+              lorc_stage(P, st - ks, lmat, ch, vp, ltp);
             }
 #pragma unroll
             for (int nm = 0; nm < NG * NMAT; ++nm) {  // A block (ng * NMAT + mat) = accumulator nm
@@ -727,9 +752,16 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
                 for (int k16 = 0; k16 < 8; ++k16)
                   pf_mma_ts_w(dN, aN + (uint32_t)(k16 * 8), dB + (k16 < 4 ? 2 * k16 : ib16 + 2 * (k16 - 4)), idesc,
                               k16 > 0 ? 1u : acc0);
-              } else {  // LoRC: 4 k16 steps over a 64-rank chunk
-#pragma unroll
+              } else if (ltp >= 0) {  // LoRC part, 64 ranks: 4 k16 steps (t part ltp)
+#pragma unroll 1
                 for (int k16 = 0; k16 < 4; ++k16) pf_mma_ts_w(dN, aN + (uint32_t)(k16 * 8), dB + 2 * k16, idesc, 1u);
+              } else {  // merged LoRC, 64 ranks: V_hi.t_hi + V_hi.t_lo + V_lo.t_hi
+#pragma unroll 1
+                for (int k16 = 0; k16 < 4; ++k16) {
+                  pf_mma_ts_w(dN, aN + (uint32_t)(k16 * 8), dB + 2 * k16, idesc, 1u);
+                  pf_mma_ts_w(dN, aN + (uint32_t)(k16 * 8), dB + ib16 + 2 * k16, idesc, 1u);
+                  pf_mma_ts_w(dN, aN + (uint32_t)(32 + k16 * 8), dB + 2 * k16, idesc, 1u);
+                }
               }
               issued = true;
             }
