@@ -46,6 +46,9 @@ namespace milo_dev {
 #ifndef PF_VPREFETCH
 #define PF_VPREFETCH 0  // 1: packed producer prefetches the item's V^T images to L2 at item start
 #endif
+#ifndef PF_DQ_ROLLED
+#define PF_DQ_ROLLED 1  // the dequant warps' two 64-k halves per stage run one loop body (0: unrolled)
+#endif
 #ifndef PF_LMERGE_MIN
 // token tiles >= this run one merged LoRC stage per chunk (else 3).  Off by default:
 // merged (32) measured DeepSeek batch 256 -30 us but Arctic +300 us, and with it
@@ -337,8 +340,8 @@ __device__ __forceinline__ void pf_dequant_stage(const uint8_t* sP, int lane, co
 // ---------------------------------------------------------------- the kernel
 // Persistent: CTA c handles items c, c + grid, ...  Three rings decouple the
 // roles: packed weights (deep, HBM latency), dequantized A, activation images.
-// Every role walks the same stage sequence: per item, k / 64 main stages then
-// 3 LoRC stages per 64-rank chunk per matrix.
+// Every role walks the same stage sequence: per item, k / 128 main stages then
+// the LoRC stages of each 64-rank chunk per matrix.
 #ifndef PF_SPIN_WAITS
 #define PF_SPIN_WAITS 0  // experiments: all ring waits spin on test_wait instead of try_wait
 #endif
@@ -611,7 +614,11 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
             // k-tiles 2, 3 -> nm * 64 + [32, 64)
             const uint8_t* sP = smem + CF::kOffP + ps * CF::kStageP + sl * 4 * kTileBytes;
             if (!(a.flags & 1)) {  // branch-free stage bodies per half (the units interleave)
+#if PF_DQ_ROLLED
+#pragma unroll 1
+#else
 #pragma unroll
+#endif
               for (int h = 0; h < 2; ++h) {
                 if (ih == 0)
                   pf_dequant_stage<0, NG * NMAT>(sP + h * 2 * kTileBytes, lane, dq, a_col + lane_q + 32 * h);
