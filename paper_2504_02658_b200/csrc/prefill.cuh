@@ -49,6 +49,9 @@ namespace milo_dev {
 #ifndef PF_DQ_ROLLED
 #define PF_DQ_ROLLED 1  // the dequant warps' two 64-k halves per stage run one loop body (0: unrolled)
 #endif
+#ifndef PF_ISSUE_ROLLED
+#define PF_ISSUE_ROLLED 0  // 1: the issuers' accumulator loop is not unrolled (smaller kernel)
+#endif
 #ifndef PF_LMERGE_MIN
 // token tiles >= this run one merged LoRC stage per chunk (else 3).  Off by default:
 // merged (32) measured DeepSeek batch 256 -30 us but Arctic +300 us, and with it
@@ -749,7 +752,11 @@ __global__ void __launch_bounds__(PfRoles<NMAT, NG>::kThreads, 1) pf_gemm_kernel
               int ch, vp;
               lorc_stage(P, st - ks, lmat, ch, vp, ltp);
             }
+#if PF_ISSUE_ROLLED
+#pragma unroll 1
+#else
 #pragma unroll
+#endif
             for (int nm = 0; nm < NG * NMAT; ++nm) {  // A block (ng * NMAT + mat) = accumulator nm
               if (PF_ISSUERS == 2 && nm % 2 != issuer) continue;
               if (lmat >= 0 && nm % NMAT != lmat) continue;  // LoRC: that matrix's blocks only
